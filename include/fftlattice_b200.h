@@ -1,0 +1,91 @@
+/* fftlattice_b200.h -- C ABI of the B200-native fftlattice pricing library.
+ *
+ * Drop-in boundary for the reference package `fftlattice` (pure Python; its
+ * pricing entry points are plain functions, no plugin registry).  Each entry
+ * point below replaces the reference function named beside it; the reference
+ * binding a maintainer would add is the ctypes stub in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain C types only: host pointers to struct-of-arrays option inputs,
+ *    host pointers for outputs, an optional cudaStream_t passed as void*.
+ *  - Returns 0 on success, nonzero on a launch / configuration error
+ *    (message via fl_last_error()).  Per-option pricing failures are NOT call
+ *    errors: they are reported in status[i] (see paper_2303_02317_b200/csrc/
+ *    fl_status.h: (class << 8) | detail, classes mirroring model.py:44-97).
+ *  - Boundary records are optional (pass NULL); at most bnd_cap records per
+ *    option are stored row-major at [i * bnd_cap], bnd_count[i] holds the true
+ *    count.  Columns use the reference sentinel NO_GREEN = INT64_MIN.
+ *  - All entry points synchronize the given stream before returning, except
+ *    fl_batch_run, which only enqueues.
+ *  - Reentrant across devices; one library context per device.
+ */
+#ifndef FFTLATTICE_B200_H
+#define FFTLATTICE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_KIND_EURO 0 /* binomial European call  */
+#define FL_KIND_CALL 1 /* binomial American call  */
+#define FL_KIND_PUT 2  /* BSM American put        */
+
+#define FL_METHOD_FAST 0     /* fast_european / fast_american_call / fast_put_bsm        */
+#define FL_METHOD_BASELINE 1 /* baseline_european / baseline_american_call / baseline_put_fd */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int fl_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* fl_last_error(void);
+
+/* Price a batch of options of mixed kinds.
+ *   kind[i] in {FL_KIND_*}; S,K,R,Y,V,E as in fftlattice.OptionSpec
+ *   (spot, strike, rate, dividend_yield, volatility, days_to_expiry; Y is
+ *   validated but unused for puts, as in the reference); T = steps.
+ *   lam: BSM grid ratio (bsm.py:66 default 0.4); call_cutoff / put_cutoff:
+ *   the reference base_cutoff arguments (defaults 256 / 128).
+ * Replaces, per option:
+ *   FL_KIND_EURO + FAST      binomial.py:161  fast_european
+ *   FL_KIND_EURO + BASELINE  binomial.py:80   baseline_european
+ *   FL_KIND_CALL + FAST      american.py:428  fast_american_call
+ *   FL_KIND_CALL + BASELINE  binomial.py:94   baseline_american_call
+ *   FL_KIND_PUT  + FAST      bsm.py:585       fast_put_bsm
+ *   FL_KIND_PUT  + BASELINE  bsm.py:273       baseline_put_fd
+ * and cli.py:753-794 (_batch_row_price) for a whole portfolio at once. */
+int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+                   const double* Y, const double* V, const double* E, const int64_t* T, double lam,
+                   int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
+                   int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
+
+/* Device-resident batches (for repeated pricing and benchmarking): prepare
+ * does the host-side parameter derivation and the H2D copy once; run only
+ * enqueues the kernels on `stream` (inputs and outputs stay in HBM); fetch
+ * copies results back and synchronizes. */
+typedef struct fl_batch fl_batch;
+int fl_batch_prepare(fl_batch** out, int64_t n, const int8_t* kind, const double* S, const double* K,
+                     const double* R, const double* Y, const double* V, const double* E, const int64_t* T,
+                     double lam, int64_t call_cutoff, int64_t put_cutoff, int method, int32_t bnd_cap,
+                     void* stream);
+int fl_batch_run(fl_batch* b, void* stream);
+int fl_batch_fetch(fl_batch* b, double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols,
+                   int32_t* bnd_count, void* stream);
+/* Number of kernel launches one fl_batch_run enqueues. */
+int fl_batch_launches(const fl_batch* b);
+void fl_batch_free(fl_batch* b);
+
+/* Batched valid-mode composed-stencil correlation (fft.py:263 apply_linear_steps,
+ * american.py:180 / bsm.py:384 _valid_corr), on host buffers:
+ *   y[k] = sum_{r=0}^{h*(taps-1)} W_h[r] x[k+r],  k = 0 .. L - h*(taps-1) - 1,
+ * W_h = coefficients of (c0 + c1 z [+ c2 z^2])^h (fft.py:203 kernel_power).
+ * taps in {2,3}; coefficients must be nonnegative (lattice / FD weights). */
+int fl_apply_linear_steps(const double* x, int64_t L, int taps, double c0, double c1, double c2, int64_t h,
+                          double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFTLATTICE_B200_H */

@@ -1,0 +1,270 @@
+"""ctypes binding of ``libfftlattice_b200.so`` (the C ABI in include/fftlattice_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+usable, every pricing call raises.  Batched entry points take and return numpy
+arrays (host memory); device buffers are owned by the library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .model import (
+    DomainError,
+    GeometryError,
+    NumericalIntegrityError,
+    PricingError,
+    StabilityError,
+    ValidationError,
+)
+
+__all__ = [
+    "KIND_EURO", "KIND_CALL", "KIND_PUT", "METHOD_FAST", "METHOD_BASELINE",
+    "lib", "lib_path", "BatchResult", "price_batch", "DeviceBatch", "apply_linear_steps",
+    "status_error", "EXPORTED_SYMBOLS", "NativeLibraryError",
+]
+
+KIND_EURO, KIND_CALL, KIND_PUT = 0, 1, 2
+METHOD_FAST, METHOD_BASELINE = 0, 1
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_NAME = "libfftlattice_b200.so"
+_lock = threading.Lock()
+_lib = None
+
+#: Every symbol include/fftlattice_b200.h declares.
+EXPORTED_SYMBOLS = (
+    "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
+    "fl_batch_fetch", "fl_batch_launches", "fl_batch_free", "fl_apply_linear_steps",
+)
+
+
+class NativeLibraryError(RuntimeError):
+    """The CUDA library is missing or a library call failed (not a pricing error)."""
+
+
+def lib_path() -> str:
+    return os.path.join(HERE, _LIB_NAME)
+
+
+def lib():
+    """Load the CUDA library (raises NativeLibraryError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = lib_path()
+        if not os.path.exists(path):
+            raise NativeLibraryError(
+                f"{path} is not built; run `python -m paper_2303_02317_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(path)
+        P, i64, i32, d, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int
+        L.fl_version.restype = c_int
+        L.fl_last_error.restype = ctypes.c_char_p
+        L.fl_price_batch.argtypes = [i64, P, P, P, P, P, P, P, P, d, i64, i64, c_int, P, P, P, P, P, i32, P]
+        L.fl_price_batch.restype = c_int
+        L.fl_batch_prepare.argtypes = [ctypes.POINTER(P), i64, P, P, P, P, P, P, P, P, d, i64, i64, c_int, i32, P]
+        L.fl_batch_prepare.restype = c_int
+        L.fl_batch_run.argtypes = [P, P]
+        L.fl_batch_run.restype = c_int
+        L.fl_batch_fetch.argtypes = [P, P, P, P, P, P, P]
+        L.fl_batch_fetch.restype = c_int
+        L.fl_batch_launches.argtypes = [P]
+        L.fl_batch_launches.restype = c_int
+        L.fl_batch_free.argtypes = [P]
+        L.fl_batch_free.restype = None
+        L.fl_apply_linear_steps.argtypes = [P, i64, c_int, d, d, d, i64, P, P]
+        L.fl_apply_linear_steps.restype = c_int
+        _lib = L
+        return L
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise NativeLibraryError(lib().fl_last_error().decode(errors="replace"))
+
+
+def _f64(a, n):
+    out = np.ascontiguousarray(np.broadcast_to(np.asarray(a, dtype=np.float64), (n,)))
+    return out
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# --------------------------------------------------------------------------
+# status codes (csrc/fl_status.h)
+
+_FIELDS = {1: "spot", 2: "strike", 3: "rate", 4: "dividend_yield", 5: "volatility",
+           6: "days_to_expiry", 7: "steps", 8: "prob_up", 9: "lam", 10: "base_cutoff"}
+_FIELD_MSG = {
+    "spot": "spot must be positive and finite",
+    "strike": "strike must be nonnegative and finite",
+    "rate": "rate must be nonnegative and finite",
+    "dividend_yield": "dividend_yield must be nonnegative and finite",
+    "volatility": "volatility must be positive",
+    "days_to_expiry": "days_to_expiry must be positive",
+    "steps": "steps must be >= 1",
+    "prob_up": "prob_up out of (0, 1): the carry outruns one lattice step; "
+               "increase steps or volatility",
+    "lam": "lambda must be positive",
+    "base_cutoff": "base_cutoff must be >= 1",
+}
+_WEIGHTS = {1: ("coef_mid", "centre weight is negative; choose a smaller lambda"),
+            2: ("coef_up", "upper weight is negative; increase steps or adjust lambda"),
+            3: ("coef_down", "lower weight is negative; increase steps or adjust lambda")}
+
+
+def status_error(code: int) -> Exception | None:
+    """Exception instance equivalent to the reference's for a status code."""
+    code = int(code)
+    if code == 0:
+        return None
+    cls, det = code & 0xFF00, code & 0xFF
+    if cls == 0x100:
+        f = _FIELDS.get(det, "unknown")
+        return ValidationError(f, _FIELD_MSG.get(f, f))
+    if cls == 0x200:
+        w, msg = _WEIGHTS.get(det, ("unknown", "negative weight"))
+        return StabilityError(w, msg)
+    if cls == 0x300:
+        if det == 1:
+            return DomainError("spot lies too many grid nodes from the strike")
+        return DomainError("put grid requires a positive strike")
+    if cls == 0x400:
+        return GeometryError(f"decomposition failed to tile its region (site {det})")
+    if cls == 0x500:
+        return NumericalIntegrityError("numerical self-check failed")
+    if cls == 0x600:
+        return ValueError("math domain error")
+    return PricingError(f"unsupported on this GPU build (status {code:#x})")
+
+
+# --------------------------------------------------------------------------
+# batched pricing
+
+
+class BatchResult:
+    """Per-option outputs of a batched call (numpy, host)."""
+
+    def __init__(self, price, status, bt, bc, bcount, cap):
+        self.price, self.status = price, status
+        self.bnd_times, self.bnd_cols, self.bnd_count, self.cap = bt, bc, bcount, cap
+
+    def boundary(self, i: int):
+        c = int(self.bnd_count[i])
+        if c > self.cap:
+            raise IndexError("boundary record truncated; re-run with a larger bnd_cap")
+        return self.bnd_times[i, :c].copy(), self.bnd_cols[i, :c].copy()
+
+
+def _inputs(kind, S, K, R, Y, V, E, T):
+    n = int(np.asarray(S).shape[0]) if np.ndim(S) else 1
+    k = np.ascontiguousarray(np.broadcast_to(np.asarray(kind, dtype=np.int8), (n,)))
+    t = np.ascontiguousarray(np.broadcast_to(np.asarray(T, dtype=np.int64), (n,)))
+    return n, k, _f64(S, n), _f64(K, n), _f64(R, n), _f64(Y, n), _f64(V, n), _f64(E, n), t
+
+
+def price_batch(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128,
+                method=METHOD_FAST, bnd_cap=0, stream=None) -> BatchResult:
+    """Price a batch through ``fl_price_batch`` (host arrays in and out)."""
+    n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
+    price = np.empty(n)
+    status = np.empty(n, dtype=np.int32)
+    cap = int(bnd_cap)
+    bt = np.empty((n, max(cap, 1)), dtype=np.int64)
+    bc = np.empty((n, max(cap, 1)), dtype=np.int64)
+    bcount = np.zeros(n, dtype=np.int32)
+    _check(lib().fl_price_batch(
+        n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), float(lam),
+        int(call_cutoff), int(put_cutoff), int(method), _ptr(price), _ptr(status),
+        _ptr(bt) if cap else None, _ptr(bc) if cap else None, _ptr(bcount) if cap else None,
+        cap, ctypes.c_void_p(stream) if stream else None))
+    return BatchResult(price, status, bt, bc, bcount, cap)
+
+
+class DeviceBatch:
+    """A prepared, device-resident batch (``fl_batch_prepare`` / run / fetch)."""
+
+    def __init__(self, kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128,
+                 method=METHOD_FAST, bnd_cap=0, stream=None):
+        n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
+        self.n, self.cap = n, int(bnd_cap)
+        h = ctypes.c_void_p()
+        _check(lib().fl_batch_prepare(
+            ctypes.byref(h), n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T),
+            float(lam), int(call_cutoff), int(put_cutoff), int(method), self.cap,
+            ctypes.c_void_p(stream) if stream else None))
+        self._h = h
+
+    def run(self, stream=None) -> None:
+        _check(lib().fl_batch_run(self._h, ctypes.c_void_p(stream) if stream else None))
+
+    def launches(self) -> int:
+        return int(lib().fl_batch_launches(self._h))
+
+    def fetch(self, stream=None) -> BatchResult:
+        n, cap = self.n, self.cap
+        price = np.empty(n)
+        status = np.empty(n, dtype=np.int32)
+        bt = np.empty((n, max(cap, 1)), dtype=np.int64)
+        bc = np.empty((n, max(cap, 1)), dtype=np.int64)
+        bcount = np.zeros(n, dtype=np.int32)
+        _check(lib().fl_batch_fetch(self._h, _ptr(price), _ptr(status), _ptr(bt) if cap else None,
+                                    _ptr(bc) if cap else None, _ptr(bcount) if cap else None,
+                                    ctypes.c_void_p(stream) if stream else None))
+        return BatchResult(price, status, bt, bc, bcount, cap)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().fl_batch_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def apply_linear_steps(x: np.ndarray, taps: int, c0: float, c1: float, c2: float, h: int) -> np.ndarray:
+    """Valid-mode correlation of x with the h-th composed stencil, on device."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty(x.shape[0] - h * (taps - 1))
+    _check(lib().fl_apply_linear_steps(_ptr(x), x.shape[0], int(taps), float(c0), float(c1),
+                                       float(c2), int(h), _ptr(out), None))
+    return out
+
+
+def price_batch_full(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128,
+                     method=METHOD_FAST, bnd_cap=64, stream=None) -> BatchResult:
+    """``price_batch`` with complete boundary records: options whose record
+    exceeded ``bnd_cap`` are re-run with a capacity that fits them."""
+    res = price_batch(kind, S, K, R, Y, V, E, T, lam=lam, call_cutoff=call_cutoff, put_cutoff=put_cutoff,
+                      method=method, bnd_cap=bnd_cap, stream=stream)
+    over = np.nonzero(res.bnd_count > res.cap)[0]
+    if over.size == 0:
+        return res
+    n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
+    cap2 = int(res.bnd_count[over].max())
+    sub = price_batch(k[over], S[over], K[over], R[over], Y[over], V[over], E[over], T[over], lam=lam,
+                      call_cutoff=call_cutoff, put_cutoff=put_cutoff, method=method, bnd_cap=cap2,
+                      stream=stream)
+    bt = np.full((n, cap2), 0, dtype=np.int64)
+    bc = np.full((n, cap2), 0, dtype=np.int64)
+    c0 = res.cap
+    bt[:, :c0] = res.bnd_times[:, :c0]
+    bc[:, :c0] = res.bnd_cols[:, :c0]
+    bt[over] = sub.bnd_times
+    bc[over] = sub.bnd_cols
+    price, status, bcount = res.price.copy(), res.status.copy(), res.bnd_count.copy()
+    price[over], status[over], bcount[over] = sub.price, sub.status, sub.bnd_count
+    return BatchResult(price, status, bt, bc, bcount, cap2)

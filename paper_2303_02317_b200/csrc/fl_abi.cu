@@ -1,0 +1,481 @@
+// fl_abi.cu -- the C ABI (include/fftlattice_b200.h): host-side parameter
+// derivation (host_params.h), device buffer management, kernel dispatch and
+// result merging.  The reference's pricing entry points (binomial.py:80/161,
+// american.py:428, bsm.py:273/585) map onto fl_price_batch per option kind.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fftlattice_b200.h"
+#include "fl_kernels.h"
+#include "host_params.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const std::string& msg) {
+  g_last_error = msg;
+  return 1;
+}
+
+#define FL_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t sz = want < 256 ? 256 : want;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e == cudaSuccess) bytes = sz;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostPinned {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+std::mutex g_init_mu;
+bool g_tw_ready[64] = {false};
+
+cudaError_t ensure_device_init(int dev, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!g_tw_ready[dev]) {
+    fl::init_twiddles(stream);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    g_tw_ready[dev] = true;
+  }
+  return cudaSuccess;
+}
+
+inline double cost_put(int64_t n) {
+  const double l = std::log2((double)std::max<int64_t>(n, 2));
+  return 24.8 * (double)n * l * l;
+}
+inline double cost_call(int64_t n) {
+  const double l = std::log2((double)std::max<int64_t>(n, 2));
+  return 10.0 * (double)n * l * l;
+}
+
+void sort_by_cost(std::vector<int32_t>& ord, const std::vector<double>& cost) {
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+}
+
+}  // namespace
+
+struct fl_batch {
+  int dev = 0;
+  int64_t n = 0;
+  int method = FL_METHOD_FAST;
+  int32_t cap = 0;
+  int launches = 0;
+  // host-side
+  std::vector<int8_t> kind;
+  std::vector<int32_t> hstatus;  // host-decided status (errors)
+  std::vector<int32_t> mode;
+  std::vector<fl::PutParams> put;
+  std::vector<fl::CallParams> call;
+  std::vector<fl::EuroParams> euro;
+  std::vector<double> cost;
+  std::vector<int32_t> o_put_fast, o_put_base, o_call_fast, o_call_base, o_euro_fast, o_euro_base;
+  // device-side
+  DevBuf d_put, d_call, d_euro, d_orders, d_price, d_status, d_bt, d_bc, d_bcount, d_counter;
+  DevBuf d_ws_put, d_ws_call, d_ws_base;
+  int64_t ws_put_stride = 0, ws_call_stride = 0, ws_base_stride = 0;
+  int grid_put = 0, grid_call = 0;
+  size_t off_put_fast = 0, off_put_base = 0, off_call_fast = 0, off_call_base = 0, off_euro_fast = 0,
+         off_euro_base = 0;
+
+  void release() {
+    for (DevBuf* b : {&d_put, &d_call, &d_euro, &d_orders, &d_price, &d_status, &d_bt, &d_bc, &d_bcount, &d_counter,
+                      &d_ws_put, &d_ws_call, &d_ws_base})
+      b->release();
+  }
+};
+
+namespace {
+
+// Host-side derivation + dispatch lists.  Pure host work (libm), no CUDA.
+void plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+               const double* Y, const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
+               int64_t put_cutoff, int method, int32_t cap) {
+  b->n = n;
+  b->method = method;
+  b->cap = cap;
+  b->kind.assign(kind, kind + n);
+  b->hstatus.assign(n, 0);
+  b->mode.assign(n, fl::MODE_ERROR);
+  b->put.resize(n);
+  b->call.resize(n);
+  b->euro.resize(n);
+  b->cost.assign(n, 0.0);
+  for (auto* v : {&b->o_put_fast, &b->o_put_base, &b->o_call_fast, &b->o_call_base, &b->o_euro_fast, &b->o_euro_base})
+    v->clear();
+  for (int64_t i = 0; i < n; ++i) {
+    const fl::SpecIn s{S[i], K[i], R[i], Y[i], V[i], E[i], T[i]};
+    const int32_t o = (int32_t)i;
+    int32_t st = 0;
+    switch (kind[i]) {
+      case FL_KIND_EURO: {
+        st = fl::prep_euro(s, b->euro[i]);
+        if (!st) {
+          b->mode[i] = (method == FL_METHOD_FAST) ? fl::MODE_FAST : fl::MODE_BASELINE;
+          (method == FL_METHOD_FAST ? b->o_euro_fast : b->o_euro_base).push_back(o);
+        }
+        break;
+      }
+      case FL_KIND_CALL: {
+        if (method == FL_METHOD_FAST) {
+          st = fl::prep_call(s, call_cutoff, b->call[i], b->euro[i]);
+          if (!st) {
+            b->mode[i] = b->call[i].mode;
+            if (b->mode[i] == fl::MODE_FAST) b->o_call_fast.push_back(o);
+            else if (b->mode[i] == fl::MODE_BASELINE) b->o_call_base.push_back(o);
+            else if (b->mode[i] == fl::MODE_EURO) b->o_euro_fast.push_back(o);
+          }
+        } else {
+          fl::Binom bn;
+          st = fl::derive_binomial(s, bn);
+          if (!st) {
+            fl::CallParams& c = b->call[i];
+            c.S = s.S; c.K = s.K; c.wd = bn.wd; c.wu = bn.wu; c.lu = bn.lu; c.n = s.T;
+            c.top_b = -1; c.junc_j = -1; c.cutoff = (int32_t)call_cutoff; c.mode = fl::MODE_BASELINE; c.price = 0;
+            b->mode[i] = fl::MODE_BASELINE;
+            b->o_call_base.push_back(o);
+          }
+        }
+        b->cost[i] = cost_call(s.T);
+        break;
+      }
+      case FL_KIND_PUT: {
+        st = fl::prep_put(s, lam, put_cutoff, b->put[i]);
+        if (method == FL_METHOD_BASELINE) {
+          // baseline_put_fd: discretization errors only, no cutoff / intrinsic dispatch
+          if (!st || (st == (FL_E_VALIDATION | FL_F_CUTOFF))) {
+            st = 0;
+            b->put[i].mode = fl::MODE_BASELINE;
+          }
+        }
+        if (!st) {
+          b->mode[i] = b->put[i].mode;
+          if (b->mode[i] == fl::MODE_FAST) b->o_put_fast.push_back(o);
+          else if (b->mode[i] == fl::MODE_BASELINE) b->o_put_base.push_back(o);
+        }
+        b->cost[i] = cost_put(s.T);
+        break;
+      }
+      default:
+        st = FL_E_VALIDATION;
+    }
+    b->hstatus[i] = st;
+    if (st) b->mode[i] = fl::MODE_ERROR;
+  }
+  sort_by_cost(b->o_put_fast, b->cost);
+  sort_by_cost(b->o_call_fast, b->cost);
+}
+
+int upload(fl_batch* b, cudaStream_t stream) {
+  const int64_t n = b->n;
+  FL_CUDA(cudaGetDevice(&b->dev));
+  FL_CUDA(ensure_device_init(b->dev, stream));
+  int nsm = 0;
+  FL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, b->dev));
+  FL_CUDA(b->d_put.ensure(sizeof(fl::PutParams) * n));
+  FL_CUDA(b->d_call.ensure(sizeof(fl::CallParams) * n));
+  FL_CUDA(b->d_euro.ensure(sizeof(fl::EuroParams) * n));
+  // orders packed into one buffer
+  size_t off = 0;
+  auto place = [&](const std::vector<int32_t>& v, size_t& o) { o = off; off += v.size(); };
+  place(b->o_put_fast, b->off_put_fast);
+  place(b->o_put_base, b->off_put_base);
+  place(b->o_call_fast, b->off_call_fast);
+  place(b->o_call_base, b->off_call_base);
+  place(b->o_euro_fast, b->off_euro_fast);
+  place(b->o_euro_base, b->off_euro_base);
+  FL_CUDA(b->d_orders.ensure(sizeof(int32_t) * (off + 1)));
+  FL_CUDA(b->d_price.ensure(sizeof(double) * n));
+  FL_CUDA(b->d_status.ensure(sizeof(int32_t) * n));
+  FL_CUDA(b->d_bcount.ensure(sizeof(int32_t) * n));
+  if (b->cap > 0) {
+    FL_CUDA(b->d_bt.ensure(sizeof(int64_t) * n * b->cap));
+    FL_CUDA(b->d_bc.ensure(sizeof(int64_t) * n * b->cap));
+  }
+  FL_CUDA(b->d_counter.ensure(64));
+  // workspaces
+  int64_t nmax_put = 0, ksmax = 0, nmax_call = 0, nmax_base = 0;
+  for (int32_t o : b->o_put_fast) {
+    nmax_put = std::max(nmax_put, b->put[o].n);
+    ksmax = std::max<int64_t>(ksmax, std::max<int64_t>(b->put[o].ks, 0));
+  }
+  for (int32_t o : b->o_call_fast) nmax_call = std::max(nmax_call, b->call[o].n);
+  for (int32_t o : b->o_put_base) nmax_base = std::max(nmax_base, b->put[o].n * 2 + 2);
+  for (int32_t o : b->o_call_base) nmax_base = std::max(nmax_base, b->call[o].n + 2);
+  for (int32_t o : b->o_euro_base) nmax_base = std::max(nmax_base, b->euro[o].n + 2);
+  int occ = 1;
+  if (!b->o_put_fast.empty()) {
+    b->ws_put_stride = fl::put_ws_doubles(nmax_put, ksmax);
+    b->grid_put = std::min<int>((int)b->o_put_fast.size(), nsm * 2);
+    FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_put_stride * b->grid_put));
+  }
+  if (!b->o_call_fast.empty()) {
+    b->ws_call_stride = fl::call_ws_doubles(nmax_call);
+    b->grid_call = std::min<int>((int)b->o_call_fast.size(), nsm * 2);
+    FL_CUDA(b->d_ws_call.ensure(sizeof(double) * b->ws_call_stride * b->grid_call));
+  }
+  (void)occ;
+  const int64_t nbase = (int64_t)std::max({b->o_put_base.size(), b->o_call_base.size(), b->o_euro_base.size()});
+  if (nbase > 0) {
+    b->ws_base_stride = 3 * nmax_base + 16;
+    FL_CUDA(b->d_ws_base.ensure(sizeof(double) * b->ws_base_stride * nbase));
+  }
+  // H2D
+  std::vector<int32_t> orders(off + 1, 0);
+  auto copy_in = [&](const std::vector<int32_t>& v, size_t o) { std::copy(v.begin(), v.end(), orders.begin() + o); };
+  copy_in(b->o_put_fast, b->off_put_fast);
+  copy_in(b->o_put_base, b->off_put_base);
+  copy_in(b->o_call_fast, b->off_call_fast);
+  copy_in(b->o_call_base, b->off_call_base);
+  copy_in(b->o_euro_fast, b->off_euro_fast);
+  copy_in(b->o_euro_base, b->off_euro_base);
+  FL_CUDA(cudaMemcpyAsync(b->d_put.p, b->put.data(), sizeof(fl::PutParams) * n, cudaMemcpyHostToDevice, stream));
+  FL_CUDA(cudaMemcpyAsync(b->d_call.p, b->call.data(), sizeof(fl::CallParams) * n, cudaMemcpyHostToDevice, stream));
+  FL_CUDA(cudaMemcpyAsync(b->d_euro.p, b->euro.data(), sizeof(fl::EuroParams) * n, cudaMemcpyHostToDevice, stream));
+  FL_CUDA(cudaMemcpyAsync(b->d_orders.p, orders.data(), sizeof(int32_t) * (off + 1), cudaMemcpyHostToDevice, stream));
+  FL_CUDA(cudaStreamSynchronize(stream));
+  return 0;
+}
+
+fl::BatchOut make_out(fl_batch* b) {
+  fl::BatchOut o;
+  o.price = b->d_price.as<double>();
+  o.status = b->d_status.as<int32_t>();
+  o.bt = b->cap > 0 ? b->d_bt.as<int64_t>() : nullptr;
+  o.bc = b->cap > 0 ? b->d_bc.as<int64_t>() : nullptr;
+  o.bcount = b->d_bcount.as<int32_t>();
+  o.cap = b->cap;
+  return o;
+}
+
+int run(fl_batch* b, cudaStream_t stream) {
+  const fl::BatchOut out = make_out(b);
+  const int32_t* ord = b->d_orders.as<int32_t>();
+  int32_t* counter = b->d_counter.as<int32_t>();
+  b->launches = 0;
+  if (!b->o_put_fast.empty()) {
+    FL_CUDA(fl::launch_put_fast(b->d_put.as<fl::PutParams>(), ord + b->off_put_fast, (int)b->o_put_fast.size(),
+                                counter, b->d_ws_put.as<double>(), b->ws_put_stride, b->grid_put, out, stream));
+    ++b->launches;
+  }
+  if (!b->o_call_fast.empty()) {
+    FL_CUDA(fl::launch_call_fast(b->d_call.as<fl::CallParams>(), ord + b->off_call_fast,
+                                 (int)b->o_call_fast.size(), counter + 8, b->d_ws_call.as<double>(),
+                                 b->ws_call_stride, b->grid_call, out, stream));
+    ++b->launches;
+  }
+  if (!b->o_euro_fast.empty()) {
+    FL_CUDA(fl::launch_euro_fast(b->d_euro.as<fl::EuroParams>(), ord + b->off_euro_fast, (int)b->o_euro_fast.size(),
+                                 out, stream));
+    ++b->launches;
+  }
+  if (!b->o_put_base.empty()) {
+    FL_CUDA(fl::launch_put_baseline(b->d_put.as<fl::PutParams>(), ord + b->off_put_base, (int)b->o_put_base.size(),
+                                    b->d_ws_base.as<double>(), b->ws_base_stride, out, stream));
+    ++b->launches;
+  }
+  if (!b->o_call_base.empty()) {
+    FL_CUDA(fl::launch_call_baseline(b->d_call.as<fl::CallParams>(), ord + b->off_call_base,
+                                     (int)b->o_call_base.size(), b->d_ws_base.as<double>(), b->ws_base_stride, out,
+                                     stream));
+    ++b->launches;
+  }
+  if (!b->o_euro_base.empty()) {
+    FL_CUDA(fl::launch_euro_baseline(b->d_euro.as<fl::EuroParams>(), ord + b->off_euro_base,
+                                     (int)b->o_euro_base.size(), b->d_ws_base.as<double>(), b->ws_base_stride, out,
+                                     stream));
+    ++b->launches;
+  }
+  return 0;
+}
+
+inline int64_t fg_rec(int64_t i, int64_t j) { return j >= i ? INT64_MIN : j + 1; }
+
+int fetch(fl_batch* b, double* price, int32_t* status, int64_t* bt, int64_t* bc, int32_t* bcount,
+          cudaStream_t stream) {
+  const int64_t n = b->n;
+  const int32_t cap = b->cap;
+  FL_CUDA(cudaMemcpyAsync(price, b->d_price.p, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+  FL_CUDA(cudaMemcpyAsync(status, b->d_status.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, stream));
+  std::vector<int32_t> cnt(n, 0);
+  FL_CUDA(cudaMemcpyAsync(cnt.data(), b->d_bcount.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, stream));
+  const bool want_b = cap > 0 && bt && bc && bcount;
+  if (want_b) {
+    FL_CUDA(cudaMemcpyAsync(bt, b->d_bt.p, sizeof(int64_t) * n * cap, cudaMemcpyDeviceToHost, stream));
+    FL_CUDA(cudaMemcpyAsync(bc, b->d_bc.p, sizeof(int64_t) * n * cap, cudaMemcpyDeviceToHost, stream));
+  }
+  FL_CUDA(cudaStreamSynchronize(stream));
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t m = b->mode[i];
+    int32_t c = cnt[i];
+    auto rec = [&](int32_t k, int64_t t, int64_t col) {
+      if (want_b && k < cap) {
+        bt[i * cap + k] = t;
+        bc[i * cap + k] = col;
+      }
+    };
+    if (m == fl::MODE_ERROR) {
+      status[i] = b->hstatus[i];
+      price[i] = std::nan("");
+      c = 0;
+    } else if (b->kind[i] == FL_KIND_PUT && m == fl::MODE_INTRINSIC) {
+      status[i] = 0;
+      price[i] = b->put[i].price;
+      rec(0, 0, std::min<int64_t>(0, b->put[i].ks + b->put[i].n));
+      c = 1;
+    } else if (b->kind[i] == FL_KIND_CALL && m == fl::MODE_INTRINSIC) {
+      const fl::CallParams& p = b->call[i];
+      status[i] = 0;
+      price[i] = p.price;
+      rec(0, p.n - 1, fg_rec(p.n - 1, p.junc_j));  // ascending order: T-1, T
+      rec(1, p.n, fg_rec(p.n, p.top_b));
+      c = 2;
+    } else if (b->kind[i] == FL_KIND_CALL && m == fl::MODE_EURO) {
+      const fl::CallParams& p = b->call[i];
+      rec(0, p.n, p.top_b == p.n ? INT64_MIN : fg_rec(p.n, p.top_b));
+      c = 1;
+    } else if (b->kind[i] == FL_KIND_CALL && m == fl::MODE_FAST && want_b && status[i] == 0) {
+      // device records run T, T-1, ..., 0: reverse into ascending order
+      const int32_t k = std::min(c, cap);
+      std::reverse(bt + i * cap, bt + i * cap + k);
+      std::reverse(bc + i * cap + 0, bc + i * cap + k);
+    }
+    if (bcount) bcount[i] = c;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fl_version(void) { return 100; }
+
+const char* fl_last_error(void) { return g_last_error.c_str(); }
+
+int fl_batch_prepare(fl_batch** out, int64_t n, const int8_t* kind, const double* S, const double* K,
+                     const double* R, const double* Y, const double* V, const double* E, const int64_t* T,
+                     double lam, int64_t call_cutoff, int64_t put_cutoff, int method, int32_t bnd_cap,
+                     void* stream) {
+  if (!out) return fail("fl_batch_prepare: null out");
+  if (n < 0) return fail("fl_batch_prepare: negative n");
+  fl_batch* b = new fl_batch();
+  plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+  int rc = upload(b, (cudaStream_t)stream);
+  if (rc) {
+    b->release();
+    delete b;
+    return rc;
+  }
+  *out = b;
+  return 0;
+}
+
+int fl_batch_run(fl_batch* b, void* stream) {
+  if (!b) return fail("fl_batch_run: null batch");
+  return run(b, (cudaStream_t)stream);
+}
+
+int fl_batch_fetch(fl_batch* b, double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols,
+                   int32_t* bnd_count, void* stream) {
+  if (!b) return fail("fl_batch_fetch: null batch");
+  return fetch(b, price, status, bnd_times, bnd_cols, bnd_count, (cudaStream_t)stream);
+}
+
+int fl_batch_launches(const fl_batch* b) { return b ? b->launches : 0; }
+
+void fl_batch_free(fl_batch* b) {
+  if (!b) return;
+  b->release();
+  delete b;
+}
+
+int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+                   const double* Y, const double* V, const double* E, const int64_t* T, double lam,
+                   int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
+                   int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream) {
+  // one cached batch per (thread, device): device buffers grow and are reused
+  thread_local fl_batch* cache[64] = {nullptr};
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail("fl_price_batch: device index out of range");
+  if (!cache[dev]) cache[dev] = new fl_batch();
+  fl_batch* b = cache[dev];
+  plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+  int rc = upload(b, (cudaStream_t)stream);
+  if (rc) return rc;
+  rc = run(b, (cudaStream_t)stream);
+  if (rc) return rc;
+  return fetch(b, price, status, bnd_times, bnd_cols, bnd_count, (cudaStream_t)stream);
+}
+
+int fl_apply_linear_steps(const double* x, int64_t L, int taps, double c0, double c1, double c2, int64_t h,
+                          double* y, void* stream) {
+  if (taps != 2 && taps != 3) return fail("fl_apply_linear_steps: taps must be 2 or 3");
+  if (h < 1 || h > (1 << 30)) return fail("fl_apply_linear_steps: h out of range");
+  if (!(c0 >= 0.0 && c1 >= 0.0 && c2 >= 0.0)) return fail("fl_apply_linear_steps: negative coefficient");
+  const int span = taps - 1;
+  const int64_t Lout = L - h * span;
+  if (Lout < 1) return fail("fl_apply_linear_steps: row too narrow");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  FL_CUDA(ensure_device_init(dev, st));
+  double *dx = nullptr, *dy = nullptr;
+  FL_CUDA(cudaMalloc(&dx, sizeof(double) * L));
+  FL_CUDA(cudaMalloc(&dy, sizeof(double) * Lout));
+  cudaError_t e = cudaMemcpyAsync(dx, x, sizeof(double) * L, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = fl::launch_linear_steps(dx, L, dy, Lout, (int)h, c0, c1, taps == 3 ? c2 : 0.0, span, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(y, dy, sizeof(double) * Lout, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dx);
+  cudaFree(dy);
+  if (e != cudaSuccess) return fail(std::string("fl_apply_linear_steps: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// fl_kernels.h -- device-kernel launchers shared by the C-ABI layer.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "host_params.h"
+
+namespace fl {
+
+// Per-option outputs (device pointers).  Boundary records are optional
+// (bt == nullptr); at most `cap` records per option are stored, bcount holds
+// the true count.
+struct BatchOut {
+  double* price;
+  int32_t* status;
+  int64_t* bt;
+  int64_t* bc;
+  int32_t* bcount;
+  int32_t cap;
+};
+
+void init_twiddles(cudaStream_t stream);
+
+int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max);
+int put_fast_smem_bytes();
+cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
+                            int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
+cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, double* ws,
+                                int64_t ws_stride, BatchOut out, cudaStream_t stream);
+
+cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, BatchOut out,
+                             cudaStream_t stream);
+cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, int nwork, double* ws,
+                                 int64_t ws_stride, BatchOut out, cudaStream_t stream);
+
+int linear_steps_smem_bytes();
+cudaError_t launch_linear_steps(const double* x, int64_t L, double* y, int64_t Lout, int h, double c0, double c1,
+                                double c2, int span, cudaStream_t stream);
+
+// American call (fl_call.cu)
+int64_t call_ws_doubles(int64_t n_max);
+int call_fast_smem_bytes();
+cudaError_t launch_call_fast(const CallParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
+                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
+cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,
+                                 int64_t ws_stride, BatchOut out, cudaStream_t stream);
+
+}  // namespace fl

@@ -1,0 +1,81 @@
+// fl_strip.cuh -- warp-level explicit projected sweeps (the nonlinear base cases).
+//
+// put_strip_warp  replaces _accel.bsm_strip_sweep        (_accel.py:203-242)
+//                 as driven by bsm._strip_advance          (bsm.py:402-440)
+// call_strip_warp replaces _accel.binomial_strip_sweep   (_accel.py:105-160)
+//
+// One warp owns the whole strip; lane l holds CPL consecutive columns in
+// registers, neighbours move by warp shuffles, and the boundary (last green
+// for the put, first green for the call) comes from warp-wide min/max
+// reductions instead of a scalar scan.  Tie rules follow the reference:
+// put cells are continuation iff lin > payoff (ties exercise); call cells are
+// continuation iff lin >= green (ties continuation).
+#pragma once
+
+#include "fl_common.cuh"
+
+namespace fl {
+
+constexpr int64_t NONE_SEEN = -(((int64_t)1) << 60);  // _accel.py:46
+
+// Put strip over columns [lo, hi], `height` forward rows.  Cells <= f hold the
+// payoff, cells f+1..hi come from in_org[col].  Writes the continuation values
+// of cols kb+1 .. hi-height of the final row to out_org[col] and returns kb, the
+// largest exercise column of the final row within its valid range (NONE_SEEN
+// if none).  Every lane of the warp must call.
+template <int CPL>
+__device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                  const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
+                                  int height, double cd, double cm, double cu) {
+  const int lane = threadIdx.x & 31;
+  double v[CPL], p[CPL];
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
+  }
+  unsigned green = 0;
+  for (int s = 1; s <= height; ++s) {
+    const double left = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double right = __shfl_down_sync(FULL, v[0], 1);
+    double nv[CPL];
+    green = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double l = (c == 0) ? left : v[c - 1];
+      const double r = (c == CPL - 1) ? right : v[c + 1];
+      const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+      const bool red = lin > p[c];
+      nv[c] = red ? lin : p[c];
+      green |= (red ? 0u : 1u) << c;
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  // last green inside the final valid range [lo+height, hi-height]
+  const int64_t vlo = lo + height, vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col >= vlo && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = v[c];
+  }
+  return kb;
+}
+
+}  // namespace fl

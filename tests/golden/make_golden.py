@@ -1,0 +1,185 @@
+"""Generate golden vectors by running the REFERENCE itself (this container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Imports the unmodified reference package ``fftlattice`` from
+/root/reference/pkg/src, prices seeded batches drawn by
+``paper_2303_02317_b200.workloads`` (the BASELINE.json configs, some reduced in
+size) plus hand-picked edge cases, and writes ``tests/golden/*.npz``.  The GPU
+box has no /root/reference: tests there read only these committed fixtures.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import fftlattice as fl  # noqa: E402  (the reference)
+
+from paper_2303_02317_b200.workloads import (  # noqa: E402
+    KIND_CALL, KIND_EURO, KIND_PUT, Batch, draw_config,
+)
+
+ERR_KINDS = ["ValidationError", "StabilityError", "DomainError", "GeometryError",
+             "NumericalIntegrityError", "InsufficientWidthError", "UnsupportedCombinationError"]
+
+
+def run_ref(kind, spec, method="fast"):
+    """(price, times, cols, err_kind, err_field) from the reference."""
+    try:
+        if kind == KIND_EURO:
+            p = fl.fast_european(spec) if method == "fast" else fl.baseline_european(spec)
+            t, c = np.zeros(0, np.int64), np.zeros(0, np.int64)
+        elif kind == KIND_CALL:
+            r = fl.fast_american_call(spec) if method == "fast" else fl.baseline_american_call(spec)
+            p, t, c = r.price, r.boundaries.times, r.boundaries.columns
+        else:
+            r = fl.fast_put_bsm(spec, 0.4) if method == "fast" else fl.baseline_put_fd(spec, 0.4)
+            p, t, c = r.price, r.boundaries.times, r.boundaries.columns
+        return float(p), np.asarray(t, np.int64), np.asarray(c, np.int64), "", ""
+    except (fl.PricingError, ValueError) as e:
+        # ValueError: the reference's own math-domain failure (zero strike on
+        # the American junction path, american.py:403) is mirrored too.
+        fld = getattr(e, "field", getattr(e, "weight", ""))
+        return math.nan, np.zeros(0, np.int64), np.zeros(0, np.int64), type(e).__name__, fld or ""
+
+
+def save(name, batch: Batch, method="fast"):
+    t0 = time.time()
+    prices, terr, tfld, offs, times, cols = [], [], [], [0], [], []
+    for i in range(len(batch)):
+        p, t, c, ek, ef = run_ref(int(batch.kind[i]), batch.spec(i), method)
+        prices.append(p); terr.append(ek); tfld.append(ef)
+        times.append(t); cols.append(c); offs.append(offs[-1] + len(t))
+    np.savez_compressed(
+        os.path.join(HERE, f"{name}.npz"),
+        kind=batch.kind, S=batch.S, K=batch.K, R=batch.R, Y=batch.Y, V=batch.V,
+        E=batch.E, T=batch.T, price=np.asarray(prices), err_kind=np.asarray(terr),
+        err_field=np.asarray(tfld), bnd_off=np.asarray(offs, np.int64),
+        bnd_times=np.concatenate(times) if times else np.zeros(0, np.int64),
+        bnd_cols=np.concatenate(cols) if cols else np.zeros(0, np.int64),
+        method=np.asarray(method),
+    )
+    print(f"{name}: {len(batch)} options, {time.time() - t0:.1f}s", flush=True)
+
+
+def from_specs(rows):
+    kinds = [r[0] for r in rows]
+    specs = [r[1] for r in rows]
+    n = len(rows)
+    b = Batch(np.asarray(kinds, np.int8), *(np.empty(n) for _ in range(6)), np.empty(n, np.int64))
+    for i, s in enumerate(specs):
+        b.S[i], b.K[i], b.R[i], b.Y[i] = s.spot, s.strike, s.rate, s.dividend_yield
+        b.V[i], b.E[i], b.T[i] = s.volatility, s.days_to_expiry, s.steps
+    return b
+
+
+def edge_cases():
+    O = fl.OptionSpec
+    rows = [
+        # reference KAT specs (test_binomial.py:39-47, test_american.py:38-39, test_bsm.py:30-33)
+        (KIND_EURO, O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024)),
+        (KIND_CALL, O(100.0, 90.0, 0.03, 0.07, 0.25, 365, 512)),
+        (KIND_CALL, O(150.0, 80.0, 0.09, 0.05, 0.15, 365, 512)),  # junction widening
+        (KIND_PUT, O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024)),
+        # dispatch branches
+        (KIND_CALL, O(120.0, 100.0, 0.05, 0.0, 0.3, 365, 4096)),   # Y == 0 -> European
+        (KIND_CALL, O(100.0, 95.0, 0.04, 0.06, 0.3, 365, 200)),    # T <= cutoff -> baseline
+        (KIND_CALL, O(50.0, 200.0, 0.05, 0.03, 0.1, 30, 512)),     # all-red terminal row
+        (KIND_CALL, O(100.0, 0.0, 0.05, 0.03, 0.2, 365, 1024)),    # zero strike
+        (KIND_CALL, O(200.0, 50.0, 0.01, 0.1, 0.1, 365, 1024)),    # deep ITM, large yield
+        (KIND_PUT, O(50.0, 160.0, 0.05, 0.0, 0.2, 365, 16)),       # k* <= -T intrinsic
+        (KIND_PUT, O(100.0, 100.0, 0.04, 0.0, 0.25, 180, 200)),    # T <= 2 cutoff -> baseline
+        (KIND_PUT, O(140.0, 100.0, 0.03, 0.0, 0.5, 60, 16384)),    # k* > 0 (Appendix C P3)
+        (KIND_PUT, O(90.0, 110.0, 0.06, 0.0, 0.35, 500, 16384)),   # k* < 0 (Appendix C P2)
+        (KIND_PUT, O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 4096)),
+        (KIND_PUT, O(60.0, 100.0, 0.08, 0.0, 0.1, 30, 1000)),      # deep ITM, boundary far down
+        (KIND_PUT, O(150.0, 50.0, 0.01, 0.0, 0.6, 730, 2000)),     # far OTM put
+        (KIND_EURO, O(100.0, 95.0, 0.03, 0.05, 0.25, 180, 16384)),
+        (KIND_CALL, O(100.0, 95.0, 0.03, 0.05, 0.25, 180, 16384)),
+        (KIND_CALL, O(120.0, 100.0, 0.04, 0.02, 0.35, 300, 16384)),
+        (KIND_CALL, O(80.0, 110.0, 0.02, 0.04, 0.45, 90, 16384)),
+        # error parity
+        (KIND_PUT, O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024)),    # fine
+        (KIND_PUT, O(200.0, 50.0, 0.05, 0.0, 0.1, 30, 4)),         # DomainError grid nodes
+        (KIND_PUT, O(100.0, 0.0, 0.05, 0.0, 0.2, 365, 64)),        # DomainError strike
+        (KIND_EURO, O(-1.0, 100.0, 0.05, 0.0, 0.2, 365, 64)),      # ValidationError spot
+        (KIND_CALL, O(100.0, 100.0, 0.05, 0.02, 0.0, 365, 64)),    # ValidationError volatility
+        (KIND_CALL, O(100.0, 100.0, 0.9, 0.0, 0.01, 365, 4)),      # prob_up out of range
+    ]
+    # a StabilityError put: search a seeded stream for one
+    rng = np.random.default_rng(7)
+    while True:
+        s = O(float(rng.uniform(50, 200)), float(rng.uniform(50, 200)), float(rng.uniform(0.01, 0.1)),
+              0.0, float(rng.uniform(0.1, 0.5)), int(rng.integers(30, 731)), int(rng.integers(64, 1024)))
+        try:
+            fl.discretize_bsm(s, 0.4)
+        except fl.StabilityError:
+            rows.append((KIND_PUT, s))
+            break
+    return from_specs(rows)
+
+
+def small_random(seed, n, tlo, thi):
+    """Random specs (all three kinds) at small T, for full-boundary baseline goldens."""
+    rng = np.random.default_rng([seed, 20261019])
+    rows = []
+    while len(rows) < n:
+        kind = int(rng.integers(0, 3))
+        T = int(rng.integers(tlo, thi + 1))
+        s = fl.OptionSpec(float(rng.uniform(50, 150)), float(rng.uniform(50, 150)),
+                          float(rng.uniform(0.01, 0.08)),
+                          0.0 if kind == KIND_PUT else float(rng.uniform(0.0, 0.06)),
+                          float(rng.uniform(0.1, 0.6)), float(rng.uniform(30, 730)), T)
+        try:
+            if kind == KIND_PUT:
+                fl.discretize_bsm(s, 0.4)
+            else:
+                fl.derive_binomial_params(s)
+        except fl.PricingError:
+            continue
+        rows.append((kind, s))
+    return from_specs(rows)
+
+
+def stratified_c5(per=2):
+    b = draw_config(5)
+    idx = []
+    for kind in (KIND_EURO, KIND_CALL, KIND_PUT):
+        for e in range(10, 17):
+            sel = np.nonzero((b.kind == kind) & (b.T == 2 ** e))[0][:per]
+            idx.extend(sel.tolist())
+    return b.subset(np.asarray(idx))
+
+
+if __name__ == "__main__":
+    which = set(sys.argv[1:])
+    want = lambda k: not which or k in which  # noqa: E731
+    if want("edge"):
+        save("edge_fast", edge_cases(), "fast")
+        save("edge_baseline", edge_cases(), "baseline")
+    if want("small"):
+        sm = small_random(1, 96, 40, 1500)
+        save("small_fast", sm, "fast")
+        save("small_baseline", sm, "baseline")
+    if want("c1"):
+        save("c1_fast", draw_config(1), "fast")
+    if want("c2"):
+        save("c2_fast", draw_config(2), "fast")
+    if want("c3"):
+        save("c3_fast", draw_config(3), "fast")
+    if want("c6"):
+        save("c6_fast", draw_config(6, n=32), "fast")
+    if want("c4"):
+        b = draw_config(4)
+        save("c4_fast", b.subset(np.r_[0:4, 64:68]), "fast")
+    if want("c5"):
+        save("c5_fast", stratified_c5(), "fast")
