@@ -74,6 +74,10 @@ int fl_batch_fetch(fl_batch* b, double* price, int32_t* status, int64_t* bnd_tim
                    int32_t* bnd_count, void* stream);
 /* Number of kernel launches one fl_batch_run enqueues. */
 int fl_batch_launches(const fl_batch* b);
+/* After a run: fp64 flops the fast kernels executed in it (FFT convention
+ * 5 C log2 C per complex transform + 5 per explicit cell), and the bytes the
+ * last prepare / fetch moved H2D / D2H. */
+int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t* d2h_bytes, void* stream);
 void fl_batch_free(fl_batch* b);
 
 /* Batched valid-mode composed-stencil correlation (fft.py:263 apply_linear_steps,
@@ -83,6 +87,10 @@ void fl_batch_free(fl_batch* b);
  * taps in {2,3}; coefficients must be nonnegative (lattice / FD weights). */
 int fl_apply_linear_steps(const double* x, int64_t L, int taps, double c0, double c1, double c2, int64_t h,
                           double* y, void* stream);
+
+/* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
+ * roofline denominator bench.py reports against. */
+int fl_probe_fp64(double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

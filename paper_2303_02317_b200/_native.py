@@ -39,7 +39,8 @@ _lib = None
 #: Every symbol include/fftlattice_b200.h declares.
 EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
-    "fl_batch_fetch", "fl_batch_launches", "fl_batch_free", "fl_apply_linear_steps",
+    "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_free", "fl_apply_linear_steps",
+    "fl_probe_fp64",
 )
 
 
@@ -82,6 +83,10 @@ def lib():
         L.fl_batch_free.restype = None
         L.fl_apply_linear_steps.argtypes = [P, i64, c_int, d, d, d, i64, P, P]
         L.fl_apply_linear_steps.restype = c_int
+        L.fl_batch_stats.argtypes = [P, P, P, P, P]
+        L.fl_batch_stats.restype = c_int
+        L.fl_probe_fp64.argtypes = [P, P]
+        L.fl_probe_fp64.restype = c_int
         _lib = L
         return L
 
@@ -211,6 +216,14 @@ class DeviceBatch:
     def launches(self) -> int:
         return int(lib().fl_batch_launches(self._h))
 
+    def stats(self, stream=None) -> dict:
+        """Executed fp64 flops of the last run and the H2D / D2H bytes moved."""
+        f = ctypes.c_double(0.0)
+        hb, db = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(lib().fl_batch_stats(self._h, ctypes.byref(f), ctypes.byref(hb), ctypes.byref(db),
+                                    ctypes.c_void_p(stream) if stream else None))
+        return {"fp64_flops": f.value, "h2d_bytes": hb.value, "d2h_bytes": db.value}
+
     def fetch(self, stream=None) -> BatchResult:
         n, cap = self.n, self.cap
         price = np.empty(n)
@@ -268,3 +281,10 @@ def price_batch_full(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put
     price, status, bcount = res.price.copy(), res.status.copy(), res.bnd_count.copy()
     price[over], status[over], bcount[over] = sub.price, sub.status, sub.bnd_count
     return BatchResult(price, status, bt, bc, bcount, cap2)
+
+
+def probe_fp64_tflops(stream=None) -> float:
+    """Measured DFMA throughput of the current device (TFLOP/s)."""
+    t = ctypes.c_double(0.0)
+    _check(lib().fl_probe_fp64(ctypes.byref(t), ctypes.c_void_p(stream) if stream else None))
+    return t.value

@@ -69,6 +69,34 @@ struct HostPinned {
   }
 };
 
+// Grow-only pinned host array (params are staged here, then copied H2D).
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t cap = 0, n = 0;
+  cudaError_t resize(size_t want) {
+    if (want > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      const size_t c = want < 64 ? 64 : want;
+      cudaError_t e = cudaMallocHost((void**)&p, c * sizeof(T));
+      if (e != cudaSuccess) return e;
+      cap = c;
+    }
+    n = want;
+    return cudaSuccess;
+  }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  T* data() { return p; }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = n = 0;
+  }
+};
+
 std::mutex g_init_mu;
 bool g_tw_ready[64] = {false};
 
@@ -109,9 +137,13 @@ struct fl_batch {
   std::vector<int8_t> kind;
   std::vector<int32_t> hstatus;  // host-decided status (errors)
   std::vector<int32_t> mode;
-  std::vector<fl::PutParams> put;
-  std::vector<fl::CallParams> call;
-  std::vector<fl::EuroParams> euro;
+  PinnedVec<fl::PutParams> put;
+  PinnedVec<fl::CallParams> call;
+  PinnedVec<fl::EuroParams> euro;
+  PinnedVec<int32_t> orders;
+  DevBuf d_stats;
+  size_t h2d_bytes = 0, d2h_bytes = 0;
+  bool need_put = false, need_call = false, need_euro = false;
   std::vector<double> cost;
   std::vector<int32_t> o_put_fast, o_put_base, o_call_fast, o_call_base, o_euro_fast, o_euro_base;
   // device-side
@@ -124,15 +156,19 @@ struct fl_batch {
 
   void release() {
     for (DevBuf* b : {&d_put, &d_call, &d_euro, &d_orders, &d_price, &d_status, &d_bt, &d_bc, &d_bcount, &d_counter,
-                      &d_ws_put, &d_ws_call, &d_ws_base})
+                      &d_ws_put, &d_ws_call, &d_ws_base, &d_stats})
       b->release();
+    put.release();
+    call.release();
+    euro.release();
+    orders.release();
   }
 };
 
 namespace {
 
 // Host-side derivation + dispatch lists.  Pure host work (libm), no CUDA.
-void plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
                const double* Y, const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
                int64_t put_cutoff, int method, int32_t cap) {
   b->n = n;
@@ -141,9 +177,9 @@ void plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, cons
   b->kind.assign(kind, kind + n);
   b->hstatus.assign(n, 0);
   b->mode.assign(n, fl::MODE_ERROR);
-  b->put.resize(n);
-  b->call.resize(n);
-  b->euro.resize(n);
+  FL_CUDA(b->put.resize(n));
+  FL_CUDA(b->call.resize(n));
+  FL_CUDA(b->euro.resize(n));
   b->cost.assign(n, 0.0);
   for (auto* v : {&b->o_put_fast, &b->o_put_base, &b->o_call_fast, &b->o_call_base, &b->o_euro_fast, &b->o_euro_base})
     v->clear();
@@ -208,6 +244,10 @@ void plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, cons
   }
   sort_by_cost(b->o_put_fast, b->cost);
   sort_by_cost(b->o_call_fast, b->cost);
+  b->need_put = !b->o_put_fast.empty() || !b->o_put_base.empty();
+  b->need_call = !b->o_call_fast.empty() || !b->o_call_base.empty();
+  b->need_euro = !b->o_euro_fast.empty() || !b->o_euro_base.empty();
+  return 0;
 }
 
 int upload(fl_batch* b, cudaStream_t stream) {
@@ -216,9 +256,10 @@ int upload(fl_batch* b, cudaStream_t stream) {
   FL_CUDA(ensure_device_init(b->dev, stream));
   int nsm = 0;
   FL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, b->dev));
-  FL_CUDA(b->d_put.ensure(sizeof(fl::PutParams) * n));
-  FL_CUDA(b->d_call.ensure(sizeof(fl::CallParams) * n));
-  FL_CUDA(b->d_euro.ensure(sizeof(fl::EuroParams) * n));
+  if (b->need_put) FL_CUDA(b->d_put.ensure(sizeof(fl::PutParams) * n));
+  if (b->need_call) FL_CUDA(b->d_call.ensure(sizeof(fl::CallParams) * n));
+  if (b->need_euro) FL_CUDA(b->d_euro.ensure(sizeof(fl::EuroParams) * n));
+  FL_CUDA(b->d_stats.ensure(64));
   // orders packed into one buffer
   size_t off = 0;
   auto place = [&](const std::vector<int32_t>& v, size_t& o) { o = off; off += v.size(); };
@@ -264,20 +305,31 @@ int upload(fl_batch* b, cudaStream_t stream) {
     b->ws_base_stride = 3 * nmax_base + 16;
     FL_CUDA(b->d_ws_base.ensure(sizeof(double) * b->ws_base_stride * nbase));
   }
-  // H2D
-  std::vector<int32_t> orders(off + 1, 0);
-  auto copy_in = [&](const std::vector<int32_t>& v, size_t o) { std::copy(v.begin(), v.end(), orders.begin() + o); };
+  // H2D (pinned staging)
+  FL_CUDA(b->orders.resize(off + 1));
+  int32_t* orders = b->orders.data();
+  orders[off] = 0;
+  auto copy_in = [&](const std::vector<int32_t>& v, size_t o) { std::copy(v.begin(), v.end(), orders + o); };
   copy_in(b->o_put_fast, b->off_put_fast);
   copy_in(b->o_put_base, b->off_put_base);
   copy_in(b->o_call_fast, b->off_call_fast);
   copy_in(b->o_call_base, b->off_call_base);
   copy_in(b->o_euro_fast, b->off_euro_fast);
   copy_in(b->o_euro_base, b->off_euro_base);
-  FL_CUDA(cudaMemcpyAsync(b->d_put.p, b->put.data(), sizeof(fl::PutParams) * n, cudaMemcpyHostToDevice, stream));
-  FL_CUDA(cudaMemcpyAsync(b->d_call.p, b->call.data(), sizeof(fl::CallParams) * n, cudaMemcpyHostToDevice, stream));
-  FL_CUDA(cudaMemcpyAsync(b->d_euro.p, b->euro.data(), sizeof(fl::EuroParams) * n, cudaMemcpyHostToDevice, stream));
-  FL_CUDA(cudaMemcpyAsync(b->d_orders.p, orders.data(), sizeof(int32_t) * (off + 1), cudaMemcpyHostToDevice, stream));
-  FL_CUDA(cudaStreamSynchronize(stream));
+  b->h2d_bytes = sizeof(int32_t) * (off + 1);
+  if (b->need_put) {
+    FL_CUDA(cudaMemcpyAsync(b->d_put.p, b->put.data(), sizeof(fl::PutParams) * n, cudaMemcpyHostToDevice, stream));
+    b->h2d_bytes += sizeof(fl::PutParams) * n;
+  }
+  if (b->need_call) {
+    FL_CUDA(cudaMemcpyAsync(b->d_call.p, b->call.data(), sizeof(fl::CallParams) * n, cudaMemcpyHostToDevice, stream));
+    b->h2d_bytes += sizeof(fl::CallParams) * n;
+  }
+  if (b->need_euro) {
+    FL_CUDA(cudaMemcpyAsync(b->d_euro.p, b->euro.data(), sizeof(fl::EuroParams) * n, cudaMemcpyHostToDevice, stream));
+    b->h2d_bytes += sizeof(fl::EuroParams) * n;
+  }
+  FL_CUDA(cudaMemcpyAsync(b->d_orders.p, orders, sizeof(int32_t) * (off + 1), cudaMemcpyHostToDevice, stream));
   return 0;
 }
 
@@ -289,6 +341,7 @@ fl::BatchOut make_out(fl_batch* b) {
   o.bc = b->cap > 0 ? b->d_bc.as<int64_t>() : nullptr;
   o.bcount = b->d_bcount.as<int32_t>();
   o.cap = b->cap;
+  o.flops = b->d_stats.as<unsigned long long>();
   return o;
 }
 
@@ -297,6 +350,7 @@ int run(fl_batch* b, cudaStream_t stream) {
   const int32_t* ord = b->d_orders.as<int32_t>();
   int32_t* counter = b->d_counter.as<int32_t>();
   b->launches = 0;
+  FL_CUDA(cudaMemsetAsync(b->d_stats.p, 0, 16, stream));
   if (!b->o_put_fast.empty()) {
     FL_CUDA(fl::launch_put_fast(b->d_put.as<fl::PutParams>(), ord + b->off_put_fast, (int)b->o_put_fast.size(),
                                 counter, b->d_ws_put.as<double>(), b->ws_put_stride, b->grid_put, out, stream));
@@ -349,6 +403,7 @@ int fetch(fl_batch* b, double* price, int32_t* status, int64_t* bt, int64_t* bc,
     FL_CUDA(cudaMemcpyAsync(bc, b->d_bc.p, sizeof(int64_t) * n * cap, cudaMemcpyDeviceToHost, stream));
   }
   FL_CUDA(cudaStreamSynchronize(stream));
+  b->d2h_bytes = (sizeof(double) + 2 * sizeof(int32_t)) * n + (want_b ? 2 * sizeof(int64_t) * n * cap : 0);
   for (int64_t i = 0; i < n; ++i) {
     const int32_t m = b->mode[i];
     int32_t c = cnt[i];
@@ -404,8 +459,9 @@ int fl_batch_prepare(fl_batch** out, int64_t n, const int8_t* kind, const double
   if (!out) return fail("fl_batch_prepare: null out");
   if (n < 0) return fail("fl_batch_prepare: negative n");
   fl_batch* b = new fl_batch();
-  plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
-  int rc = upload(b, (cudaStream_t)stream);
+  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+  if (!rc) rc = upload(b, (cudaStream_t)stream);
+  if (!rc && cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) rc = fail("fl_batch_prepare: sync failed");
   if (rc) {
     b->release();
     delete b;
@@ -428,6 +484,23 @@ int fl_batch_fetch(fl_batch* b, double* price, int32_t* status, int64_t* bnd_tim
 
 int fl_batch_launches(const fl_batch* b) { return b ? b->launches : 0; }
 
+int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t* d2h_bytes, void* stream) {
+  if (!b) return fail("fl_batch_stats: null batch");
+  unsigned long long f = 0;
+  FL_CUDA(cudaMemcpyAsync(&f, b->d_stats.p, sizeof(f), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (fp64_flops) *fp64_flops = (double)f;
+  if (h2d_bytes) *h2d_bytes = (int64_t)b->h2d_bytes;
+  if (d2h_bytes) *d2h_bytes = (int64_t)b->d2h_bytes;
+  return 0;
+}
+
+int fl_probe_fp64(double* tflops, void* stream) {
+  if (!tflops) return fail("fl_probe_fp64: null output");
+  FL_CUDA(fl::probe_fp64(tflops, (cudaStream_t)stream));
+  return 0;
+}
+
 void fl_batch_free(fl_batch* b) {
   if (!b) return;
   b->release();
@@ -445,8 +518,9 @@ int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double*
   if (dev < 0 || dev >= 64) return fail("fl_price_batch: device index out of range");
   if (!cache[dev]) cache[dev] = new fl_batch();
   fl_batch* b = cache[dev];
-  plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
-  int rc = upload(b, (cudaStream_t)stream);
+  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+  if (rc) return rc;
+  rc = upload(b, (cudaStream_t)stream);
   if (rc) return rc;
   rc = run(b, (cudaStream_t)stream);
   if (rc) return rc;

@@ -35,7 +35,7 @@ __device__ __forceinline__ int64_t first_green_rec(int64_t i, int64_t j) {  // a
 // lane l holds column lo+l.  Reads in_org[lo..j], writes out_org[lo..jp].
 __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict__ in_org,
                                   double* __restrict__ out_org, int64_t lo, int64_t top_row, int64_t j0,
-                                  int height) {
+                                  int height, double* cells) {
   const int lane = threadIdx.x & 31;
   const int W = (int)(j0 - lo + 1);
   const int64_t col = lo + lane;
@@ -50,6 +50,7 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
     if (j < lo) break;
     const int64_t child = top_row - s - 1;
     const int64_t top = j < child ? j : child;
+    *cells += (double)(top - lo + 1);
     const double bp = __shfl_sync(FULL, Bl, s);
     const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
     const double right = __shfl_down_sync(FULL, v, 1);
@@ -75,7 +76,7 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
 // Residual strip over the whole run (american.py:499-521): lo = 0, height = i,
 // CTA-wide in shared memory.  Returns j0 and leaves row values in sv.
 __device__ int64_t call_resid_cta(const CallParams& P, const double* row_org, int64_t i, int64_t j0, double* sv,
-                                  double* se2, int* s_fg) {
+                                  double* se2, int* s_fg, double* cells) {
   const int64_t W = j0 + 1;
   for (int64_t c = threadIdx.x; c <= W; c += CTA_THREADS) {
     sv[c] = (c < W) ? row_org[c] : 0.0;
@@ -87,6 +88,7 @@ __device__ int64_t call_resid_cta(const CallParams& P, const double* row_org, in
     if (j < 0) break;
     const int64_t parent = i - s, child = parent - 1;
     const int64_t top = j < child ? j : child;
+    *cells += (double)(top + 1);
     const double bc = P.S * exp((double)(0 - child) * P.lu);
     const double bp = P.S * exp((double)(0 - parent) * P.lu);
     if (threadIdx.x == 0) *s_fg = INT32_MAX;
@@ -138,7 +140,7 @@ __device__ __forceinline__ void cta_bcast(int64_t& v, int64_t* slot) {
 // writes out_org[j-h+1 .. jp]; returns jp.
 __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0, int64_t j0, int h0,
                               double* in_org, double* out_org, double* frames, int64_t arena0, double2* sbuf,
-                              int64_t* slot, int32_t* err) {
+                              int64_t* slot, int32_t* err, double* fl) {
   CallFrame stk[CALL_MAX_DEPTH];
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
   stk[0].arena = arena0; stk[0].state = 0;
@@ -151,8 +153,10 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
     if (F.state == 0) {
       if (h <= CALL_LEAF) {
         int64_t jp = 0;
-        if (threadIdx.x < 32) jp = call_leaf_warp(P, F.in_org, F.out_org, F.j - h + 1, F.i, F.j, h);
+        double cells = 0.0;
+        if (threadIdx.x < 32) jp = call_leaf_warp(P, F.in_org, F.out_org, F.j - h + 1, F.i, F.j, h, &cells);
         cta_bcast(jp, slot);
+        *fl += 5.0 * cells;  // meaningful on thread 0 (the accumulating thread)
         ret = jp;
         --sp;
         continue;
@@ -160,7 +164,7 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       const int64_t lo = F.j - h + 1;
       F.asm_org = frames + F.arena - lo;
       // mid: cols lo .. j-h1 of row i-h1
-      conv_valid(F.in_org + lo, h, F.asm_org + lo, h2, h1, st, sbuf, CALL_LOGN_MAX);
+      *fl += conv_valid(F.in_org + lo, h, F.asm_org + lo, h2, h1, st, sbuf, CALL_LOGN_MAX);
       F.state = 1;
       CallFrame& C = stk[sp];
       C.i = F.i; C.j = F.j; C.h = h1; C.in_org = F.in_org; C.out_org = F.asm_org;
@@ -173,7 +177,7 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       const int64_t lo = F.j - h + 1;
       const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
       // bottom: cols lo .. jm-h2 of row i-h
-      conv_valid(F.asm_org + lo, A, F.out_org + lo, A - h2, h2, st, sbuf, CALL_LOGN_MAX);
+      *fl += conv_valid(F.asm_org + lo, A, F.out_org + lo, A - h2, h2, st, sbuf, CALL_LOGN_MAX);
       F.state = 2;
       CallFrame& C = stk[sp];
       C.i = F.i - h1; C.j = jm; C.h = h2; C.in_org = F.asm_org; C.out_org = F.out_org;
@@ -217,6 +221,7 @@ call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict_
     double* rowB = arena + (n + 8);
     double* frames = arena + 2 * (n + 8);
     const Stencil st{P.wd, P.wu, 0.0, 1};
+    double flops = 0.0;
     int32_t err = 0, cnt = 0;
     call_record(out, o, cnt, n, first_green_rec(n, P.top_b));
     int64_t i = n - 1, j = P.junc_j;
@@ -242,8 +247,8 @@ call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict_
       const int64_t hh = (j + 1 < i - resid) ? j + 1 : i - resid;
       const int h = (int)hh;
       // left: cols 0 .. j-h of row i-h (american.py:341-344)
-      if (j + 1 > hh) conv_valid(cur, j + 1, nxt, j + 1 - hh, h, st, sbuf, CALL_LOGN_MAX);
-      const int64_t jp = call_solve(P, st, i, j, h, cur, nxt, frames, 0, sbuf, &s_slot, &err);
+      if (j + 1 > hh) flops += conv_valid(cur, j + 1, nxt, j + 1 - hh, h, st, sbuf, CALL_LOGN_MAX);
+      const int64_t jp = call_solve(P, st, i, j, h, cur, nxt, frames, 0, sbuf, &s_slot, &err, &flops);
       if (err) break;
       i -= hh;
       j = jp;
@@ -262,7 +267,9 @@ call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict_
         if (j + 2 > CALL_SLOTS || j + 1 > (int64_t)CALL_RESID_CPT * CTA_THREADS) {
           err = FL_E_CAPACITY | 2;
         } else {
-          const int64_t j0 = call_resid_cta(P, cur, i, j, sv, se2, &s_fg);
+          double cells = 0.0;
+          const int64_t j0 = call_resid_cta(P, cur, i, j, sv, se2, &s_fg, &cells);
+          flops += 5.0 * cells;
           price = (j0 >= 0) ? sv[0] : P.S - P.K;
           if (i > 0) call_record(out, o, cnt, 0, first_green_rec(0, j0));
           __syncthreads();
@@ -273,6 +280,7 @@ call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict_
       out.price[o] = err ? 0.0 : price;
       out.status[o] = err;
       if (out.bcount) out.bcount[o] = err ? 0 : cnt;
+      if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
     }
     __syncthreads();
   }

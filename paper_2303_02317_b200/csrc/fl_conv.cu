@@ -22,6 +22,51 @@ void init_twiddles(cudaStream_t stream) {
 
 constexpr int LS_LOGN_MAX = 13;
 
+// FP64 DFMA throughput probe (8 independent chains per thread, 2 CTAs x 1024
+// threads per SM); used by bench.py for the live roofline denominator.
+__global__ void __launch_bounds__(1024) fp64_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+         x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+cudaError_t probe_fp64(double* tflops, cudaStream_t stream) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = 2 * nsm, block = 1024, iters = 2048;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double) * grid * block);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_probe_kernel<<<grid, block, 0, stream>>>(d, 64, 0.999, 1e-3);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, stream);
+    fp64_probe_kernel<<<grid, block, 0, stream>>>(d, iters, 0.999, 1e-3);
+    cudaEventRecord(e1, stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  e = cudaGetLastError();
+  *tflops = 2.0 * 8 * 16 * (double)iters * grid * block / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return e;
+}
+
 __global__ void __launch_bounds__(CTA_THREADS)
 linear_steps_kernel(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
                     Stencil st) {

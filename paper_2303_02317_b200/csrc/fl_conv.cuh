@@ -193,9 +193,11 @@ __device__ __forceinline__ double2 spectrum(const Stencil& st, double2 om, doubl
 // ---------------------------------------------------------------------------
 // y[k] = sum_r W_h[r] x[k+r], k in [0, Lout).  x has L >= Lout + h*span values.
 // All CTA threads must call; buf holds smem_complex_slots(2^(logNmax-1)) double2.
-__device__ void conv_valid(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout,
-                           int h, const Stencil& st, double2* buf, int logNmax) {
-  if (Lout <= 0) return;
+// Returns the fp64 flops executed (FFT convention: 5 C log2 C per complex C-point
+// transform, two per block, plus 16 C for the split / spectrum / re-pack pass).
+__device__ double conv_valid(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout,
+                             int h, const Stencil& st, double2* buf, int logNmax) {
+  if (Lout <= 0) return 0.0;
   const ConvPlan pl = plan_conv(st, h, Lout, logNmax);
   const int logN = pl.logN;
   const int logC = logN - 1;
@@ -206,6 +208,7 @@ __device__ void conv_valid(const double* __restrict__ x, int64_t L, double* __re
   const int64_t rlo_modN = pl.rlo & (N - 1);
   const double rlo_sign = (pl.rlo & 1) ? -1.0 : 1.0;
 
+  const int64_t nblk = (Lout + pl.P - 1) / pl.P;
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
     const int64_t s0 = k0 + pl.rlo;
@@ -265,6 +268,7 @@ __device__ void conv_valid(const double* __restrict__ x, int64_t L, double* __re
     }
     __syncthreads();
   }
+  return (double)nblk * (10.0 * (double)C * (double)logC + 16.0 * (double)C);
 }
 
 }  // namespace fl

@@ -18,9 +18,11 @@ struct BatchOut {
   int64_t* bc;
   int32_t* bcount;
   int32_t cap;
+  unsigned long long* flops;  // executed fp64 flops of the fast kernels (accumulated), may be null
 };
 
 void init_twiddles(cudaStream_t stream);
+cudaError_t probe_fp64(double* tflops, cudaStream_t stream);
 
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max);
 int put_fast_smem_bytes();

@@ -99,7 +99,7 @@ __device__ double put_apex(const PutParams& P, const double* cur_org, const doub
 // status through *err.
 __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0, double* in_org,
                                double* out_org, int h0, const double* pay_org, double* frames,
-                               double2* sbuf, int64_t* slot, int32_t* err) {
+                               double2* sbuf, int64_t* slot, int32_t* err, double* fl) {
   PutFrame stk[PUT_MAX_DEPTH];
   int sp = 0;
   stk[0].f = f0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
@@ -117,6 +117,7 @@ __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0
                                        P.cd, P.cm, P.cu);
         }
         cta_bcast_i64(kb, slot);
+        *fl += 5.0 * (3.0 * (double)h * h + h);  // cells of a (4h+2)-wide, h-high strip
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
         --sp;
@@ -125,7 +126,7 @@ __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0
       const int h1 = (h + 1) / 2;
       F.asm_org = frames + F.arena - (F.f - h1 + 1);
       // mid: cols f+h1+1 .. f+2h-h1 of row t+h1 from the 2h inputs
-      conv_valid(F.in_org + F.f + 1, 2 * (int64_t)h, F.asm_org + F.f + h1 + 1, 2 * (int64_t)(h - h1), h1, st,
+      *fl += conv_valid(F.in_org + F.f + 1, 2 * (int64_t)h, F.asm_org + F.f + h1 + 1, 2 * (int64_t)(h - h1), h1, st,
                  sbuf, CONV_LOGN_MAX);
       F.state = 1;
       PutFrame& C = stk[sp];
@@ -140,7 +141,7 @@ __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0
       F.km = km;
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;  // assembled cols km+1 .. f+2h-h1
       // bottom: cols km+h2+1 .. f+h of row t+h
-      conv_valid(F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2, st, sbuf,
+      *fl += conv_valid(F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2, st, sbuf,
                  CONV_LOGN_MAX);
       F.state = 2;
       PutFrame& C = stk[sp];
@@ -200,7 +201,7 @@ put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ 
     const Stencil st{P.cd, P.cm, P.cu, 2};
     int32_t err = 0, cnt = 0;
     int64_t m = 0, f = 0;
-    double price = 0.0;
+    double price = 0.0, flops = 0.0;
     put_record(out, o, cnt, 0, 0);
     for (;;) {
       const int64_t rem = n - m;
@@ -210,6 +211,7 @@ put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ 
       if (rem <= 2 * (int64_t)P.cutoff) {
         if (2 * rem + 2 > CONV_SLOTS) { err = FL_E_CAPACITY | 2; break; }
         price = P.K * put_apex(P, cur_org, pay_org, f, rem, (double*)sbuf, ((double*)sbuf) + CONV_SLOTS, &s_slot);
+        flops += 5.0 * ((double)rem * rem + rem);
         break;
       }
       const int64_t hh = (rem / 2 < red / 2) ? rem / 2 : red / 2;
@@ -218,14 +220,16 @@ put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ 
         if (threadIdx.x < 32)
           kb = put_strip_warp<PUT_CPL>(cur_org, nxt_org, pay_org, f - 3, f + 1, f, 1, P.cd, P.cm, P.cu);
         cta_bcast_i64(kb, &s_slot);
+        flops += 15.0;
         if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
         f = kb;
         m += 1;
       } else {
         const int h = (int)hh;
         if (red > 2 * hh)  // far: cols f+h+1 .. ks+rem-h stay linear
-          conv_valid(cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, st, sbuf, CONV_LOGN_MAX);
-        const int64_t kp = put_solve_q(P, st, f, cur_org, nxt_org, h, pay_org, frames, sbuf, &s_slot, &err);
+          flops += conv_valid(cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, st, sbuf, CONV_LOGN_MAX);
+        const int64_t kp =
+            put_solve_q(P, st, f, cur_org, nxt_org, h, pay_org, frames, sbuf, &s_slot, &err, &flops);
         if (err) break;
         f = kp;
         m += hh;
@@ -239,6 +243,7 @@ put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ 
       out.price[o] = err ? 0.0 : price;
       out.status[o] = err;
       if (out.bcount) out.bcount[o] = err ? 0 : cnt;
+      if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
     }
     __syncthreads();
   }
