@@ -79,6 +79,10 @@ int fl_batch_launches(const fl_batch* b);
  * last prepare / fetch moved H2D / D2H. */
 int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t* d2h_bytes, void* stream);
 void fl_batch_free(fl_batch* b);
+/* Scheduler profile counters of the last run (requires FL_PROFILE set in the
+ * environment at run time; zeros otherwise): 56 uint64 slots, see PROF_* in
+ * csrc/fl_sched.cuh. */
+int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream);
 
 /* Batched valid-mode composed-stencil correlation (fft.py:263 apply_linear_steps,
  * american.py:180 / bsm.py:384 _valid_corr), on host buffers:

@@ -39,7 +39,8 @@ _lib = None
 #: Every symbol include/fftlattice_b200.h declares.
 EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
-    "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_free", "fl_apply_linear_steps",
+    "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
+    "fl_apply_linear_steps",
     "fl_probe_fp64",
 )
 
@@ -85,6 +86,8 @@ def lib():
         L.fl_apply_linear_steps.restype = c_int
         L.fl_batch_stats.argtypes = [P, P, P, P, P]
         L.fl_batch_stats.restype = c_int
+        L.fl_batch_profile.argtypes = [P, P, P]
+        L.fl_batch_profile.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
         _lib = L
@@ -212,6 +215,12 @@ class DeviceBatch:
 
     def run(self, stream=None) -> None:
         _check(lib().fl_batch_run(self._h, ctypes.c_void_p(stream) if stream else None))
+
+    def profile(self, stream=None) -> np.ndarray:
+        """Scheduler profile counters of the last run (FL_PROFILE=1 at run time)."""
+        out = np.zeros(56, dtype=np.uint64)
+        _check(lib().fl_batch_profile(self._h, _ptr(out), ctypes.c_void_p(stream) if stream else None))
+        return out
 
     def launches(self) -> int:
         return int(lib().fl_batch_launches(self._h))

@@ -4,6 +4,7 @@
 // american.py:428, bsm.py:273/585) map onto fl_price_batch per option kind.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -259,7 +260,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
   if (b->need_put) FL_CUDA(b->d_put.ensure(sizeof(fl::PutParams) * n));
   if (b->need_call) FL_CUDA(b->d_call.ensure(sizeof(fl::CallParams) * n));
   if (b->need_euro) FL_CUDA(b->d_euro.ensure(sizeof(fl::EuroParams) * n));
-  FL_CUDA(b->d_stats.ensure(64));
+  FL_CUDA(b->d_stats.ensure(64 * sizeof(unsigned long long)));
   // orders packed into one buffer
   size_t off = 0;
   auto place = [&](const std::vector<int32_t>& v, size_t& o) { o = off; off += v.size(); };
@@ -291,8 +292,9 @@ int upload(fl_batch* b, cudaStream_t stream) {
   int occ = 1;
   if (!b->o_put_fast.empty()) {
     b->ws_put_stride = fl::put_ws_doubles(nmax_put, ksmax);
-    b->grid_put = std::min<int>((int)b->o_put_fast.size(), nsm * 2);
-    FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_put_stride * b->grid_put));
+    const int nc = fl::put_chains_per_cta();
+    b->grid_put = std::min<int>(((int)b->o_put_fast.size() + nc - 1) / nc, nsm);
+    FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_put_stride * b->grid_put * nc));
   }
   if (!b->o_call_fast.empty()) {
     b->ws_call_stride = fl::call_ws_doubles(nmax_call);
@@ -342,6 +344,7 @@ fl::BatchOut make_out(fl_batch* b) {
   o.bcount = b->d_bcount.as<int32_t>();
   o.cap = b->cap;
   o.flops = b->d_stats.as<unsigned long long>();
+  o.prof = std::getenv("FL_PROFILE") ? b->d_stats.as<unsigned long long>() + 8 : nullptr;
   return o;
 }
 
@@ -350,7 +353,7 @@ int run(fl_batch* b, cudaStream_t stream) {
   const int32_t* ord = b->d_orders.as<int32_t>();
   int32_t* counter = b->d_counter.as<int32_t>();
   b->launches = 0;
-  FL_CUDA(cudaMemsetAsync(b->d_stats.p, 0, 16, stream));
+  FL_CUDA(cudaMemsetAsync(b->d_stats.p, 0, 64 * sizeof(unsigned long long), stream));
   if (!b->o_put_fast.empty()) {
     FL_CUDA(fl::launch_put_fast(b->d_put.as<fl::PutParams>(), ord + b->off_put_fast, (int)b->o_put_fast.size(),
                                 counter, b->d_ws_put.as<double>(), b->ws_put_stride, b->grid_put, out, stream));
@@ -492,6 +495,14 @@ int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t*
   if (fp64_flops) *fp64_flops = (double)f;
   if (h2d_bytes) *h2d_bytes = (int64_t)b->h2d_bytes;
   if (d2h_bytes) *d2h_bytes = (int64_t)b->d2h_bytes;
+  return 0;
+}
+
+int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
+  if (!b) return fail("fl_batch_profile: null batch");
+  FL_CUDA(cudaMemcpyAsync(counters56, b->d_stats.as<unsigned long long>() + 8, 56 * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return 0;
 }
 

@@ -1,5 +1,6 @@
-// fl_conv.cuh -- CTA-cooperative fp64 valid-mode correlation with a composed
-// stencil power, by overlap-save real FFT blocks staged in shared memory.
+// fl_conv.cuh -- fp64 valid-mode correlation with a composed stencil power,
+// executed by a thread group (a whole CTA, or the worker warps of a
+// warp-specialised CTA).
 //
 // Replaces the reference's `convolve` / `_valid_corr` / `kernel_power`
 // (fft.py:130-163, 203-260; american.py:180-184; bsm.py:384-387):
@@ -8,23 +9,24 @@
 //
 // where W_h are the coefficients of P(z)^h, P(z) = c0 + c1 z (+ c2 z^2).
 //
-// B200 design:
-//  * The composed kernel is never materialised.  Its spectrum on each block's
-//    own FFT grid is evaluated analytically, P(e^{i theta})^h by binary
-//    exponentiation, and only where |P|^h exceeds 1e-24 (the rest is exactly
-//    zeroed) -- a few percent of the bins for large h.
-//  * Overlap-save with a window: W_h is a (scaled) lattice-walk law, so all
-//    but <= 2e-22 of its mass lies within a Hoeffding window of half-width
-//    t = span*sqrt(h ln(2/eps)/2) around its mean.  Blocks of N real points
-//    therefore yield N - Mw + 1 valid outputs with Mw ~ 20 sqrt(h) instead of
-//    2h+1, so every block fits in shared memory (N <= NMAX) and nothing is
-//    padded to next_pow2(L+M-1).  The dropped tail contributes < 1e-21 of
-//    max|x|, far below the reference FFT's own ~1e-16 rounding.
-//  * Real-to-complex packing (N real = N/2 complex), in-place Stockham radix-16
-//    passes in registers with a padded shared-memory layout (conflict-free
-//    16-byte accesses), twiddles from a global fp64 table through the
-//    read-only path.  The spectrum multiply, the real-FFT split and the
-//    inverse pre-twist are fused into one shared-memory pass.
+// Two executors:
+//  * conv_fft -- overlap-save real FFT blocks staged in shared memory.  The
+//    composed kernel is never materialised: its spectrum on each block's own
+//    grid is P(e^{i theta})^h, evaluated by binary exponentiation only where
+//    |P|^h > 1e-24 (a few percent of the bins for large h; the rest are exact
+//    zeros).  Because W_h is a (scaled) lattice-walk law, all but <= 2e-22 of
+//    its mass lies in a Hoeffding window of half-width span*sqrt(h ln(2/eps)/2)
+//    about its mean, so a block of N real points yields N - Mw + 1 valid
+//    outputs with Mw ~ 20 sqrt(h) instead of 2h+1: every block fits in shared
+//    memory and nothing is padded to next_pow2(L+M-1).  The dropped tail is
+//    < 1e-21 of max|x|, far below the reference FFT's own ~1e-16 rounding.
+//    Real-to-complex packing (N real = N/2 complex); in-place Stockham radix-16
+//    passes in registers over a padded (bank-conflict-free) shared layout;
+//    twiddles from a global fp64 table; the real split, spectrum multiply and
+//    inverse pre-twist are one fused shared-memory pass.
+//  * conv_direct -- small kernels (h <= DIRECT_H): explicit dot products
+//    against cached real-space weights (built once per option and height by
+//    conv_fft on a delta), shared-memory staged.
 #pragma once
 
 #include "fl_common.cuh"
@@ -32,6 +34,15 @@
 namespace fl {
 
 constexpr int CTA_THREADS = 256;
+
+// A cooperating thread group: index t in [0, n), named barrier `bar`.
+struct Grp {
+  int t, n, bar;
+};
+
+__device__ __forceinline__ void gsync(const Grp& g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g.bar), "r"(g.n) : "memory");
+}
 
 // padded shared-memory index: one spare slot every 16 complex values
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -88,11 +99,11 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[R]) {
   }
 }
 
-// One in-place Stockham DIT pass of radix R over C complex points (C/R <= CTA_THREADS).
+// One in-place Stockham DIT pass of radix R over C complex points (C/R <= g.n).
 template <int R>
-__device__ __forceinline__ void stockham_pass(double2* buf, int C, int Ns, int logNsR) {
+__device__ __forceinline__ void stockham_pass(double2* buf, int C, int Ns, int logNsR, const Grp& g) {
   const int nb = C / R;
-  const int j = threadIdx.x;
+  const int j = g.t;
   double2 v[R];
   const bool act = j < nb;
   if (act) {
@@ -105,26 +116,26 @@ __device__ __forceinline__ void stockham_pass(double2* buf, int C, int Ns, int l
     }
     fft_reg<R>(v);
   }
-  __syncthreads();
+  gsync(g);
   if (act) {
     const int k = j & (Ns - 1);
     const int d = (j - k) * R + k;
 #pragma unroll
     for (int r = 0; r < R; ++r) buf[pidx(d + r * Ns)] = v[r];
   }
-  __syncthreads();
+  gsync(g);
 }
 
-// Forward complex FFT of C = 2^logC points (32 <= C <= 4096), in place, natural order.
-__device__ __noinline__ void fft_cta(double2* buf, int logC) {
+// Forward complex FFT of C = 2^logC points (32 <= C <= 16 * g.n), in place, natural order.
+__device__ __noinline__ void fft_grp(double2* buf, int logC, Grp g) {
   const int C = 1 << logC;
   int rem = logC % 4;
   int Ns = 1, logNs = 0;
-  if (rem == 1) { stockham_pass<2>(buf, C, Ns, logNs + 1); Ns <<= 1; logNs += 1; }
-  else if (rem == 2) { stockham_pass<4>(buf, C, Ns, logNs + 2); Ns <<= 2; logNs += 2; }
-  else if (rem == 3) { stockham_pass<8>(buf, C, Ns, logNs + 3); Ns <<= 3; logNs += 3; }
+  if (rem == 1) { stockham_pass<2>(buf, C, Ns, logNs + 1, g); Ns <<= 1; logNs += 1; }
+  else if (rem == 2) { stockham_pass<4>(buf, C, Ns, logNs + 2, g); Ns <<= 2; logNs += 2; }
+  else if (rem == 3) { stockham_pass<8>(buf, C, Ns, logNs + 3, g); Ns <<= 3; logNs += 3; }
   while (logNs < logC) {
-    stockham_pass<16>(buf, C, Ns, logNs + 4);
+    stockham_pass<16>(buf, C, Ns, logNs + 4, g);
     Ns <<= 4;
     logNs += 4;
   }
@@ -147,7 +158,7 @@ struct ConvPlan {
 
 constexpr double LN_2_OVER_EPS = 50.656872045869936;  // ln(2 / 2e-22)
 
-// Window + block plan for one task; uniform across the CTA (every thread computes it).
+// Window + block plan for one task; uniform across the group (every thread computes it).
 __device__ __forceinline__ ConvPlan plan_conv(const Stencil& st, int h, int64_t Lout, int logNmax) {
   ConvPlan p;
   const int64_t M = (int64_t)h * st.span + 1;
@@ -191,39 +202,40 @@ __device__ __forceinline__ double2 spectrum(const Stencil& st, double2 om, doubl
 }
 
 // ---------------------------------------------------------------------------
-// y[k] = sum_r W_h[r] x[k+r], k in [0, Lout).  x has L >= Lout + h*span values.
-// All CTA threads must call; buf holds smem_complex_slots(2^(logNmax-1)) double2.
-// Returns the fp64 flops executed (FFT convention: 5 C log2 C per complex C-point
-// transform, two per block, plus 16 C for the split / spectrum / re-pack pass).
-__device__ double conv_valid(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout,
-                             int h, const Stencil& st, double2* buf, int logNmax) {
+// FFT executor.  y[k] = sum_r W_h[r] x[k+r], k in [0, Lout); x has L >= Lout + h*span
+// values.  buf: smem_complex_slots(2^(logNmax-1)) double2.  Returns the executed
+// fp64 flops (FFT convention 5 C log2 C per complex transform, two per block,
+// plus 16 C for the split / spectrum / re-pack pass).  P < 1 (window wider
+// than the largest block) returns -1.
+__device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
+                           const Stencil& st, double2* buf, int logNmax, const Grp& g) {
   if (Lout <= 0) return 0.0;
   const ConvPlan pl = plan_conv(st, h, Lout, logNmax);
+  if (pl.P < 1) return -1.0;
   const int logN = pl.logN;
   const int logC = logN - 1;
   const int C = 1 << logC;
   const int N = 1 << logN;
   const double inv_c = 1.0 / (double)C;
-  const int tid = threadIdx.x;
   const int64_t rlo_modN = pl.rlo & (N - 1);
   const double rlo_sign = (pl.rlo & 1) ? -1.0 : 1.0;
-
   const int64_t nblk = (Lout + pl.P - 1) / pl.P;
+
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
     const int64_t s0 = k0 + pl.rlo;
 #pragma unroll 1
-    for (int n = tid; n < C; n += CTA_THREADS) {
+    for (int n = g.t; n < C; n += g.n) {
       const int64_t i0 = s0 + 2 * (int64_t)n;
       const double a = (i0 < L) ? x[i0] : 0.0;
       const double b = (i0 + 1 < L) ? x[i0 + 1] : 0.0;
       buf[pidx(n)] = make_double2(a, b);
     }
-    __syncthreads();
-    fft_cta(buf, logC);
+    gsync(g);
+    fft_grp(buf, logC, g);
     // -- split to the real spectrum, multiply, re-pack for the inverse (conjugated, /C)
 #pragma unroll 1
-    for (int k = tid; k <= C / 2; k += CTA_THREADS) {
+    for (int k = g.t; k <= C / 2; k += g.n) {
       const int kc = (C - k) & (C - 1);
       const double2 Zk = buf[pidx(k)];
       const double2 Zc = buf[pidx(kc)];
@@ -255,20 +267,57 @@ __device__ double conv_valid(const double* __restrict__ x, int64_t L, double* __
       buf[pidx(k)] = cconj(Zpk);
       if (k != 0 && k != C / 2) buf[pidx(kc)] = cscale(csub(A, iCWB), 0.5);  // conj(Zp[C-k])
     }
-    __syncthreads();
-    fft_cta(buf, logC);
+    gsync(g);
+    fft_grp(buf, logC, g);
     // -- store valid outputs: y[2n] = Re, y[2n+1] = -Im
     const int64_t lim = (Lout - k0 < pl.P) ? (Lout - k0) : pl.P;
 #pragma unroll 1
-    for (int n = tid; n < C; n += CTA_THREADS) {
+    for (int n = g.t; n < C; n += g.n) {
       const double2 v = buf[pidx(n)];
       const int64_t j = 2 * (int64_t)n;
       if (j < lim) y[k0 + j] = v.x;
       if (j + 1 < lim) y[k0 + j + 1] = -v.y;
     }
-    __syncthreads();
+    gsync(g);
   }
   return (double)nblk * (10.0 * (double)C * (double)logC + 16.0 * (double)C);
+}
+
+// ---------------------------------------------------------------------------
+// Direct executor for small kernels.  wrev[i] = W_h[M-1-i] (as conv_fft of a delta
+// returns it).  Stages x and the weights in shared memory (sx holds >= L + M
+// doubles).  Returns executed flops.
+__device__ double conv_direct(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout,
+                              const double* __restrict__ wrev, int M, double* sx, const Grp& g) {
+  if (Lout <= 0) return 0.0;
+  double* sw = sx + L;
+  for (int i = g.t; i < L; i += g.n) sx[i] = x[i];
+  for (int i = g.t; i < M; i += g.n) sw[i] = wrev[M - 1 - i];  // sw[r] = W[r]
+  gsync(g);
+  // G threads per output (power of two, <= 32), taps strided by G
+  int G = 1;
+  while (G < 32 && (int64_t)(g.n / (2 * G)) >= Lout) G <<= 1;
+  const int sub = g.t & (G - 1);
+  const int per = g.n / G;
+  for (int64_t k0 = 0; k0 < Lout; k0 += per) {
+    const int64_t k = k0 + g.t / G;
+    double a0 = 0.0, a1 = 0.0;
+    if (k < Lout) {
+      const double* xk = sx + k;
+      int r = sub;
+#pragma unroll 4
+      for (; r + G < M; r += 2 * G) {
+        a0 = fma(sw[r], xk[r], a0);
+        a1 = fma(sw[r + G], xk[r + G], a1);
+      }
+      if (r < M) a0 = fma(sw[r], xk[r], a0);
+    }
+    double s = a0 + a1;
+    for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (k < Lout && sub == 0) y[k] = s;
+  }
+  gsync(g);
+  return 2.0 * (double)Lout * (double)M;
 }
 
 }  // namespace fl

@@ -19,6 +19,7 @@ struct BatchOut {
   int32_t* bcount;
   int32_t cap;
   unsigned long long* flops;  // executed fp64 flops of the fast kernels (accumulated), may be null
+  unsigned long long* prof;   // optional profile counters (PROF_* in fl_sched.cuh), may be null
 };
 
 void init_twiddles(cudaStream_t stream);
@@ -26,6 +27,7 @@ cudaError_t probe_fp64(double* tflops, cudaStream_t stream);
 
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max);
 int put_fast_smem_bytes();
+int put_chains_per_cta();
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
 cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, double* ws,

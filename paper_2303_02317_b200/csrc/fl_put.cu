@@ -3,30 +3,33 @@
 // projected march (replaces bsm.baseline_put_fd / _accel.put_march_window,
 // bsm.py:273-338, _accel.py:163-200).
 //
-// Fast path: one persistent CTA per option at a time (options pulled from an
-// atomic queue in cost order).  The whole halving recursion runs on device with
-// an explicit per-thread stack (every thread holds an identical copy; control
-// flow is CTA-uniform), so there are no host round-trips:
-//   * linear jumps (far / mid / bottom) -> conv_valid (fl_conv.cuh), all warps;
-//   * nonlinear leaves (h <= LEAF)      -> put_strip_warp, warp 0;
-//   * apex finish (rem <= 2 cutoff)     -> CTA sweep in shared memory.
-// Row data live in a per-CTA HBM arena, column-indexed so that concatenations
-// in the reference (upper|mid, lower|bottom, near|far) are free.
+// Fast path: a persistent, warp-specialised CTA per SM (fl_sched.cuh).  Each
+// chain warp prices one option at a time, pulled from a global queue in
+// decreasing-cost order:
+//   * stage loop (bsm.py:639-665) and the _solve_q halving recursion
+//     (bsm.py:443-501) run on the chain warp with an explicit stack;
+//   * nonlinear leaves (h <= PUT_LEAF, the reference's _strip_advance /
+//     bsm_strip_sweep) run on the chain warp, registers + shuffles;
+//   * every linear jump (far / mid / bottom) is issued to the worker warps;
+//   * the apex finish (bsm.py:679-713) is a worker task over shared memory.
+// Row data live in a per-chain HBM arena, column-indexed, so the reference's
+// concatenations (upper|mid, lower|bottom, near|far) are free.
 #include <cstdint>
 
 #include "fl_common.cuh"
 #include "fl_conv.cuh"
 #include "fl_kernels.h"
+#include "fl_sched.cuh"
 #include "fl_strip.cuh"
 #include "host_params.h"
 
 namespace fl {
 
-constexpr int PUT_LEAF = 32;                     // device recursion leaf height
+constexpr int PUT_LEAF = 32;                           // device recursion leaf height
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
 constexpr int PUT_MAX_DEPTH = 24;
-constexpr int CONV_LOGN_MAX = 13;                // real FFT block <= 8192
-constexpr int CONV_SLOTS = smem_complex_slots(1 << (CONV_LOGN_MAX - 1));
+
+enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1 };
 
 struct PutFrame {
   int64_t f, km;
@@ -50,90 +53,82 @@ __host__ __device__ inline PutLayout put_layout(int64_t n, int64_t ks) {
   return L;
 }
 
-// doubles needed per CTA for a batch whose options have at most these sizes
+constexpr int64_t KCACHE_DOUBLES = (int64_t)(DIRECT_H + 2) * (DIRECT_H + 2) * 2;
+constexpr int64_t DELTA_DOUBLES = 4 * DIRECT_H + 8;
+
+// doubles needed per chain for a batch whose options have at most these sizes
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max) {
   const int64_t span = 2 * n_max + ks_pos_max + 4 * PUT_LEAF + 32;
   const int64_t frames = 2 * n_max + 64 * PUT_MAX_DEPTH;
-  return 3 * span + frames + 64;
+  return 3 * span + frames + KCACHE_DOUBLES + DELTA_DOUBLES + 64;
 }
 
-__device__ __forceinline__ void cta_bcast_i64(int64_t& v, int64_t* slot) {
-  if (threadIdx.x == 0) *slot = v;
-  __syncthreads();
-  v = *slot;
-  __syncthreads();
+struct PutChainCtx {
+  SchedShared* S;
+  int c;
+  Stencil st;
+  double* kc;
+  unsigned char* kbuilt;
+  const double* delta;
+  double* frames;
+  const double* pay_org;
+  double flops;  // strip flops (lane-uniform)
+  unsigned long long* prof;
+};
+
+__device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
+                                         int h) {
+  issue_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.kbuilt, X.delta);
 }
 
-// Apex cone sweep in shared memory (bsm._apex_finish, bsm.py:679-713), restricted
-// to the apex dependency cone [ks-rem-1, ks+rem] (identical arithmetic for
-// every cell the apex depends on).
-__device__ double put_apex(const PutParams& P, const double* cur_org, const double* pay_org, int64_t f,
-                           int64_t rem, double* sA, double* sB, int64_t* slot) {
-  const int64_t lo = P.ks - rem - 1, hi = P.ks + rem;
-  const int W = (int)(hi - lo + 1);
-  for (int i = threadIdx.x; i < W; i += CTA_THREADS) {
-    const int64_t col = lo + i;
-    sA[i] = (col <= f) ? pay_org[col] : cur_org[col];
-    sB[i] = sA[i];
+// Leaf strip on the chain warp, after waiting for conflicting pending jumps.
+__device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, double* in_org, double* out_org,
+                                            int64_t lo, int64_t hi, int64_t f, int height) {
+  const long long t0 = clock64();
+  wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + hi + 1), U(X.pay_org + lo), U(X.pay_org + hi + 1),
+                 U(out_org + lo), U(out_org + hi + 1));
+  const long long t1 = clock64();
+  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu);
+  if (X.prof && lane_id() == 0) {
+    const long long t2 = clock64();
+    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
+    prof_add(X.prof, PROF_WAIT_N, (t1 - t0) > 200 ? 1 : 0);
+    prof_add(X.prof, PROF_STRIP_CYC, t2 - t1);
+    prof_add(X.prof, PROF_STRIP_N, height);
   }
-  __syncthreads();
-  double* a = sA;
-  double* b = sB;
-  for (int s = 1; s <= rem; ++s) {
-    for (int i = s + threadIdx.x; i <= W - 1 - s; i += CTA_THREADS) {
-      const double lin = fma(P.cd, a[i - 1], fma(P.cu, a[i + 1], P.cm * a[i]));
-      const double pay = pay_org[lo + i];
-      b[i] = lin > pay ? lin : pay;
-    }
-    __syncthreads();
-    double* t = a;
-    a = b;
-    b = t;
-  }
-  const double r = a[P.ks - lo];
-  __syncthreads();
-  return r;
+  const double W = (double)(hi - lo + 1);
+  X.flops += 5.0 * (W * height - (double)height * (height + 1));
+  return kb;
 }
 
-// _solve_q (bsm.py:443-501) as an explicit-stack loop.  Returns kp or an error
-// status through *err.
-__device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0, double* in_org,
-                               double* out_org, int h0, const double* pay_org, double* frames,
-                               double2* sbuf, int64_t* slot, int32_t* err, double* fl) {
+// _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
+__device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, double* in_org, double* out_org,
+                               int h0, int32_t* err) {
   PutFrame stk[PUT_MAX_DEPTH];
-  int sp = 0;
   stk[0].f = f0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
   stk[0].arena = 0; stk[0].state = 0;
-  sp = 1;
+  int sp = 1;
   int64_t ret = 0;
   while (sp > 0) {
     PutFrame& F = stk[sp - 1];
     const int h = F.h;
     if (F.state == 0) {
       if (h <= PUT_LEAF) {
-        int64_t kb = 0;
-        if (threadIdx.x < 32) {
-          kb = put_strip_warp<PUT_CPL>(F.in_org, F.out_org, pay_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h,
-                                       P.cd, P.cm, P.cu);
-        }
-        cta_bcast_i64(kb, slot);
-        *fl += 5.0 * (3.0 * (double)h * h + h);  // cells of a (4h+2)-wide, h-high strip
+        const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
         --sp;
         continue;
       }
       const int h1 = (h + 1) / 2;
-      F.asm_org = frames + F.arena - (F.f - h1 + 1);
+      F.asm_org = X.frames + F.arena - (F.f - h1 + 1);
       // mid: cols f+h1+1 .. f+2h-h1 of row t+h1 from the 2h inputs
-      *fl += conv_valid(F.in_org + F.f + 1, 2 * (int64_t)h, F.asm_org + F.f + h1 + 1, 2 * (int64_t)(h - h1), h1, st,
-                 sbuf, CONV_LOGN_MAX);
+      put_conv(X, F.in_org + F.f + 1, 2 * (int64_t)h, F.asm_org + F.f + h1 + 1, 2 * (int64_t)(h - h1), h1);
       F.state = 1;
       PutFrame& C = stk[sp];
       C.f = F.f; C.h = h1; C.in_org = F.in_org; C.out_org = F.asm_org;
       C.arena = F.arena + 2 * (int64_t)h + 8; C.state = 0;
-      ++sp;
-      if (sp >= PUT_MAX_DEPTH) { *err = FL_E_CAPACITY | 1; return 0; }
+      if (++sp >= PUT_MAX_DEPTH) { *err = FL_E_CAPACITY | 1; return 0; }
     } else if (F.state == 1) {
       const int h1 = (h + 1) / 2, h2 = h - h1;
       const int64_t km = ret;
@@ -141,16 +136,14 @@ __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0
       F.km = km;
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;  // assembled cols km+1 .. f+2h-h1
       // bottom: cols km+h2+1 .. f+h of row t+h
-      *fl += conv_valid(F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2, st, sbuf,
-                 CONV_LOGN_MAX);
+      put_conv(X, F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2);
       F.state = 2;
       PutFrame& C = stk[sp];
       C.f = km; C.h = h2; C.in_org = F.asm_org; C.out_org = F.out_org;
       C.arena = F.arena + 2 * (int64_t)h + 8; C.state = 0;
       ++sp;
     } else {
-      const int h1 = (h + 1) / 2, h2 = h - h1;
-      (void)h1;
+      const int h2 = h - (h + 1) / 2;
       const int64_t kp = ret;
       if (kp < F.km - h2 || kp > F.km) { *err = FL_E_GEOMETRY | 3; return 0; }
       --sp;
@@ -160,93 +153,215 @@ __device__ int64_t put_solve_q(const PutParams& P, const Stencil& st, int64_t f0
 }
 
 __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, int64_t c) {
-  if (threadIdx.x == 0 && out.bt != nullptr && cnt < out.cap) {
+  if (lane_id() == 0 && out.bt != nullptr && cnt < out.cap) {
     out.bt[(int64_t)o * out.cap + cnt] = t;
     out.bc[(int64_t)o * out.cap + cnt] = c;
   }
   ++cnt;
 }
 
-__global__ void __launch_bounds__(CTA_THREADS, 2)
+// One option on chain warp c.
+__device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
+                                 unsigned char* kbuilt, const BatchOut& out, double* strip_flops) {
+  const int64_t n = P.n, ks = P.ks;
+  const PutLayout Lo = put_layout(n, ks);
+  double* bufA = arena;
+  double* bufB = arena + Lo.span;
+  double* pay = arena + 2 * Lo.span;
+  double* frames = arena + 3 * Lo.span;
+  double* kc = frames + 2 * n + 64 * PUT_MAX_DEPTH;
+  double* delta = kc + KCACHE_DOUBLES;
+  // delta buffer for direct-kernel builds (zeros, 1.0 at 2*DIRECT_H+1)
+  for (int i = lane_id(); i < DELTA_DOUBLES; i += 32) delta[i] = (i == 2 * DIRECT_H + 1) ? 1.0 : 0.0;
+  for (int i = lane_id(); i <= DIRECT_H; i += 32) kbuilt[i] = 0;
+  __syncwarp();
+  PutChainCtx X{&S, c, Stencil{P.cd, P.cm, P.cu, 2}, kc, kbuilt, delta, frames, pay - Lo.colbase, 0.0, out.prof};
+  const long long t_opt = clock64();
+  double* cur_org = bufA - Lo.colbase;
+  double* nxt_org = bufB - Lo.colbase;
+  // payoff table 1 - e^{col ds} (bsm.py:238-244) and the initial row (zeros on 1..ks+n)
+  {
+    Task t;
+    t.kind = TK_PUT_INIT;
+    t.x = nullptr; t.w = nullptr;
+    t.y = bufA;
+    t.L = Lo.span;
+    t.i0 = Lo.colbase;
+    t.d0 = P.ds;
+    t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0; t.Lout = 0;
+    issue(S, c, t, 0, 0, U(bufA), U(pay + Lo.span));
+  }
+  int32_t err = 0, cnt = 0;
+  int64_t m = 0, f = 0;
+  double price = 0.0;
+  put_record(out, o, cnt, 0, 0);
+  for (;;) {
+    const int64_t rem = n - m;
+    const int64_t red = ks + rem - f;
+    if (red < 0) { err = FL_E_GEOMETRY | 4; break; }
+    if (red == 0) { price = P.K * (1.0 - exp((double)ks * P.ds)); break; }
+    if (rem <= 2 * (int64_t)P.cutoff) {
+      if (2 * rem + 2 > SCHED_SLOTS) { err = FL_E_CAPACITY | 2; break; }
+      Task t;
+      t.kind = TK_PUT_APEX;
+      t.x = cur_org; t.w = X.pay_org; t.y = nullptr;
+      t.i0 = f; t.i1 = rem; t.i2 = ks;
+      t.c0 = P.cd; t.c1 = P.cm; t.c2 = P.cu; t.h = 0; t.span = 2; t.L = 0; t.Lout = 0;
+      const int idx = issue(S, c, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
+      wait_task(S, idx);
+      price = P.K * S.result[c];
+      X.flops += 5.0 * ((double)rem * rem + rem);
+      break;
+    }
+    const int64_t hh = (rem / 2 < red / 2) ? rem / 2 : red / 2;
+    if (hh < 1) {
+      const int64_t kb = put_leaf(X, P, cur_org, nxt_org, f - 3, f + 1, f, 1);
+      if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
+      f = kb;
+      m += 1;
+    } else {
+      const int h = (int)hh;
+      if (red > 2 * hh)  // far: cols f+h+1 .. ks+rem-h stay linear
+        put_conv(X, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h);
+      const int64_t kp = put_solve_q(X, P, f, cur_org, nxt_org, h, &err);
+      if (err) break;
+      f = kp;
+      m += hh;
+    }
+    put_record(out, o, cnt, m, f);
+    double* t = cur_org;
+    cur_org = nxt_org;
+    nxt_org = t;
+  }
+  wait_all_own(S, c);  // the next option reuses this arena
+  if (lane_id() == 0) prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
+  if (lane_id() == 0) {
+    out.price[o] = err ? 0.0 : price;
+    out.status[o] = err;
+    if (out.bcount) out.bcount[o] = err ? 0 : cnt;
+  }
+  *strip_flops += X.flops;
+}
+
+// Worker-side execution of the put-specific tasks.
+__device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, const Grp& g) {
+  if (t.kind == TK_PUT_INIT) {
+    double* A = t.y;
+    double* pay = t.y + 2 * t.L;
+    for (int64_t i = g.t; i < t.L; i += g.n) {
+      A[i] = 0.0;
+      pay[i] = 1.0 - exp((double)(t.i0 + i) * t.d0);
+    }
+    return 0.0;
+  }
+  if (t.kind == TK_PUT_APEX) {
+    // apex cone sweep (bsm._apex_finish) restricted to [ks-rem-1, ks+rem]
+    const double* cur_org = t.x;
+    const double* pay_org = t.w;
+    const int64_t f = t.i0, rem = t.i1, ks = t.i2;
+    const int64_t lo = ks - rem - 1, hi = ks + rem;
+    const int W = (int)(hi - lo + 1);
+    double* a = (double*)sbuf;
+    double* b = a + SCHED_SLOTS;
+    for (int i = g.t; i < W; i += g.n) {
+      const int64_t col = lo + i;
+      a[i] = (col <= f) ? pay_org[col] : cur_org[col];
+      b[i] = a[i];
+    }
+    gsync(g);
+    for (int s = 1; s <= rem; ++s) {
+      for (int i = s + g.t; i <= W - 1 - s; i += g.n) {
+        const double lin = fma(t.c0, a[i - 1], fma(t.c2, a[i + 1], t.c1 * a[i]));
+        const double p = pay_org[lo + i];
+        b[i] = lin > p ? lin : p;
+      }
+      gsync(g);
+      double* tmp = a;
+      a = b;
+      b = tmp;
+    }
+    if (g.t == 0) S.result[t.chain] = a[ks - lo];
+    return 0.0;
+  }
+  return exec_generic(t, sbuf, g);
+}
+
+__global__ void __launch_bounds__(SCHED_THREADS, 1)
 put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
   extern __shared__ double2 sbuf[];
-  __shared__ int s_work;
-  __shared__ int64_t s_slot;
-  double* arena = ws + (int64_t)blockIdx.x * ws_stride;
-  for (;;) {
-    if (threadIdx.x == 0) s_work = atomicAdd(counter, 1);
-    __syncthreads();
-    const int w = s_work;
-    __syncthreads();
-    if (w >= nwork) break;
-    const int o = order[w];
-    const PutParams P = opts[o];
-    const int64_t n = P.n, ks = P.ks;
-    const PutLayout Lo = put_layout(n, ks);
-    double* bufA = arena;
-    double* bufB = arena + Lo.span;
-    double* pay = arena + 2 * Lo.span;
-    double* frames = arena + 3 * Lo.span;
-    double* pay_org = pay - Lo.colbase;
-    double* cur_org = bufA - Lo.colbase;
-    double* nxt_org = bufB - Lo.colbase;
-    // payoff table 1 - e^{col ds} (bsm.py:238-244) and the initial row: zeros on 1..ks+n
-    for (int64_t i = threadIdx.x; i < Lo.span; i += CTA_THREADS) {
-      const int64_t col = Lo.colbase + i;
-      pay[i] = 1.0 - exp((double)col * P.ds);
-      bufA[i] = 0.0;
-    }
-    __syncthreads();
-    const Stencil st{P.cd, P.cm, P.cu, 2};
-    int32_t err = 0, cnt = 0;
-    int64_t m = 0, f = 0;
-    double price = 0.0, flops = 0.0;
-    put_record(out, o, cnt, 0, 0);
+  __shared__ SchedShared S;
+  __shared__ unsigned char kbuilt[NCHAIN][DIRECT_H + 1];
+  sched_init(S);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp >= NWORKER_WARPS) {  // chain warps take the highest warp ids: the issue arbiter favours them
+    // ---- chain warp
+    const int c = warp - NWORKER_WARPS;
+    double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
+    double strip_flops = 0.0;
     for (;;) {
-      const int64_t rem = n - m;
-      const int64_t red = ks + rem - f;
-      if (red < 0) { err = FL_E_GEOMETRY | 4; break; }
-      if (red == 0) { price = P.K * (1.0 - exp((double)ks * P.ds)); break; }
-      if (rem <= 2 * (int64_t)P.cutoff) {
-        if (2 * rem + 2 > CONV_SLOTS) { err = FL_E_CAPACITY | 2; break; }
-        price = P.K * put_apex(P, cur_org, pay_org, f, rem, (double*)sbuf, ((double*)sbuf) + CONV_SLOTS, &s_slot);
-        flops += 5.0 * ((double)rem * rem + rem);
-        break;
-      }
-      const int64_t hh = (rem / 2 < red / 2) ? rem / 2 : red / 2;
-      if (hh < 1) {
-        int64_t kb = 0;
-        if (threadIdx.x < 32)
-          kb = put_strip_warp<PUT_CPL>(cur_org, nxt_org, pay_org, f - 3, f + 1, f, 1, P.cd, P.cm, P.cu);
-        cta_bcast_i64(kb, &s_slot);
-        flops += 15.0;
-        if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
-        f = kb;
-        m += 1;
-      } else {
-        const int h = (int)hh;
-        if (red > 2 * hh)  // far: cols f+h+1 .. ks+rem-h stay linear
-          flops += conv_valid(cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, st, sbuf, CONV_LOGN_MAX);
-        const int64_t kp =
-            put_solve_q(P, st, f, cur_org, nxt_org, h, pay_org, frames, sbuf, &s_slot, &err, &flops);
-        if (err) break;
-        f = kp;
-        m += hh;
-      }
-      put_record(out, o, cnt, m, f);
-      double* t = cur_org;
-      cur_org = nxt_org;
-      nxt_org = t;
+      int w = 0;
+      if (lane_id() == 0) w = atomicAdd(counter, 1);
+      w = __shfl_sync(FULL, w, 0);
+      if (w >= nwork) break;
+      const int o = order[w];
+      put_chain_option(S, c, opts[o], o, arena, kbuilt[c], out, &strip_flops);
     }
-    if (threadIdx.x == 0) {
-      out.price[o] = err ? 0.0 : price;
-      out.status[o] = err;
-      if (out.bcount) out.bcount[o] = err ? 0 : cnt;
-      if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
+    if (lane_id() == 0) {
+      if (out.flops) atomicAdd(out.flops, (unsigned long long)strip_flops);
+      if (atomicSub(&S.chains_left, 1) == 1) {
+        // last chain out: stop the workers
+        const int idx = atomicAdd(&S.reserve, 1);
+        while (idx - S.done >= QCAP) __nanosleep(64);
+        Task& s = S.ring[idx % QCAP];
+        s.kind = TK_EXIT;
+        __threadfence_block();
+        s.seq = idx;
+      }
     }
-    __syncthreads();
+    return;
   }
+  // ---- worker warps
+  const Grp g{(int)threadIdx.x, WORKERS, WORKER_BAR};
+  double flops = 0.0;
+  unsigned long long* prof = out.prof;
+  const long long t_start = clock64();
+  for (int next = 0;; ++next) {
+    Task& slot = S.ring[next % QCAP];
+    long long t0 = clock64();
+    if (g.t == 0) {
+      while (slot.seq != next) __nanosleep(20);
+    }
+    gsync(g);
+    long long t1 = clock64();
+    if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+    __threadfence_block();
+    Task t;
+    t.x = slot.x; t.y = slot.y; t.w = slot.w; t.L = slot.L; t.Lout = slot.Lout;
+    t.c0 = slot.c0; t.c1 = slot.c1; t.c2 = slot.c2; t.h = slot.h; t.span = slot.span; t.kind = slot.kind;
+    t.chain = slot.chain; t.i0 = slot.i0; t.i1 = slot.i1; t.i2 = slot.i2; t.i3 = slot.i3;
+    t.d0 = slot.d0; t.d1 = slot.d1; t.d2 = slot.d2; t.d3 = slot.d3; t.d4 = slot.d4;
+    if (t.kind == TK_EXIT) break;
+    const double fl = put_exec_task(S, t, sbuf, g);
+    flops += fl > 0 ? fl : 0.0;
+    gsync(g);
+    if (g.t == 0) {
+      __threadfence();
+      S.done = next + 1;
+      if (prof) {
+        const long long dt = clock64() - t1;
+        const int slot0 = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC
+                        : (t.kind == TK_KBUILD) ? PROF_KB_CYC : PROF_OTHER_CYC;
+        prof_add(prof, slot0, dt);
+        prof_add(prof, slot0 + 1, 1);
+        if (t.kind == TK_FFT) prof_add(prof, PROF_FFT_LOUT, t.Lout);
+        if (t.kind == TK_DIRECT) prof_add(prof, PROF_DIR_LOUT, t.Lout);
+      }
+    }
+  }
+  if (g.t == 0 && out.flops) atomicAdd(out.flops, (unsigned long long)flops);
+  if (g.t == 0) prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
 }
 
 // ---------------------------------------------------------------------------
@@ -312,7 +427,8 @@ put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restric
 // ---------------------------------------------------------------------------
 // launchers
 
-int put_fast_smem_bytes() { return CONV_SLOTS * (int)sizeof(double2); }
+int put_fast_smem_bytes() { return SCHED_SLOTS * (int)sizeof(double2); }
+int put_chains_per_cta() { return NCHAIN; }
 
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream) {
@@ -326,7 +442,7 @@ cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwo
   if (nwork <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
   if (e != cudaSuccess) return e;
-  put_fast_kernel<<<grid, CTA_THREADS, smem, stream>>>(opts, order, nwork, counter, ws, ws_stride, out);
+  put_fast_kernel<<<grid, SCHED_THREADS, smem, stream>>>(opts, order, nwork, counter, ws, ws_stride, out);
   return cudaGetLastError();
 }
 
