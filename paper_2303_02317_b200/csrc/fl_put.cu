@@ -88,13 +88,19 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + hi + 1), U(X.pay_org + lo), U(X.pay_org + hi + 1),
                  U(out_org + lo), U(out_org + hi + 1));
   const long long t1 = clock64();
-  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu);
+  if (X.prof && __activemask() != FULL && lane_id() == 0) prof_add(X.prof, PROF_DIVERGED, 1);
+  __syncwarp();
+  long long tm[2] = {0, 0};
+  const int64_t kb =
+      put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu, X.prof ? tm : nullptr);
   if (X.prof && lane_id() == 0) {
     const long long t2 = clock64();
     prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
     prof_add(X.prof, PROF_WAIT_N, (t1 - t0) > 200 ? 1 : 0);
     prof_add(X.prof, PROF_STRIP_CYC, t2 - t1);
     prof_add(X.prof, PROF_STRIP_N, height);
+    prof_add(X.prof, PROF_ISSUE_CYC, tm[1]);      // row loop only
+    prof_add(X.prof, PROF_QFULL_CYC, tm[0] - t1);  // loads before the loop
   }
   const double W = (double)(hi - lo + 1);
   X.flops += 5.0 * (W * height - (double)height * (height + 1));
@@ -172,8 +178,14 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
   double* kc = frames + 2 * n + 64 * PUT_MAX_DEPTH;
   double* delta = kc + KCACHE_DOUBLES;
   // delta buffer for direct-kernel builds (zeros, 1.0 at 2*DIRECT_H+1)
-  for (int i = lane_id(); i < DELTA_DOUBLES; i += 32) delta[i] = (i == 2 * DIRECT_H + 1) ? 1.0 : 0.0;
-  for (int i = lane_id(); i <= DIRECT_H; i += 32) kbuilt[i] = 0;
+  for (int b = 0; b < DELTA_DOUBLES; b += 32) {  // uniform trip counts keep the warp converged
+    const int i = b + lane_id();
+    if (i < DELTA_DOUBLES) delta[i] = (i == 2 * DIRECT_H + 1) ? 1.0 : 0.0;
+  }
+  for (int b = 0; b <= DIRECT_H; b += 32) {
+    const int i = b + lane_id();
+    if (i <= DIRECT_H) kbuilt[i] = 0;
+  }
   __syncwarp();
   PutChainCtx X{&S, c, Stencil{P.cd, P.cm, P.cu, 2}, kc, kbuilt, delta, frames, pay - Lo.colbase, 0.0, out.prof};
   const long long t_opt = clock64();

@@ -76,7 +76,7 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 enum : int {
   PROF_FFT_CYC = 0, PROF_FFT_N, PROF_DIR_CYC, PROF_DIR_N, PROF_KB_CYC, PROF_KB_N, PROF_OTHER_CYC, PROF_OTHER_N,
   PROF_STRIP_CYC, PROF_STRIP_N, PROF_WAIT_CYC, PROF_WAIT_N, PROF_ISSUE_CYC, PROF_KERNEL_CYC, PROF_IDLE_CYC,
-  PROF_FFT_LOUT, PROF_DIR_LOUT, PROF_CHAIN_CYC, PROF_QFULL_CYC,
+  PROF_FFT_LOUT, PROF_DIR_LOUT, PROF_CHAIN_CYC, PROF_QFULL_CYC, PROF_DIVERGED,
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
@@ -105,9 +105,11 @@ __device__ int issue(SchedShared& S, int c, const Task& t, uintptr_t rlo, uintpt
   __threadfence_block();  // this lane's earlier global writes before the publish
   __syncwarp();
   int idx = 0;
+  if (lane_id() == 0) idx = atomicAdd(&S.reserve, 1);
+  idx = __shfl_sync(FULL, idx, 0);
+  // warp-uniform spin (a lane-0-only loop would leave the warp split)
+  while (idx - __shfl_sync(FULL, S.done, 0) >= QCAP) __nanosleep(64);
   if (lane_id() == 0) {
-    idx = atomicAdd(&S.reserve, 1);
-    while (idx - S.done >= QCAP) __nanosleep(64);
     Task& s = S.ring[idx % QCAP];
     s.x = t.x; s.y = t.y; s.w = t.w; s.L = t.L; s.Lout = t.Lout;
     s.c0 = t.c0; s.c1 = t.c1; s.c2 = t.c2; s.h = t.h; s.span = t.span; s.kind = t.kind; s.chain = c;
@@ -119,17 +121,13 @@ __device__ int issue(SchedShared& S, int c, const Task& t, uintptr_t rlo, uintpt
     __threadfence_block();
     s.seq = idx;
   }
-  idx = __shfl_sync(FULL, idx, 0);
   __syncwarp();
   return idx;
 }
 
 // Chain waits until task `idx` (and so every earlier task) has completed.
 __device__ __forceinline__ void wait_task(SchedShared& S, int idx) {
-  if (lane_id() == 0) {
-    while (S.done <= idx) __nanosleep(32);
-  }
-  __syncwarp();
+  while (__shfl_sync(FULL, S.done, 0) <= idx) __nanosleep(32);  // warp-uniform spin
   __threadfence_block();
 }
 
@@ -141,12 +139,18 @@ __device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1
   const int np = S.npend[c];
   int need = -1;
   const int first = np > QCAP ? np - QCAP : 0;
-  for (int i = first + lane_id(); i < np; i += 32) {
-    const Pend& p = S.pend[c][i % QCAP];
-    if (p.idx < done) continue;
-    const bool raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
-    const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
-    if ((raw || war) && p.idx > need) need = p.idx;
+  // warp-uniform trip count: keeps the chain warp converged (a lane-dependent
+  // loop bound here splits the warp and sends later shuffles down the slow
+  // collective path)
+  for (int base = first; base < np; base += 32) {
+    const int i = base + lane_id();
+    if (i < np) {
+      const Pend& p = S.pend[c][i % QCAP];
+      const bool live = p.idx >= done;
+      const bool raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
+      const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
+      if (live && (raw || war) && p.idx > need) need = p.idx;
+    }
   }
   need = __reduce_max_sync(FULL, need);
   if (need >= 0) wait_task(S, need);

@@ -12,7 +12,7 @@ db = _native.DeviceBatch(b.kind, b.S, b.K, b.R, b.Y, b.V, b.E, b.T)
 db.run(); db.fetch()
 t0 = time.perf_counter(); db.run(); r = db.fetch(); t1 = time.perf_counter()
 p = db.profile().astype(np.float64)
-names = ["FFT_CYC","FFT_N","DIR_CYC","DIR_N","KB_CYC","KB_N","OTHER_CYC","OTHER_N","STRIP_CYC","STRIP_ROWS","WAIT_CYC","WAIT_N","ISSUE_CYC","KERNEL_CYC","IDLE_CYC","FFT_LOUT","DIR_LOUT","CHAIN_CYC","QFULL"]
+names = ["FFT_CYC","FFT_N","DIR_CYC","DIR_N","KB_CYC","KB_N","OTHER_CYC","OTHER_N","STRIP_CYC","STRIP_ROWS","WAIT_CYC","WAIT_N","ROWLOOP_CYC","KERNEL_CYC","IDLE_CYC","FFT_LOUT","DIR_LOUT","CHAIN_CYC","LOADS_CYC","DIVERGED"]
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
 for i, nm in enumerate(names):
     print(f"{nm:12s} {p[i]:.4g}")
