@@ -40,8 +40,9 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    extra = os.environ.get("FL_NVCC_FLAGS", "").split()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", "-o", LIB + ".tmp", os.path.join(CSRC, "fl_lib.cu")]
+           "-Xptxas", "-warn-spills", *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "fl_lib.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

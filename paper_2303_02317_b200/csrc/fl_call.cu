@@ -164,7 +164,7 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       const int64_t lo = F.j - h + 1;
       F.asm_org = frames + F.arena - lo;
       // mid: cols lo .. j-h1 of row i-h1
-      *fl += conv_fft(F.in_org + lo, h, F.asm_org + lo, h2, h1, st, sbuf, CALL_LOGN_MAX, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+      *fl += conv_fft(F.in_org + lo, h, F.asm_org + lo, h2, h1, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
       F.state = 1;
       CallFrame& C = stk[sp];
       C.i = F.i; C.j = F.j; C.h = h1; C.in_org = F.in_org; C.out_org = F.asm_org;
@@ -177,7 +177,7 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       const int64_t lo = F.j - h + 1;
       const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
       // bottom: cols lo .. jm-h2 of row i-h
-      *fl += conv_fft(F.asm_org + lo, A, F.out_org + lo, A - h2, h2, st, sbuf, CALL_LOGN_MAX, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+      *fl += conv_fft(F.asm_org + lo, A, F.out_org + lo, A - h2, h2, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
       F.state = 2;
       CallFrame& C = stk[sp];
       C.i = F.i - h1; C.j = jm; C.h = h2; C.in_org = F.asm_org; C.out_org = F.out_org;
@@ -247,7 +247,7 @@ call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict_
       const int64_t hh = (j + 1 < i - resid) ? j + 1 : i - resid;
       const int h = (int)hh;
       // left: cols 0 .. j-h of row i-h (american.py:341-344)
-      if (j + 1 > hh) flops += conv_fft(cur, j + 1, nxt, j + 1 - hh, h, st, sbuf, CALL_LOGN_MAX, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+      if (j + 1 > hh) flops += conv_fft(cur, j + 1, nxt, j + 1 - hh, h, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
       const int64_t jp = call_solve(P, st, i, j, h, cur, nxt, frames, 0, sbuf, &s_slot, &err, &flops);
       if (err) break;
       i -= hh;

@@ -26,8 +26,9 @@ __device__ __forceinline__ double cnorm2(double2 a) { return fma(a.x, a.x, a.y *
 // ---------------------------------------------------------------------------
 // Twiddle table: fl_tw[m] = exp(-2 pi i m / TW_N), TW_N = largest real block.
 
-constexpr int TW_LOG = 14;
+constexpr int TW_LOG = 13;
 constexpr int TW_N = 1 << TW_LOG;
+constexpr int TWQ = TW_N / 4;  // quarter-wave table length (entries 0..TWQ-1 suffice)
 
 // Defined here: the library is one translation unit (csrc/fl_lib.cu).
 __device__ double2 fl_tw[TW_N];
@@ -36,6 +37,18 @@ __device__ __forceinline__ double2 tw_get(int m) { return __ldg(&fl_tw[m]); }
 
 // W_L^m = exp(-2 pi i m / L) for L a power of two <= TW_N.
 __device__ __forceinline__ double2 tw_l(int m, int log_l) { return tw_get(m << (TW_LOG - log_l)); }
+
+// exp(-2 pi i m / TW_N), m in [0, TW_N), from a quarter-wave table tq[0..TWQ)
+// (shared memory or the global fl_tw): W^(m+TWQ) = -i W^m.
+__device__ __forceinline__ double2 twq(const double2* tq, int m) {
+  // branch-free: lanes of a warp sit in different quadrants
+  const double2 b = tq[m & (TWQ - 1)];
+  const int q = m >> (TW_LOG - 2);
+  const double x = (q & 1) ? b.y : b.x;
+  const double y = (q & 1) ? -b.x : b.y;
+  const double s = (q & 2) ? -1.0 : 1.0;
+  return make_double2(s * x, s * y);
+}
 
 // ---------------------------------------------------------------------------
 // warp helpers

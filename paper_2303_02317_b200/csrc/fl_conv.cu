@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(CTA_THREADS)
 linear_steps_kernel(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
                     Stencil st) {
   extern __shared__ double2 sbuf[];
-  conv_fft(x, L, y, Lout, h, st, sbuf, LS_LOGN_MAX, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+  conv_fft(x, L, y, Lout, h, st, sbuf, LS_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
 }
 
 int linear_steps_smem_bytes() { return smem_complex_slots(1 << (LS_LOGN_MAX - 1)) * (int)sizeof(double2); }

@@ -1,6 +1,6 @@
 // fl_conv.cuh -- fp64 valid-mode correlation with a composed stencil power,
-// executed by a thread group (a whole CTA, or the worker warps of a
-// warp-specialised CTA).
+// executed by a thread group (one warp, the worker warps of a warp-specialised
+// CTA, or a whole CTA).
 //
 // Replaces the reference's `convolve` / `_valid_corr` / `kernel_power`
 // (fft.py:130-163, 203-260; american.py:180-184; bsm.py:384-387):
@@ -20,13 +20,16 @@
 //    outputs with Mw ~ 20 sqrt(h) instead of 2h+1: every block fits in shared
 //    memory and nothing is padded to next_pow2(L+M-1).  The dropped tail is
 //    < 1e-21 of max|x|, far below the reference FFT's own ~1e-16 rounding.
-//    Real-to-complex packing (N real = N/2 complex); in-place Stockham radix-16
-//    passes in registers over a padded (bank-conflict-free) shared layout;
-//    twiddles from a global fp64 table; the real split, spectrum multiply and
-//    inverse pre-twist are one fused shared-memory pass.
-//  * conv_direct -- small kernels (h <= DIRECT_H): explicit dot products
-//    against cached real-space weights (built once per option and height by
-//    conv_fft on a delta), shared-memory staged.
+//    Real-to-complex packing (N real = N/2 complex).  The complex transform is
+//    in place: decimation-in-frequency radix-16 stages forward (natural ->
+//    digit-reversed), decimation-in-time stages back (digit-reversed ->
+//    natural), so no reordering pass exists and any number of threads can
+//    share a stage (each butterfly writes back to the slots it read).  The
+//    real split, spectrum multiply and inverse re-pack are one fused pass over
+//    digit-reversed slots.  Twiddles come from a quarter-wave fp64 table.
+//  * conv_direct -- small kernels: explicit dot products against cached
+//    real-space weights (built once per option and height by conv_fft on a
+//    delta), shared-memory staged.
 #pragma once
 
 #include "fl_common.cuh"
@@ -35,13 +38,18 @@ namespace fl {
 
 constexpr int CTA_THREADS = 256;
 
-// A cooperating thread group: index t in [0, n), named barrier `bar`.
+// A cooperating thread group: index t in [0, n); bar >= 0 -> named barrier,
+// bar < 0 -> the group is one warp (n == 32).
 struct Grp {
   int t, n, bar;
 };
 
 __device__ __forceinline__ void gsync(const Grp& g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(g.bar), "r"(g.n) : "memory");
+  if (g.bar < 0) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(g.bar), "r"(g.n) : "memory");
+  }
 }
 
 // padded shared-memory index: one spare slot every 16 complex values
@@ -99,46 +107,115 @@ __device__ __forceinline__ void fft_reg(double2 (&v)[R]) {
   }
 }
 
-// One in-place Stockham DIT pass of radix R over C complex points (C/R <= g.n).
+// ---------------------------------------------------------------------------
+// In-place mixed-radix transform of C = 2^logC complex points.  Stage radices:
+// 16, 16, ..., then 2/4/8 for the remainder (last DIF stage, smallest span).
+
+// w[q] = w1^q, q = 1..R-1, by a product tree of depth log2(R) (one table
+// lookup per butterfly: strided table reads are heavily bank-conflicted).
 template <int R>
-__device__ __forceinline__ void stockham_pass(double2* buf, int C, int Ns, int logNsR, const Grp& g) {
-  const int nb = C / R;
-  const int j = g.t;
-  double2 v[R];
-  const bool act = j < nb;
-  if (act) {
+__device__ __forceinline__ void tw_powers(double2 w1, double2 (&w)[R]) {
+  w[1] = w1;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[pidx(j + r * nb)];
-    const int k = j & (Ns - 1);
-    if (Ns > 1) {
+  for (int q = 2; q < R; ++q) w[q] = cmul(w[q / 2], w[q - q / 2]);
+}
+
+__device__ __forceinline__ int last_radix_log(int logC) {
+  const int r = logC & 3;
+  return r ? r : 4;
+}
+
+// DIF stage of radix R on spans of S = 2^logS points.
+template <int R>
+__device__ __forceinline__ void dif_stage(double2* buf, int logC, int logS, const double2* tq, const Grp& g) {
+  constexpr int LR = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : 4;
+  const int nb = 1 << (logC - LR);
+  const int lstride = logS - LR;  // stride = S / R
+  const int jmask = (1 << lstride) - 1;
+  const int tshift = TW_LOG - logS;
+#pragma unroll 1
+  for (int u = g.t; u < nb; u += g.n) {
+    const int j = u & jmask;
+    const int base = ((u >> lstride) << logS) + j;
+    double2 v[R];
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw_l(r * k, logNsR));
-    }
+    for (int r = 0; r < R; ++r) v[r] = buf[pidx(base + (r << lstride))];
     fft_reg<R>(v);
-  }
-  gsync(g);
-  if (act) {
-    const int k = j & (Ns - 1);
-    const int d = (j - k) * R + k;
+    double2 w[R];
+    tw_powers<R>(twq(tq, j << tshift), w);
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[pidx(d + r * Ns)] = v[r];
+    for (int q = 1; q < R; ++q) v[q] = cmul(v[q], w[q]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) buf[pidx(base + (q << lstride))] = v[q];
   }
   gsync(g);
 }
 
-// Forward complex FFT of C = 2^logC points (32 <= C <= 16 * g.n), in place, natural order.
-__device__ __noinline__ void fft_grp(double2* buf, int logC, Grp g) {
-  const int C = 1 << logC;
-  int rem = logC % 4;
-  int Ns = 1, logNs = 0;
-  if (rem == 1) { stockham_pass<2>(buf, C, Ns, logNs + 1, g); Ns <<= 1; logNs += 1; }
-  else if (rem == 2) { stockham_pass<4>(buf, C, Ns, logNs + 2, g); Ns <<= 2; logNs += 2; }
-  else if (rem == 3) { stockham_pass<8>(buf, C, Ns, logNs + 3, g); Ns <<= 3; logNs += 3; }
-  while (logNs < logC) {
-    stockham_pass<16>(buf, C, Ns, logNs + 4, g);
-    Ns <<= 4;
-    logNs += 4;
+// Inverse (DIT) stage: undoes dif_stage<R> up to the factor R.
+template <int R>
+__device__ __forceinline__ void dit_stage(double2* buf, int logC, int logS, const double2* tq, const Grp& g) {
+  constexpr int LR = (R == 2) ? 1 : (R == 4) ? 2 : (R == 8) ? 3 : 4;
+  const int nb = 1 << (logC - LR);
+  const int lstride = logS - LR;
+  const int jmask = (1 << lstride) - 1;
+  const int tshift = TW_LOG - logS;
+#pragma unroll 1
+  for (int u = g.t; u < nb; u += g.n) {
+    const int j = u & jmask;
+    const int base = ((u >> lstride) << logS) + j;
+    double2 v[R];
+    // IDFT(conj-twiddled x) = conj(DFT(conj(x conj(w)))) = conj(DFT(conj(x) w))
+    double2 w[R];
+    tw_powers<R>(twq(tq, j << tshift), w);
+    v[0] = cconj(buf[pidx(base)]);
+#pragma unroll
+    for (int q = 1; q < R; ++q) v[q] = cmul(cconj(buf[pidx(base + (q << lstride))]), w[q]);
+    fft_reg<R>(v);
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pidx(base + (r << lstride))] = cconj(v[r]);
   }
+  gsync(g);
+}
+
+// Forward: natural order in, X[k] at slot P(k) out.
+__device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* tq, Grp g) {
+  const int lr = last_radix_log(logC);
+  int logS = logC;
+  while (logS > lr) {
+    dif_stage<16>(buf, logC, logS, tq, g);
+    logS -= 4;
+  }
+  if (lr == 1) dif_stage<2>(buf, logC, logS, tq, g);
+  else if (lr == 2) dif_stage<4>(buf, logC, logS, tq, g);
+  else if (lr == 3) dif_stage<8>(buf, logC, logS, tq, g);
+  else dif_stage<16>(buf, logC, logS, tq, g);
+}
+
+// Inverse (unnormalised, x C): slot P(k) in, natural order out.
+__device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g) {
+  const int lr = last_radix_log(logC);
+  if (lr == 1) dit_stage<2>(buf, logC, lr, tq, g);
+  else if (lr == 2) dit_stage<4>(buf, logC, lr, tq, g);
+  else if (lr == 3) dit_stage<8>(buf, logC, lr, tq, g);
+  else dit_stage<16>(buf, logC, lr, tq, g);
+  for (int logS = lr + 4; logS <= logC; logS += 4) dit_stage<16>(buf, logC, logS, tq, g);
+}
+
+// Slot holding frequency k after fft_dif: digits of k (radix 16 from the
+// least significant end, the last remainder digit most significant in k)
+// written most-significant-first into the slot index.
+__device__ __forceinline__ int slot_of(int k, int logC) {
+  const int lr = last_radix_log(logC);
+  const int nfull = (logC - lr) / 4;  // radix-16 stages
+  int p = 0;
+  int logS = logC;
+#pragma unroll 1
+  for (int s = 0; s < nfull; ++s) {
+    logS -= 4;
+    p |= (k & 15) << logS;
+    k >>= 4;
+  }
+  return p | k;  // remainder digit (< 2^lr) in the lowest lr bits
 }
 
 // ---------------------------------------------------------------------------
@@ -150,17 +227,16 @@ struct Stencil {
 };
 
 struct ConvPlan {
-  int64_t rlo;     // first kernel index kept in the window
-  int64_t P;       // valid outputs per block
-  int logN;        // real block size N = 2^logN
-  double tau;      // |P(e^{i th})|^2 below tau -> |P|^h < 1e-24 -> bin zeroed
+  int64_t rlo;  // first kernel index kept in the window
+  int64_t P;    // valid outputs per block
+  int logN;     // real block size N = 2^logN
+  double tau;   // |P(e^{i th})|^2 below tau -> |P|^h < 1e-24 -> bin zeroed
 };
 
 constexpr double LN_2_OVER_EPS = 50.656872045869936;  // ln(2 / 2e-22)
 
-// Window + block plan for one task; uniform across the group (every thread computes it).
-__device__ __forceinline__ ConvPlan plan_conv(const Stencil& st, int h, int64_t Lout, int logNmax) {
-  ConvPlan p;
+// Hoeffding window width Mw of W_h (rlo/rhi clamped to [0, M-1]).
+__host__ __device__ inline int64_t window_width(const Stencil& st, int h, int64_t* rlo_out) {
   const int64_t M = (int64_t)h * st.span + 1;
   const double mass = st.c0 + st.c1 + st.c2;
   const double mu = (double)h * (st.c1 + 2.0 * st.c2) / mass;
@@ -169,7 +245,15 @@ __device__ __forceinline__ ConvPlan plan_conv(const Stencil& st, int h, int64_t 
   int64_t rhi = (int64_t)ceil(mu + t) + 1;
   if (rlo < 0) rlo = 0;
   if (rhi > M - 1) rhi = M - 1;
-  const int64_t Mw = rhi - rlo + 1;
+  if (rlo_out) *rlo_out = rlo;
+  return rhi - rlo + 1;
+}
+
+// Window + block plan for one task; uniform across the group (every thread computes it).
+__device__ __forceinline__ ConvPlan plan_conv(const Stencil& st, int h, int64_t Lout, int logNmax) {
+  ConvPlan p;
+  int64_t rlo;
+  const int64_t Mw = window_width(st, h, &rlo);
   const int64_t need = Lout + Mw - 1;
   int logN = 6;
   while (logN < logNmax && ((int64_t)1 << logN) < need) ++logN;
@@ -203,12 +287,12 @@ __device__ __forceinline__ double2 spectrum(const Stencil& st, double2 om, doubl
 
 // ---------------------------------------------------------------------------
 // FFT executor.  y[k] = sum_r W_h[r] x[k+r], k in [0, Lout); x has L >= Lout + h*span
-// values.  buf: smem_complex_slots(2^(logNmax-1)) double2.  Returns the executed
-// fp64 flops (FFT convention 5 C log2 C per complex transform, two per block,
-// plus 16 C for the split / spectrum / re-pack pass).  P < 1 (window wider
-// than the largest block) returns -1.
+// values.  buf: smem_complex_slots(2^(logNmax-1)) double2; tq: quarter-wave
+// twiddle table (shared or global).  Returns the executed fp64 flops (FFT
+// convention 5 C log2 C per complex transform, two per block, plus 16 C for
+// the split / spectrum / re-pack pass); -1 if the window exceeds the block.
 __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
-                           const Stencil& st, double2* buf, int logNmax, const Grp& g) {
+                           const Stencil& st, double2* buf, int logNmax, const double2* tq, const Grp& g) {
   if (Lout <= 0) return 0.0;
   const ConvPlan pl = plan_conv(st, h, Lout, logNmax);
   if (pl.P < 1) return -1.0;
@@ -216,6 +300,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
   const int logC = logN - 1;
   const int C = 1 << logC;
   const int N = 1 << logN;
+  const int tsh = TW_LOG - logN;  // W_N^k = twq(k << tsh)
   const double inv_c = 1.0 / (double)C;
   const int64_t rlo_modN = pl.rlo & (N - 1);
   const double rlo_sign = (pl.rlo & 1) ? -1.0 : 1.0;
@@ -224,7 +309,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
     const int64_t s0 = k0 + pl.rlo;
-#pragma unroll 1
+#pragma unroll 4
     for (int n = g.t; n < C; n += g.n) {
       const int64_t i0 = s0 + 2 * (int64_t)n;
       const double a = (i0 < L) ? x[i0] : 0.0;
@@ -232,14 +317,20 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       buf[pidx(n)] = make_double2(a, b);
     }
     gsync(g);
-    fft_grp(buf, logC, g);
-    // -- split to the real spectrum, multiply, re-pack for the inverse (conjugated, /C)
+    fft_dif(buf, logC, tq, g);
+    // -- split to the real spectrum, multiply, re-pack for the inverse (/C)
+    // W_N^k and the window phase W_N^(k rlo) advance by fixed steps per iteration
+    // (one table lookup each instead of conflicted strided lookups per bin)
+    double2 Wk = twq(tq, (g.t & (N - 1)) << tsh);
+    double2 ph = twq(tq, (int)(((int64_t)g.t * rlo_modN) & (N - 1)) << tsh);
+    const double2 Wstep = twq(tq, (g.n & (N - 1)) << tsh);
+    const double2 phstep = twq(tq, (int)(((int64_t)g.n * rlo_modN) & (N - 1)) << tsh);
 #pragma unroll 1
     for (int k = g.t; k <= C / 2; k += g.n) {
       const int kc = (C - k) & (C - 1);
-      const double2 Zk = buf[pidx(k)];
-      const double2 Zc = buf[pidx(kc)];
-      const double2 Wk = tw_l(k, logN);  // exp(-2 pi i k / N)
+      const int pk = slot_of(k, logC), pc = slot_of(kc, logC);
+      const double2 Zk = buf[pidx(pk)];
+      const double2 Zc = buf[pidx(pc)];
       const double2 E = make_double2(0.5 * (Zk.x + Zc.x), 0.5 * (Zk.y - Zc.y));
       const double2 D = make_double2(Zk.x - Zc.x, Zk.y + Zc.y);  // Zk - conj(Zc)
       const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);     // D / (2i)
@@ -251,32 +342,31 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
         Xc = make_double2(Zk.x - Zk.y, 0.0);
       }
       // spectrum at omega_k = conj(Wk), omega_{C-k} = -Wk; window phase W^{k rlo}
-      const int64_t ph_idx = ((int64_t)k * rlo_modN) & (N - 1);
-      const double2 ph = tw_l((int)ph_idx, logN);
       const double2 Hk = spectrum(st, cconj(Wk), ph, h, pl.tau, inv_c);
       const double2 ph_c = cscale(cconj(ph), rlo_sign);
       const double2 Hc = spectrum(st, make_double2(-Wk.x, -Wk.y), ph_c, h, pl.tau, inv_c);
       const double2 Yk = cmul(Xk, Hk);
       const double2 Yc = cmul(Xc, Hc);
-      // A = Yk + conj(Yc), B = Yk - conj(Yc); Zp[k] = (A + i conj(Wk) B)/2
+      // A = Yk + conj(Yc), B = Yk - conj(Yc); Zp[k] = (A + i conj(Wk) B)/2, Zp[C-k] = conj((A - i conj(Wk) B)/2)
       const double2 A = make_double2(Yk.x + Yc.x, Yk.y - Yc.y);
       const double2 B = make_double2(Yk.x - Yc.x, Yk.y + Yc.y);
       const double2 cWB = cmul(cconj(Wk), B);
       const double2 iCWB = make_double2(-cWB.y, cWB.x);
-      const double2 Zpk = cscale(cadd(A, iCWB), 0.5);
-      buf[pidx(k)] = cconj(Zpk);
-      if (k != 0 && k != C / 2) buf[pidx(kc)] = cscale(csub(A, iCWB), 0.5);  // conj(Zp[C-k])
+      buf[pidx(pk)] = cscale(cadd(A, iCWB), 0.5);
+      if (k != 0 && k != C / 2) buf[pidx(pc)] = cconj(cscale(csub(A, iCWB), 0.5));
+      Wk = cmul(Wk, Wstep);
+      ph = cmul(ph, phstep);
     }
     gsync(g);
-    fft_grp(buf, logC, g);
-    // -- store valid outputs: y[2n] = Re, y[2n+1] = -Im
+    fft_dit(buf, logC, tq, g);
+    // -- store valid outputs: y[2n] = Re, y[2n+1] = Im
     const int64_t lim = (Lout - k0 < pl.P) ? (Lout - k0) : pl.P;
-#pragma unroll 1
+#pragma unroll 4
     for (int n = g.t; n < C; n += g.n) {
       const double2 v = buf[pidx(n)];
       const int64_t j = 2 * (int64_t)n;
       if (j < lim) y[k0 + j] = v.x;
-      if (j + 1 < lim) y[k0 + j + 1] = -v.y;
+      if (j + 1 < lim) y[k0 + j + 1] = v.y;
     }
     gsync(g);
   }
@@ -301,18 +391,20 @@ __device__ double conv_direct(const double* __restrict__ x, int64_t L, double* _
   const int per = g.n / G;
   for (int64_t k0 = 0; k0 < Lout; k0 += per) {
     const int64_t k = k0 + g.t / G;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     if (k < Lout) {
       const double* xk = sx + k;
       int r = sub;
-#pragma unroll 4
-      for (; r + G < M; r += 2 * G) {
+#pragma unroll 2
+      for (; r + 3 * G < M; r += 4 * G) {
         a0 = fma(sw[r], xk[r], a0);
         a1 = fma(sw[r + G], xk[r + G], a1);
+        a2 = fma(sw[r + 2 * G], xk[r + 2 * G], a2);
+        a3 = fma(sw[r + 3 * G], xk[r + 3 * G], a3);
       }
-      if (r < M) a0 = fma(sw[r], xk[r], a0);
+      for (; r < M; r += G) a0 = fma(sw[r], xk[r], a0);
     }
-    double s = a0 + a1;
+    double s = (a0 + a1) + (a2 + a3);
     for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
     if (k < Lout && sub == 0) y[k] = s;
   }

@@ -6,11 +6,13 @@
 // Fast path: a persistent, warp-specialised CTA per SM (fl_sched.cuh).  Each
 // chain warp prices one option at a time, pulled from a global queue in
 // decreasing-cost order:
-//   * stage loop (bsm.py:639-665) and the _solve_q halving recursion
+//   * the stage loop (bsm.py:639-665) and the _solve_q halving recursion
 //     (bsm.py:443-501) run on the chain warp with an explicit stack;
-//   * nonlinear leaves (h <= PUT_LEAF, the reference's _strip_advance /
-//     bsm_strip_sweep) run on the chain warp, registers + shuffles;
-//   * every linear jump (far / mid / bottom) is issued to the worker warps;
+//   * leaves (h <= PUT_LEAF: the reference's _strip_advance /
+//     bsm_strip_sweep) run on the chain warp, in registers with shuffles;
+//   * nodes with h <= FUSE_H run whole on the chain warp in shared memory
+//     (mid jump, leaf, bottom jump, leaf: no round trip through L2);
+//   * every longer linear jump (far / mid / bottom) is a worker task;
 //   * the apex finish (bsm.py:679-713) is a worker task over shared memory.
 // Row data live in a per-chain HBM arena, column-indexed, so the reference's
 // concatenations (upper|mid, lower|bottom, near|far) are free.
@@ -25,9 +27,18 @@
 
 namespace fl {
 
-constexpr int PUT_LEAF = 32;                           // device recursion leaf height
+#ifndef FL_PUT_LEAF
+#define FL_PUT_LEAF 32
+#endif
+constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
+constexpr int FUSE_H = 2 * PUT_LEAF;                   // nodes up to this height are fused on the chain
 constexpr int PUT_MAX_DEPTH = 24;
+// chain scratch (doubles): fused-node input and assembled rows + staged weights
+constexpr int FUSE_SEG = 2 * FUSE_H + 8;
+constexpr int CHAIN_SCRATCH = 2 * FUSE_SEG + (2 * PUT_LEAF + 1) + 16 > 4 * DIRECT_H + 8
+                                  ? 2 * FUSE_SEG + (2 * PUT_LEAF + 1) + 16
+                                  : 4 * DIRECT_H + 8;
 
 enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1 };
 
@@ -48,63 +59,89 @@ struct PutLayout {
 __host__ __device__ inline PutLayout put_layout(int64_t n, int64_t ks) {
   PutLayout L;
   const int64_t lowest = (ks - n < -n ? ks - n : -n);
-  L.colbase = lowest - 4 * PUT_LEAF - 16;
+  L.colbase = lowest - 4 * FUSE_H - 16;
   L.span = (ks + n + 8) - L.colbase + 1;
   return L;
 }
 
-constexpr int64_t KCACHE_DOUBLES = (int64_t)(DIRECT_H + 2) * (DIRECT_H + 2) * 2;
-constexpr int64_t DELTA_DOUBLES = 4 * DIRECT_H + 8;
-
 // doubles needed per chain for a batch whose options have at most these sizes
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max) {
-  const int64_t span = 2 * n_max + ks_pos_max + 4 * PUT_LEAF + 32;
+  const int64_t span = 2 * n_max + ks_pos_max + 4 * FUSE_H + 32;
   const int64_t frames = 2 * n_max + 64 * PUT_MAX_DEPTH;
-  return 3 * span + frames + KCACHE_DOUBLES + DELTA_DOUBLES + 64;
+  return 3 * span + frames + KTABLE_DOUBLES + 64;
 }
 
 struct PutChainCtx {
   SchedShared* S;
   int c;
   Stencil st;
-  double* kc;
-  unsigned char* kbuilt;
-  const double* delta;
+  const double* kc;  // composed weights W_1..W_DIRECT_H (slot m at kc + m*m)
   double* frames;
   const double* pay_org;
-  double flops;  // strip flops (lane-uniform)
+  double* scratch;   // chain's shared scratch (CHAIN_SCRATCH doubles)
+  double flops;      // chain-side flops (lane-uniform)
   unsigned long long* prof;
 };
 
-__device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
-                                         int h) {
-  issue_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.kbuilt, X.delta);
-}
-
-// Leaf strip on the chain warp, after waiting for conflicting pending jumps.
-__device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, double* in_org, double* out_org,
-                                            int64_t lo, int64_t hi, int64_t f, int height) {
-  const long long t0 = clock64();
-  wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + hi + 1), U(X.pay_org + lo), U(X.pay_org + hi + 1),
-                 U(out_org + lo), U(out_org + hi + 1));
+// Leaf strip on the chain warp.  in_org / out_org may address shared memory.
+__device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
+                                            double* out_org, int64_t lo, int64_t hi, int64_t f, int height) {
   const long long t1 = clock64();
-  if (X.prof && __activemask() != FULL && lane_id() == 0) prof_add(X.prof, PROF_DIVERGED, 1);
-  __syncwarp();
-  long long tm[2] = {0, 0};
-  const int64_t kb =
-      put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu, X.prof ? tm : nullptr);
+  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu);
   if (X.prof && lane_id() == 0) {
-    const long long t2 = clock64();
-    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
-    prof_add(X.prof, PROF_WAIT_N, (t1 - t0) > 200 ? 1 : 0);
-    prof_add(X.prof, PROF_STRIP_CYC, t2 - t1);
+    prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
     prof_add(X.prof, PROF_STRIP_N, height);
-    prof_add(X.prof, PROF_ISSUE_CYC, tm[1]);      // row loop only
-    prof_add(X.prof, PROF_QFULL_CYC, tm[0] - t1);  // loads before the loop
   }
   const double W = (double)(hi - lo + 1);
   X.flops += 5.0 * (W * height - (double)height * (height + 1));
   return kb;
+}
+
+// A node with PUT_LEAF < h <= FUSE_H done whole on the chain warp (bsm.py:443-501
+// for one level): input cols f+1..f+2h of in_org, output cols kp+1..f+h of out_org.
+// The mid jump, the first leaf, the assembled row and the bottom jump stay in
+// shared memory.  Returns kp (or NONE_SEEN-derived error through *err).
+__device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f, const double* in_org,
+                                  double* out_org, int h, int32_t* err) {
+  const long long t0 = clock64();
+  wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + f + 2 * h + 1), 0, 0, U(out_org + f - h),
+                 U(out_org + f + h + 1));
+  if (X.prof && lane_id() == 0) prof_add(X.prof, PROF_WAIT_CYC, clock64() - t0);
+  const long long t1 = clock64();
+  const int h1 = (h + 1) / 2, h2 = h - h1;
+  double* s_in = X.scratch;                 // cols f+1 .. f+2h  (+4 pad)
+  double* s_asm = X.scratch + FUSE_SEG;     // cols f-h1+1 .. f+2h-h1 (+4 pad)
+  double* s_w = X.scratch + 2 * FUSE_SEG;   // staged weights
+  warp_stage(s_in, in_org + f + 1, 2 * h, 2 * h + 4);
+  const double* in_s = s_in - (f + 1);      // column origins of the shared rows
+  double* asm_s = s_asm - (f - h1 + 1);
+  // mid: cols f+h1+1 .. f+2h-h1 of row t+h1
+  int M = 2 * h1 + 1;
+  warp_stage(s_w, X.kc + (int64_t)h1 * h1, M);
+  X.flops += warp_conv_direct(s_in, asm_s + f + h1 + 1, 2 * (int64_t)(h - h1), s_w, M);
+  // first half-height leaf
+  const int64_t km = put_leaf(X, P, in_s, asm_s, f - 2 * h1 - 1, f + 2 * h1, f, h1);
+  if (km == NONE_SEEN || km < f - h1 || km > f) { *err = FL_E_GEOMETRY | 1; return 0; }
+  // bottom: cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
+  const int64_t A = f + 2 * (int64_t)h - h1 - km;
+  if (lane_id() < 4) asm_s[f + 2 * h - h1 + 1 + lane_id()] = 0.0;  // zero pad behind the assembled row
+  __syncwarp();  // leaf stores visible to the whole warp
+  M = 2 * h2 + 1;
+  warp_stage(s_w, X.kc + (int64_t)h2 * h2, M);
+  X.flops += warp_conv_direct(asm_s + km + 1, out_org + km + h2 + 1, A - 2 * (int64_t)h2, s_w, M);
+  // second half-height leaf from the assembled row
+  const int64_t kp = put_leaf(X, P, asm_s, out_org, km - 2 * h2 - 1, km + 2 * h2, km, h2);
+  if (kp == NONE_SEEN || kp < km - h2 || kp > km) { *err = FL_E_GEOMETRY | 2; return 0; }
+  if (X.prof && lane_id() == 0) {
+    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
+    prof_add(X.prof, PROF_FUSE_N, 1);
+  }
+  return kp;
+}
+
+__device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
+                                         int h) {
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.prof);
 }
 
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
@@ -120,9 +157,17 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     const int h = F.h;
     if (F.state == 0) {
       if (h <= PUT_LEAF) {
+        wait_conflicts(*X.S, X.c, U(F.in_org + F.f + 1), U(F.in_org + F.f + 2 * h + 1), 0, 0,
+                       U(F.out_org + F.f - h), U(F.out_org + F.f + h + 1));
         const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
+        --sp;
+        continue;
+      }
+      if (h <= FUSE_H) {
+        ret = put_fused_node(X, P, F.f, F.in_org, F.out_org, h, err);
+        if (*err) return 0;
         --sp;
         continue;
       }
@@ -168,7 +213,8 @@ __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, 
 
 // One option on chain warp c.
 __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
-                                 unsigned char* kbuilt, const BatchOut& out, double* strip_flops) {
+                                 double* scratch, const BatchOut& out, double* chain_flops) {
+  const long long t_opt = clock64();
   const int64_t n = P.n, ks = P.ks;
   const PutLayout Lo = put_layout(n, ks);
   double* bufA = arena;
@@ -176,19 +222,9 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
   double* pay = arena + 2 * Lo.span;
   double* frames = arena + 3 * Lo.span;
   double* kc = frames + 2 * n + 64 * PUT_MAX_DEPTH;
-  double* delta = kc + KCACHE_DOUBLES;
-  // delta buffer for direct-kernel builds (zeros, 1.0 at 2*DIRECT_H+1)
-  for (int b = 0; b < DELTA_DOUBLES; b += 32) {  // uniform trip counts keep the warp converged
-    const int i = b + lane_id();
-    if (i < DELTA_DOUBLES) delta[i] = (i == 2 * DIRECT_H + 1) ? 1.0 : 0.0;
-  }
-  for (int b = 0; b <= DIRECT_H; b += 32) {
-    const int i = b + lane_id();
-    if (i <= DIRECT_H) kbuilt[i] = 0;
-  }
-  __syncwarp();
-  PutChainCtx X{&S, c, Stencil{P.cd, P.cm, P.cu, 2}, kc, kbuilt, delta, frames, pay - Lo.colbase, 0.0, out.prof};
-  const long long t_opt = clock64();
+  const Stencil st{P.cd, P.cm, P.cu, 2};
+  build_kernel_table(kc, st, scratch);
+  PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, 0.0, out.prof};
   double* cur_org = bufA - Lo.colbase;
   double* nxt_org = bufB - Lo.colbase;
   // payoff table 1 - e^{col ds} (bsm.py:238-244) and the initial row (zeros on 1..ks+n)
@@ -198,10 +234,10 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     t.x = nullptr; t.w = nullptr;
     t.y = bufA;
     t.L = Lo.span;
-    t.i0 = Lo.colbase;
+    t.i0 = Lo.colbase; t.i1 = t.i2 = 0;
     t.d0 = P.ds;
     t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0; t.Lout = 0;
-    issue(S, c, t, 0, 0, U(bufA), U(pay + Lo.span));
+    issue(S, c, RING_BIG, t, 0, 0, U(bufA), U(pay + Lo.span));
   }
   int32_t err = 0, cnt = 0;
   int64_t m = 0, f = 0;
@@ -213,20 +249,23 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     if (red < 0) { err = FL_E_GEOMETRY | 4; break; }
     if (red == 0) { price = P.K * (1.0 - exp((double)ks * P.ds)); break; }
     if (rem <= 2 * (int64_t)P.cutoff) {
-      if (2 * rem + 2 > SCHED_SLOTS) { err = FL_E_CAPACITY | 2; break; }
+      if (2 * rem + 2 > BIG_SLOTS) { err = FL_E_CAPACITY | 2; break; }
       Task t;
       t.kind = TK_PUT_APEX;
       t.x = cur_org; t.w = X.pay_org; t.y = nullptr;
       t.i0 = f; t.i1 = rem; t.i2 = ks;
-      t.c0 = P.cd; t.c1 = P.cm; t.c2 = P.cu; t.h = 0; t.span = 2; t.L = 0; t.Lout = 0;
-      const int idx = issue(S, c, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
-      wait_task(S, idx);
+      t.c0 = P.cd; t.c1 = P.cm; t.c2 = P.cu; t.h = 0; t.span = 2; t.L = 0; t.Lout = 0; t.d0 = 0.0;
+      const int ring = (2 * rem + 2 <= SMALL_SLOTS) ? RING_SMALL : RING_BIG;
+      const int id = issue(S, c, ring, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
+      warp_wait_done(S, id);
       price = P.K * S.result[c];
       X.flops += 5.0 * ((double)rem * rem + rem);
       break;
     }
     const int64_t hh = (rem / 2 < red / 2) ? rem / 2 : red / 2;
     if (hh < 1) {
+      wait_conflicts(S, c, U(cur_org + f + 1), U(cur_org + f + 2), U(X.pay_org + f - 3), U(X.pay_org + f + 2),
+                     U(nxt_org + f - 3), U(nxt_org + f + 2));
       const int64_t kb = put_leaf(X, P, cur_org, nxt_org, f - 3, f + 1, f, 1);
       if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
       f = kb;
@@ -246,17 +285,19 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     nxt_org = t;
   }
   wait_all_own(S, c);  // the next option reuses this arena
-  if (lane_id() == 0) prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   if (lane_id() == 0) {
     out.price[o] = err ? 0.0 : price;
     out.status[o] = err;
     if (out.bcount) out.bcount[o] = err ? 0 : cnt;
+    prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
-  *strip_flops += X.flops;
+  *chain_flops += X.flops;
 }
 
-// Worker-side execution of the put-specific tasks.
-__device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, const Grp& g) {
+// Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
+// double2 (the apex uses it as two double arrays of `slots` entries).
+__device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN,
+                                const double2* tq, const Grp& g) {
   if (t.kind == TK_PUT_INIT) {
     double* A = t.y;
     double* pay = t.y + 2 * t.L;
@@ -274,7 +315,7 @@ __device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, co
     const int64_t lo = ks - rem - 1, hi = ks + rem;
     const int W = (int)(hi - lo + 1);
     double* a = (double*)sbuf;
-    double* b = a + SCHED_SLOTS;
+    double* b = a + slots;
     for (int i = g.t; i < W; i += g.n) {
       const int64_t col = lo + i;
       a[i] = (col <= f) ? pay_org[col] : cur_org[col];
@@ -295,85 +336,115 @@ __device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, co
     if (g.t == 0) S.result[t.chain] = a[ks - lo];
     return 0.0;
   }
-  return exec_generic(t, sbuf, g);
+  return exec_generic(t, sbuf, slots, logN, tq, g);
 }
 
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
-  extern __shared__ double2 sbuf[];
-  __shared__ SchedShared S;
-  __shared__ unsigned char kbuilt[NCHAIN][DIRECT_H + 1];
+  extern __shared__ double2 sdyn_raw[];
+  // dynamic shared memory: scheduler state | chain scratch | twiddles | FFT buffers
+  SchedShared& S = *reinterpret_cast<SchedShared*>(sdyn_raw);
+  double* chain_scratch = reinterpret_cast<double*>(sdyn_raw) + SCHED_SHARED_DOUBLES;
+  double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SCRATCH);  // quarter-wave twiddles
+  double2* bigbuf = tq + TWQ;                // big-group FFT buffer
+  double2* smallbuf = bigbuf + BIG_SLOTS;    // SMALL_WORKERS x SMALL_SLOTS
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
   sched_init(S);
   __syncthreads();
   const int warp = threadIdx.x >> 5;
-  if (warp >= NWORKER_WARPS) {  // chain warps take the highest warp ids: the issue arbiter favours them
-    // ---- chain warp
-    const int c = warp - NWORKER_WARPS;
+  unsigned long long* prof = out.prof;
+  if (warp >= CHAIN_WARP0) {
+    // ---- chain warps (highest warp ids: the issue arbiter favours them)
+    const int c = warp - CHAIN_WARP0;
     double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
-    double strip_flops = 0.0;
+    double chain_flops = 0.0;
     for (;;) {
       int w = 0;
       if (lane_id() == 0) w = atomicAdd(counter, 1);
       w = __shfl_sync(FULL, w, 0);
       if (w >= nwork) break;
       const int o = order[w];
-      put_chain_option(S, c, opts[o], o, arena, kbuilt[c], out, &strip_flops);
+      put_chain_option(S, c, opts[o], o, arena, chain_scratch + c * CHAIN_SCRATCH, out, &chain_flops);
     }
-    if (lane_id() == 0) {
-      if (out.flops) atomicAdd(out.flops, (unsigned long long)strip_flops);
-      if (atomicSub(&S.chains_left, 1) == 1) {
-        // last chain out: stop the workers
-        const int idx = atomicAdd(&S.reserve, 1);
-        while (idx - S.done >= QCAP) __nanosleep(64);
-        Task& s = S.ring[idx % QCAP];
-        s.kind = TK_EXIT;
-        __threadfence_block();
-        s.seq = idx;
-      }
+    if (lane_id() == 0 && out.flops) atomicAdd(out.flops, (unsigned long long)chain_flops);
+    int last = 0;
+    if (lane_id() == 0) last = (atomicSub(&S.chains_left, 1) == 1);
+    last = __shfl_sync(FULL, last, 0);
+    if (last) {
+      // last chain out: one EXIT per small worker and one for the big group
+      Task t;
+      t.kind = TK_EXIT;
+      t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
+      t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
+      t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
+      for (int k = 0; k < SMALL_WORKERS; ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
+      issue(S, c, RING_BIG, t, 0, 0, 0, 0);
     }
     return;
   }
-  // ---- worker warps
-  const Grp g{(int)threadIdx.x, WORKERS, WORKER_BAR};
   double flops = 0.0;
-  unsigned long long* prof = out.prof;
   const long long t_start = clock64();
-  for (int next = 0;; ++next) {
-    Task& slot = S.ring[next % QCAP];
-    long long t0 = clock64();
-    if (g.t == 0) {
-      while (slot.seq != next) __nanosleep(20);
+  if (warp < BIG_WARPS) {
+    // ---- big group: one task at a time over BIG_THREADS threads
+    const Grp g{(int)threadIdx.x, BIG_THREADS, BIG_BAR};
+    __shared__ int s_idx;
+    for (;;) {
+      const long long t0 = clock64();
+      if (warp == 0) {
+        int idx = 0;
+        if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_BIG], 1);
+        idx = __shfl_sync(FULL, idx, 0);
+        worker_wait_ready(S, RING_BIG, idx);
+        if (lane_id() == 0) s_idx = idx;
+      }
+      gsync(g);
+      const int idx = s_idx;
+      const Task t = load_task(S.ring[RING_BIG][idx % QCAP]);
+      const long long t1 = clock64();
+      if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+      if (t.kind == TK_EXIT) break;
+      const double fl = put_exec_task(S, t, bigbuf, BIG_SLOTS, BIG_LOGN, tq, g);
+      flops += fl > 0 ? fl : 0.0;
+      gsync(g);
+      if (g.t == 0) {
+        publish_done(S, RING_BIG, idx);
+        prof_add(prof, PROF_BIG_CYC, clock64() - t1);
+        prof_add(prof, PROF_BIG_N, 1);
+      }
     }
-    gsync(g);
-    long long t1 = clock64();
-    if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-    __threadfence_block();
-    Task t;
-    t.x = slot.x; t.y = slot.y; t.w = slot.w; t.L = slot.L; t.Lout = slot.Lout;
-    t.c0 = slot.c0; t.c1 = slot.c1; t.c2 = slot.c2; t.h = slot.h; t.span = slot.span; t.kind = slot.kind;
-    t.chain = slot.chain; t.i0 = slot.i0; t.i1 = slot.i1; t.i2 = slot.i2; t.i3 = slot.i3;
-    t.d0 = slot.d0; t.d1 = slot.d1; t.d2 = slot.d2; t.d3 = slot.d3; t.d4 = slot.d4;
-    if (t.kind == TK_EXIT) break;
-    const double fl = put_exec_task(S, t, sbuf, g);
-    flops += fl > 0 ? fl : 0.0;
-    gsync(g);
-    if (g.t == 0) {
-      __threadfence();
-      S.done = next + 1;
-      if (prof) {
-        const long long dt = clock64() - t1;
-        const int slot0 = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC
-                        : (t.kind == TK_KBUILD) ? PROF_KB_CYC : PROF_OTHER_CYC;
-        prof_add(prof, slot0, dt);
-        prof_add(prof, slot0 + 1, 1);
-        if (t.kind == TK_FFT) prof_add(prof, PROF_FFT_LOUT, t.Lout);
-        if (t.kind == TK_DIRECT) prof_add(prof, PROF_DIR_LOUT, t.Lout);
+  } else {
+    // ---- small workers: one warp per task
+    const int sw = warp - BIG_WARPS;
+    const Grp g{lane_id(), 32, -1};
+    double2* buf = smallbuf + sw * SMALL_SLOTS;
+    for (;;) {
+      const long long t0 = clock64();
+      int idx = 0;
+      if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_SMALL], 1);
+      idx = __shfl_sync(FULL, idx, 0);
+      worker_wait_ready(S, RING_SMALL, idx);
+      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
+      const long long t1 = clock64();
+      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+      if (t.kind == TK_EXIT) break;
+      const double fl = put_exec_task(S, t, buf, SMALL_SLOTS, SMALL_LOGN, tq, g);
+      flops += fl > 0 ? fl : 0.0;
+      __syncwarp();
+      if (lane_id() == 0) {
+        publish_done(S, RING_SMALL, idx);
+        if (prof) {
+          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
+          prof_add(prof, ps, clock64() - t1);
+          prof_add(prof, ps + 1, 1);
+        }
       }
     }
   }
-  if (g.t == 0 && out.flops) atomicAdd(out.flops, (unsigned long long)flops);
-  if (g.t == 0) prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
+  if ((threadIdx.x & 31) == 0 && (warp >= BIG_WARPS || warp == 0)) {
+    if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
+    prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -439,7 +510,10 @@ put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restric
 // ---------------------------------------------------------------------------
 // launchers
 
-int put_fast_smem_bytes() { return SCHED_SLOTS * (int)sizeof(double2); }
+int put_fast_smem_bytes() {
+  return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SCRATCH) * (int)sizeof(double) +
+         (TWQ + BIG_SLOTS + SMALL_WORKERS * SMALL_SLOTS) * (int)sizeof(double2);
+}
 int put_chains_per_cta() { return NCHAIN; }
 
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,

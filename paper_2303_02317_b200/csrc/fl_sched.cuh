@@ -2,19 +2,26 @@
 // pricers (the device replacement of the reference's recursion drivers and
 // their 2-thread pool, american.py:168-198 / bsm.py:372-399).
 //
-// A CTA holds NCHAIN "chain" warps and a group of worker warps.  Each chain
-// warp owns one option at a time and walks its halving recursion: it runs
-// the nonlinear strips itself (the sequential critical path) and ISSUES every
-// linear jump (valid-mode correlation with a composed stencil) as a task into
-// a shared FIFO ring.  The worker group drains the ring in order, all worker
-// threads cooperating on one task (FFT or direct executor, fl_conv.cuh).
+// CTA layout (warp ids; the issue arbiter favours high ids):
+//   warps [0, BIG_WARPS)               "big" group: one task at a time over
+//                                      all its threads (named barrier 1)
+//   warps [BIG_WARPS, +SMALL_WORKERS)  "small" workers: one warp per task
+//   warps [CHAIN_WARP0, +NCHAIN)       chain warps: one option each
+// A chain warp walks its option's halving recursion.  It keeps the sequential
+// critical path to itself -- the nonlinear strips and, at the two lowest
+// levels, whole recursion nodes fused in shared memory -- and ISSUES every
+// longer linear jump as a task: into the small ring (one warp: direct dot
+// products for kernels up to DIRECT_H, FFT blocks up to 1024 points) or the
+// big ring (FFT blocks up to 8192 points).
 //
-// Ordering: tasks execute in issue order, so task->task dependencies (RAW /
-// WAR / WAW through the option's HBM arena) hold by construction.  A chain
-// touching memory itself (a strip) first waits for those of its own pending
-// tasks whose read / write address ranges conflict with the strip's -- and
-// only those, so linear jumps with slack run concurrently with the strips.
-// Chains never share arena memory, so chains never wait on each other.
+// Tasks of a ring are claimed in issue order but run concurrently and finish
+// out of order, so each task carries explicit dependencies: at issue time the
+// chain compares the new task's read / write address ranges with those of its
+// own unfinished tasks (RAW, WAR, WAW) and records the conflicting ones; a
+// worker starts a task only when they are done.  Before touching memory
+// itself the chain likewise waits for exactly the unfinished tasks it
+// conflicts with, so jumps with slack overlap the strips.  Chains never share
+// arena memory, so chains never wait on each other.
 #pragma once
 
 #include <cstdint>
@@ -25,22 +32,39 @@
 namespace fl {
 
 constexpr int NCHAIN = 2;
-constexpr int NWORKER_WARPS = 8;
-constexpr int WORKERS = 32 * NWORKER_WARPS;
-constexpr int SCHED_THREADS = 32 * (NCHAIN + NWORKER_WARPS);
-constexpr int QCAP = 64;
-constexpr int WORKER_BAR = 1;
-constexpr int DIRECT_H = 64;  // kernels with h <= DIRECT_H use the direct executor
-constexpr int SCHED_LOGN_MAX = 13;
-constexpr int SCHED_SLOTS = smem_complex_slots(1 << (SCHED_LOGN_MAX - 1));
+constexpr int BIG_WARPS = 4;
+constexpr int BIG_THREADS = 32 * BIG_WARPS;
+constexpr int SMALL_WORKERS = 8;
+constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + NCHAIN;
+constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
+constexpr int CHAIN_WARP0 = BIG_WARPS + SMALL_WORKERS;
+constexpr int NRINGS = 2;
+#ifndef FL_QCAP
+#define FL_QCAP 64
+#endif
+#ifndef FL_DIRECT_H  // kernels with h <= FL_DIRECT_H use direct dot products
+#define FL_DIRECT_H 64
+#endif
+#ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to one warp
+#define FL_SMALL_MW 320
+#endif
+constexpr int QCAP = FL_QCAP;  // per ring
+constexpr int BIG_BAR = 1;
+constexpr int DIRECT_H = FL_DIRECT_H;
+constexpr int BIG_LOGN = 13;    // big-group FFT blocks <= 8192 real points
+constexpr int SMALL_LOGN = 10;  // small-worker FFT blocks <= 1024 real points
+constexpr int BIG_SLOTS = smem_complex_slots(1 << (BIG_LOGN - 1));
+constexpr int SMALL_SLOTS = smem_complex_slots(1 << (SMALL_LOGN - 1));
+constexpr int NDEP = 6;
 
 enum : int {
   TK_FFT = 0,
   TK_DIRECT = 1,
-  TK_KBUILD = 2,
   TK_EXIT = 3,
   TK_USER = 8,  // pricer-specific tasks start here
 };
+
+enum : int { RING_SMALL = 0, RING_BIG = 1 };
 
 struct Task {
   const double* x;
@@ -49,34 +73,42 @@ struct Task {
   int64_t L, Lout;
   double c0, c1, c2;
   int h, span, kind, chain;
-  int64_t i0, i1, i2, i3;
-  double d0, d1, d2, d3, d4;
+  int64_t i0, i1, i2;
+  double d0;
+  int ndep;
+  int dep[NDEP];     // (ring << 28) | index
   volatile int seq;  // == task index once published
 };
 
-struct Pend {  // a chain's record of one of its issued tasks (address ranges)
-  int idx;
+struct Pend {  // a chain's record of one of its issued tasks
+  int id;      // (ring << 28) | index
   uintptr_t rlo, rhi, wlo, whi;
 };
 
+constexpr int PEND_CAP = 64;
+
 struct SchedShared {
-  Task ring[QCAP];
-  Pend pend[NCHAIN][QCAP];
+  Task ring[NRINGS][QCAP];
+  volatile int done[NRINGS][QCAP];  // index of the last finished task in the slot
+  int reserve[NRINGS];
+  int claim[NRINGS];
+  Pend pend[NCHAIN][PEND_CAP];
   int npend[NCHAIN];
   double result[NCHAIN];
-  int reserve;
-  volatile int done;
   int chains_left;
-  int64_t kcache_epoch[NCHAIN];
 };
 
+// SchedShared lives at the start of dynamic shared memory (16-byte aligned size).
+constexpr int SCHED_SHARED_DOUBLES = (int)((sizeof(SchedShared) + 15) / 16) * 2;
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uintptr_t U(const void* p) { return reinterpret_cast<uintptr_t>(p); }
 
 // profile counter slots (BatchOut::prof)
 enum : int {
-  PROF_FFT_CYC = 0, PROF_FFT_N, PROF_DIR_CYC, PROF_DIR_N, PROF_KB_CYC, PROF_KB_N, PROF_OTHER_CYC, PROF_OTHER_N,
-  PROF_STRIP_CYC, PROF_STRIP_N, PROF_WAIT_CYC, PROF_WAIT_N, PROF_ISSUE_CYC, PROF_KERNEL_CYC, PROF_IDLE_CYC,
-  PROF_FFT_LOUT, PROF_DIR_LOUT, PROF_CHAIN_CYC, PROF_QFULL_CYC, PROF_DIVERGED,
+  PROF_FFT_CYC = 0, PROF_FFT_N, PROF_DIR_CYC, PROF_DIR_N, PROF_OTHER_CYC, PROF_OTHER_N, PROF_BIG_CYC, PROF_BIG_N,
+  PROF_STRIP_CYC, PROF_STRIP_N, PROF_WAIT_CYC, PROF_FUSE_CYC, PROF_FUSE_N, PROF_KERNEL_CYC, PROF_IDLE_CYC,
+  PROF_ISS_CYC, PROF_CHAIN_CYC, PROF_DEPWAIT_CYC,
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
@@ -84,12 +116,16 @@ __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, uns
 }
 
 __device__ void sched_init(SchedShared& S) {
-  for (int i = threadIdx.x; i < QCAP; i += blockDim.x) S.ring[i].seq = -1;
-  if (threadIdx.x == 0) {
-    S.reserve = 0;
-    S.done = 0;
-    S.chains_left = NCHAIN;
+  for (int i = threadIdx.x; i < NRINGS * QCAP; i += blockDim.x) {
+    const int r = i / QCAP, q = i % QCAP;
+    S.ring[r][q].seq = -1;
+    S.done[r][q] = q - QCAP;  // "previous generation finished"
   }
+  if (threadIdx.x < NRINGS) {
+    S.reserve[threadIdx.x] = 0;
+    S.claim[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) S.chains_left = NCHAIN;
   if (threadIdx.x < NCHAIN) S.npend[threadIdx.x] = 0;
 }
 
@@ -97,116 +133,287 @@ __device__ __forceinline__ bool overlap(uintptr_t a0, uintptr_t a1, uintptr_t b0
   return a0 < b1 && b0 < a1;
 }
 
-// Issue a task from chain warp `c` (all 32 lanes call).  rd / wr: byte ranges
-// the task reads / writes (for the chain's own conflict checks).  Returns the
-// task index.
-__device__ int issue(SchedShared& S, int c, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
+__device__ __forceinline__ bool task_done(const SchedShared& S, int id) {
+  const int r = (int)((unsigned)id >> 28), idx = id & 0x0fffffff;
+  return S.done[r][idx % QCAP] >= idx;
+}
+
+// All lanes of the calling warp spin (warp-uniform, keeps the warp converged).
+__device__ __forceinline__ void warp_wait_done(const SchedShared& S, int id) {
+  while (!__shfl_sync(FULL, (int)task_done(S, id), 0)) __nanosleep(32);
+  __threadfence_block();
+}
+
+// The chain's unfinished tasks conflicting with the given ranges, in issue
+// order, into out[0..min(n,cap)); returns n.
+__device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+                              uintptr_t w0, uintptr_t w1, int* out, int cap) {
+  const int np = S.npend[c];
+  const int first = np > PEND_CAP ? np - PEND_CAP : 0;
+  int n = 0;
+  for (int base = first; base < np; base += 32) {  // warp-uniform trip count
+    const int i = base + lane_id();
+    bool hit = false;
+    int id = 0;
+    if (i < np) {
+      const Pend& p = S.pend[c][i % PEND_CAP];
+      id = p.id;
+      const bool raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
+      const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
+      hit = (raw || war) && !task_done(S, id);
+    }
+    unsigned m = __ballot_sync(FULL, hit);
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      const int v = __shfl_sync(FULL, id, l);
+      if (n < cap) out[n] = v;
+      ++n;
+    }
+  }
+  return n;
+}
+
+// Chain c waits for its unfinished tasks that conflict with a region it is
+// about to read (r0/r1, r2/r3) and write (w0/w1).
+__device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+                               uintptr_t w0, uintptr_t w1) {
+  int ids[8];
+  for (;;) {
+    const int n = scan_conflicts(S, c, r0, r1, r2, r3, w0, w1, ids, 8);
+    if (n == 0) break;
+    const int m = n < 8 ? n : 8;
+    for (int i = 0; i < m; ++i) warp_wait_done(S, ids[i]);
+    if (n <= 8) break;
+  }
+  __syncwarp();
+}
+
+// Issue a task from chain warp `c` (all 32 lanes call).  Returns its id.
+// rlo/rhi: read range; wlo/whi: write range.
+__device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
                      uintptr_t whi) {
+  int deps[NDEP];
+  int nd;
+  for (;;) {
+    nd = scan_conflicts(S, c, rlo, rhi, 0, 0, wlo, whi, deps, NDEP);
+    if (nd <= NDEP) break;
+    warp_wait_done(S, deps[0]);  // too many: retire the oldest conflict first
+  }
+  // keep the pending list from overflowing: wait for the entry about to be overwritten
+  {
+    const int np = S.npend[c];
+    if (np >= PEND_CAP) warp_wait_done(S, S.pend[c][np % PEND_CAP].id);
+  }
   __threadfence_block();  // this lane's earlier global writes before the publish
   __syncwarp();
   int idx = 0;
-  if (lane_id() == 0) idx = atomicAdd(&S.reserve, 1);
+  if (lane_id() == 0) idx = atomicAdd(&S.reserve[ring], 1);
   idx = __shfl_sync(FULL, idx, 0);
-  // warp-uniform spin (a lane-0-only loop would leave the warp split)
-  while (idx - __shfl_sync(FULL, S.done, 0) >= QCAP) __nanosleep(64);
+  // the slot's previous occupant must be finished
+  while (!__shfl_sync(FULL, (int)(S.done[ring][idx % QCAP] >= idx - QCAP), 0)) __nanosleep(64);
+  const int id = (ring << 28) | (idx & 0x0fffffff);  // ring in bits 28..31
   if (lane_id() == 0) {
-    Task& s = S.ring[idx % QCAP];
+    Task& s = S.ring[ring][idx % QCAP];
     s.x = t.x; s.y = t.y; s.w = t.w; s.L = t.L; s.Lout = t.Lout;
     s.c0 = t.c0; s.c1 = t.c1; s.c2 = t.c2; s.h = t.h; s.span = t.span; s.kind = t.kind; s.chain = c;
-    s.i0 = t.i0; s.i1 = t.i1; s.i2 = t.i2; s.i3 = t.i3;
-    s.d0 = t.d0; s.d1 = t.d1; s.d2 = t.d2; s.d3 = t.d3; s.d4 = t.d4;
-    Pend& p = S.pend[c][S.npend[c] % QCAP];
-    p.idx = idx; p.rlo = rlo; p.rhi = rhi; p.wlo = wlo; p.whi = whi;
+    s.i0 = t.i0; s.i1 = t.i1; s.i2 = t.i2;
+    s.d0 = t.d0;
+    s.ndep = nd;
+    for (int i = 0; i < nd; ++i) s.dep[i] = deps[i];
+    Pend& p = S.pend[c][S.npend[c] % PEND_CAP];
+    p.id = id; p.rlo = rlo; p.rhi = rhi; p.wlo = wlo; p.whi = whi;
     S.npend[c] += 1;
     __threadfence_block();
     s.seq = idx;
   }
   __syncwarp();
-  return idx;
-}
-
-// Chain waits until task `idx` (and so every earlier task) has completed.
-__device__ __forceinline__ void wait_task(SchedShared& S, int idx) {
-  while (__shfl_sync(FULL, S.done, 0) <= idx) __nanosleep(32);  // warp-uniform spin
-  __threadfence_block();
-}
-
-// Chain c waits for its pending tasks that conflict with a region it is about
-// to read (r0/r1, r2/r3) and write (w0/w1).
-__device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
-                               uintptr_t w0, uintptr_t w1) {
-  const int done = S.done;
-  const int np = S.npend[c];
-  int need = -1;
-  const int first = np > QCAP ? np - QCAP : 0;
-  // warp-uniform trip count: keeps the chain warp converged (a lane-dependent
-  // loop bound here splits the warp and sends later shuffles down the slow
-  // collective path)
-  for (int base = first; base < np; base += 32) {
-    const int i = base + lane_id();
-    if (i < np) {
-      const Pend& p = S.pend[c][i % QCAP];
-      const bool live = p.idx >= done;
-      const bool raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
-      const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
-      if (live && (raw || war) && p.idx > need) need = p.idx;
-    }
-  }
-  need = __reduce_max_sync(FULL, need);
-  if (need >= 0) wait_task(S, need);
-  __syncwarp();
+  return id;
 }
 
 // Chain c waits for all of its issued tasks.
 __device__ void wait_all_own(SchedShared& S, int c) {
   const int np = S.npend[c];
-  if (np == 0) return;
-  const int last = S.pend[c][(np - 1) % QCAP].idx;
-  wait_task(S, last);
+  const int first = np > PEND_CAP ? np - PEND_CAP : 0;
+  for (int i = first; i < np; ++i) warp_wait_done(S, S.pend[c][i % PEND_CAP].id);
 }
 
-__device__ __forceinline__ uintptr_t U(const void* p) { return reinterpret_cast<uintptr_t>(p); }
+// Which ring an FFT correlation goes to (uniform per task).
+__device__ __forceinline__ int fft_ring(const Stencil& st, int h) {
+  const int64_t Mw = window_width(st, h, nullptr);
+  return (Mw <= FL_SMALL_MW) ? RING_SMALL : RING_BIG;
+}
 
-// Issue y[0..Lout) = valid correlation of x[0..L) with W_h (chooses the executor;
-// builds the direct weights on first use).  kc: this chain's kernel cache
-// (slot h at kc + h*h, (h*span+1) doubles); kbuilt: per-h flags in smem;
-// delta: zero buffer with 1.0 at index DIRECT_H*2+1.
-__device__ void issue_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
-                           int64_t Lout, int h, double* kc, unsigned char* kbuilt, const double* delta) {
+// ---------------------------------------------------------------------------
+// Direct dot products for short kernels: W_1..W_DIRECT_H per option (slot m at
+// kc + m*m, m*span+1 doubles), built by repeated real-space convolution with
+// the one-step stencil -- all terms nonnegative, ~m ulp relative accuracy
+// (tighter than the reference's FFT power).
+
+constexpr int64_t KTABLE_DOUBLES = (int64_t)(DIRECT_H + 2) * (DIRECT_H + 2) * 2;
+
+// scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
+__device__ void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
+  const int lane = lane_id();
+  const int span = st.span;
+  double* a = scratch;
+  double* b = scratch + (2 * DIRECT_H + 2);
+  for (int base = 0; base < 2 * DIRECT_H + 2; base += 32) {
+    const int i = base + lane;
+    if (i < 2 * DIRECT_H + 2) a[i] = (i == 0) ? st.c0 : (i == 1) ? st.c1 : (i == 2 && span == 2) ? st.c2 : 0.0;
+  }
+  __syncwarp();
+  for (int m = 1; m <= DIRECT_H; ++m) {
+    const int M = m * span + 1;
+    for (int base = 0; base < M; base += 32) {  // store W_m
+      const int r = base + lane;
+      if (r < M) kc[m * m + r] = a[r];
+    }
+    if (m == DIRECT_H) break;
+    const int M2 = M + span;
+    for (int base = 0; base < M2; base += 32) {  // W_{m+1}[r] = sum_t c_t W_m[r-t]
+      const int r = base + lane;
+      if (r < M2) {
+        double s = (r < M) ? st.c0 * a[r] : 0.0;
+        if (r >= 1 && r - 1 < M) s = fma(st.c1, a[r - 1], s);
+        if (span == 2 && r >= 2 && r - 2 < M) s = fma(st.c2, a[r - 2], s);
+        b[r] = s;
+      }
+    }
+    __syncwarp();
+    double* t = a;
+    a = b;
+    b = t;
+  }
+  __syncwarp();
+  __threadfence_block();
+}
+
+// y[k] = sum_{r<M} w[r] x[k+r], k < Lout, on the calling warp.  x and w may be
+// generic (shared or global) pointers.  Register-blocked: lane l produces the
+// B = 4 consecutive outputs 4l..4l+3 of each 128-output pass, sliding a
+// 4-element window of x through registers (2 loads per 4 multiply-adds).
+__device__ double warp_conv_direct(const double* __restrict__ x, double* __restrict__ y, int64_t Lout,
+                                   const double* __restrict__ w, int M) {
+  const int lane = lane_id();
+  for (int64_t k0 = 0; k0 < Lout; k0 += 128) {
+    const int64_t kb = k0 + 4 * lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (kb < Lout) {
+      const double* xk = x + kb;
+      double x0 = xk[0], x1 = xk[1], x2 = xk[2];
+      int r = 0;
+#pragma unroll 2
+      for (; r + 3 < M; r += 4) {
+        // taps r..r+3 with the window rotating through x0..x3 (no register moves)
+        double x3 = xk[r + 3];
+        double wr = w[r];
+        a0 = fma(wr, x0, a0); a1 = fma(wr, x1, a1); a2 = fma(wr, x2, a2); a3 = fma(wr, x3, a3);
+        x0 = xk[r + 4];
+        wr = w[r + 1];
+        a0 = fma(wr, x1, a0); a1 = fma(wr, x2, a1); a2 = fma(wr, x3, a2); a3 = fma(wr, x0, a3);
+        x1 = xk[r + 5];
+        wr = w[r + 2];
+        a0 = fma(wr, x2, a0); a1 = fma(wr, x3, a1); a2 = fma(wr, x0, a2); a3 = fma(wr, x1, a3);
+        x2 = xk[r + 6];
+        wr = w[r + 3];
+        a0 = fma(wr, x3, a0); a1 = fma(wr, x0, a1); a2 = fma(wr, x1, a2); a3 = fma(wr, x2, a3);
+      }
+      for (; r < M; ++r) {  // tail taps (window restarts from memory)
+        const double wr = w[r];
+        a0 = fma(wr, xk[r], a0);
+        a1 = fma(wr, xk[r + 1], a1);
+        a2 = fma(wr, xk[r + 2], a2);
+        a3 = fma(wr, xk[r + 3], a3);
+      }
+      y[kb] = a0;
+      if (kb + 1 < Lout) y[kb + 1] = a1;
+      if (kb + 2 < Lout) y[kb + 2] = a2;
+      if (kb + 3 < Lout) y[kb + 3] = a3;
+    }
+  }
+  __syncwarp();
+  return 2.0 * (double)Lout * (double)M;
+}
+
+// Stage n doubles from global into warp-owned shared memory (all loads in
+// flight), zero-filling up to n_total (warp_conv_direct reads 3 past its window).
+__device__ __forceinline__ void warp_stage(double* dst, const double* src, int n, int n_total = -1) {
+  if (n_total < n) n_total = n;
+  for (int base = 0; base < n_total; base += 32) {
+    const int i = base + lane_id();
+    if (i < n_total) dst[i] = (i < n) ? src[i] : 0.0;
+  }
+  __syncwarp();
+}
+
+// A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
+// or an FFT task, on the small or big ring.
+__device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
+                           int64_t Lout, int h, const double* kc, unsigned long long* prof) {
   if (Lout <= 0) return;
   Task t;
   t.c0 = st.c0; t.c1 = st.c1; t.c2 = st.c2; t.span = st.span; t.h = h;
-  if (h <= DIRECT_H && L <= 4096) {
-    const int M = h * st.span + 1;
-    double* w = kc + (int64_t)h * h;
-    if (!kbuilt[h]) {
-      Task b = t;
-      b.kind = TK_KBUILD;
-      b.x = delta + (2 * DIRECT_H + 1) - (M - 1);
-      b.L = 2 * (int64_t)M - 1;
-      b.y = w;
-      b.Lout = M;
-      issue(S, c, b, U(b.x), U(b.x + b.L), U(w), U(w + M));
-      if (lane_id() == 0) kbuilt[h] = 1;
-      __syncwarp();
-    }
+  t.i0 = t.i1 = t.i2 = 0;
+  t.d0 = 0.0;
+  t.x = x; t.L = L; t.y = y; t.Lout = Lout;
+  const long long t0 = clock64();
+  if (h <= DIRECT_H && L <= 1024) {
     t.kind = TK_DIRECT;
-    t.w = w;
+    t.w = kc + (int64_t)h * h;
+    issue(S, c, RING_SMALL, t, U(x), U(x + L), U(y), U(y + Lout));
   } else {
     t.kind = TK_FFT;
     t.w = nullptr;
+    issue(S, c, fft_ring(st, h), t, U(x), U(x + L), U(y), U(y + Lout));
   }
-  t.x = x; t.L = L; t.y = y; t.Lout = Lout;
-  issue(S, c, t, U(x), U(x + L), U(y), U(y + Lout));
+  if (prof && lane_id() == 0) prof_add(prof, PROF_ISS_CYC, clock64() - t0);
 }
 
-// Execute a generic task on the worker group; returns executed flops (or < 0 on error).
-__device__ double exec_generic(const Task& t, double2* sbuf, const Grp& g) {
+// Worker side: wait until slot `idx` of `ring` is published and its deps are done
+// (warp-uniform; called by one warp).
+__device__ __forceinline__ void worker_wait_ready(SchedShared& S, int ring, int idx) {
+  Task& s = S.ring[ring][idx % QCAP];
+  while (__shfl_sync(FULL, s.seq, 0) != idx) __nanosleep(20);
+  __threadfence_block();
+  const int nd = s.ndep;
+  for (int i = 0; i < nd; ++i) warp_wait_done(S, s.dep[i]);
+}
+
+__device__ __forceinline__ Task load_task(const Task& s) {
+  Task t;
+  t.x = s.x; t.y = s.y; t.w = s.w; t.L = s.L; t.Lout = s.Lout;
+  t.c0 = s.c0; t.c1 = s.c1; t.c2 = s.c2; t.h = s.h; t.span = s.span; t.kind = s.kind;
+  t.chain = s.chain; t.i0 = s.i0; t.i1 = s.i1; t.i2 = s.i2;
+  t.d0 = s.d0;
+  t.ndep = 0;
+  return t;
+}
+
+__device__ __forceinline__ void publish_done(SchedShared& S, int ring, int idx) {
+  __threadfence();  // outputs visible (also to later tasks on other warps)
+  S.done[ring][idx % QCAP] = idx;
+}
+
+// Execute a generic task on a worker group; returns executed flops (or < 0 on error).
+// sbuf: the group's shared buffer (slots double2).
+__device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logNmax, const double2* tq,
+                               const Grp& g) {
   const Stencil st{t.c0, t.c1, t.c2, t.span};
-  if (t.kind == TK_FFT || t.kind == TK_KBUILD)
-    return conv_fft(t.x, t.L, t.y, t.Lout, t.h, st, sbuf, SCHED_LOGN_MAX, g);
-  // TK_DIRECT
-  return conv_direct(t.x, t.L, t.y, t.Lout, t.w, t.h * t.span + 1, (double*)sbuf, g);
+  if (t.kind == TK_FFT) return conv_fft(t.x, t.L, t.y, t.Lout, t.h, st, sbuf, logNmax, tq, g);
+  // TK_DIRECT: one warp, x and weights staged in shared memory
+  const int M = t.h * t.span + 1;
+  double* sx = (double*)sbuf;
+  double* sw = sx + 2 * slots - M - 8;
+  warp_stage(sw, t.w, M);
+  double fl = 0.0;
+  const int64_t chunk = 2 * slots - 2 * M - 16;  // x values per staged chunk (+4 zero pad fits)
+  for (int64_t k0 = 0; k0 < t.Lout; k0 += chunk - M + 1) {
+    const int64_t nk = (t.Lout - k0 < chunk - M + 1) ? (t.Lout - k0) : (chunk - M + 1);
+    warp_stage(sx, t.x + k0, (int)(nk + M - 1), (int)(nk + M + 3));
+    fl += warp_conv_direct(sx, t.y + k0, nk, sw, M);
+  }
+  return fl;
 }
 
 }  // namespace fl

@@ -82,4 +82,76 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
   return kb;
 }
 
+// Time-tiled variant of put_strip_warp: lanes exchange K halo cells per side
+// once per K rows (instead of one cell per side per row) and advance K rows on
+// an extended register tile, recomputing the halo cone redundantly.  One
+// shuffle round trip per K rows takes the shuffle latency off the per-row
+// critical path.  Same arithmetic per valid cell as put_strip_warp (identical
+// results).  Requires K <= CPL.
+template <int CPL, int K>
+__device__ int64_t put_strip_tiled(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
+                                   int height, double cd, double cm, double cu) {
+  static_assert(K <= CPL, "halo must come from the neighbouring lane");
+  constexpr int E = CPL + 2 * K;
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+  double e[E], p[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int64_t col = c0 - K + i;
+    p[i] = (col >= lo && col <= hi) ? pay_org[col] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    e[K + c] = (col <= hi) ? ((col <= f) ? p[K + c] : in_org[col]) : 0.0;
+  }
+  unsigned green = 0;
+  __syncwarp();
+  for (int s0 = 0; s0 < height; s0 += K) {
+    const int kk = (height - s0 < K) ? (height - s0) : K;
+    // halo exchange: K cells from each neighbour
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      e[i] = __shfl_up_sync(FULL, e[K + CPL - K + i], 1);
+      e[K + CPL + i] = __shfl_down_sync(FULL, e[K + i], 1);
+    }
+#pragma unroll
+    for (int s = 1; s <= K; ++s) {
+      if (s <= kk) {
+        const bool last = (s0 + s == height);
+        double left = e[s - 1];
+        green = 0;
+#pragma unroll
+        for (int i = s; i <= E - 1 - s; ++i) {
+          const double cur = e[i];
+          const double lin = fma(cd, left, fma(cu, e[i + 1], cm * cur));
+          left = cur;
+          const bool red = lin > p[i];
+          e[i] = red ? lin : p[i];
+          if (last && i >= K && i < K + CPL) green |= (red ? 0u : 1u) << (i - K);
+        }
+      }
+    }
+  }
+  // last green inside the final valid range [lo+height, hi-height]
+  const int64_t vlo = lo + height, vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col >= vlo && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = e[K + c];
+  }
+  return kb;
+}
+
 }  // namespace fl

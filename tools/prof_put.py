@@ -1,4 +1,4 @@
-"""Scheduler profile of one put batch (FL_PROFILE=1)."""
+"""Scheduler profile of one put batch (FL_PROFILE=1): per-role cycle counters."""
 import os, sys, time
 os.environ["FL_PROFILE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,11 +12,21 @@ db = _native.DeviceBatch(b.kind, b.S, b.K, b.R, b.Y, b.V, b.E, b.T)
 db.run(); db.fetch()
 t0 = time.perf_counter(); db.run(); r = db.fetch(); t1 = time.perf_counter()
 p = db.profile().astype(np.float64)
-names = ["FFT_CYC","FFT_N","DIR_CYC","DIR_N","KB_CYC","KB_N","OTHER_CYC","OTHER_N","STRIP_CYC","STRIP_ROWS","WAIT_CYC","WAIT_N","ROWLOOP_CYC","KERNEL_CYC","IDLE_CYC","FFT_LOUT","DIR_LOUT","CHAIN_CYC","LOADS_CYC","DIVERGED"]
+# must match the PROF_* enum in csrc/fl_sched.cuh
+names = ["FFT_CYC", "FFT_N", "DIR_CYC", "DIR_N", "OTHER_CYC", "OTHER_N", "BIG_CYC", "BIG_N",
+         "STRIP_CYC", "STRIP_ROWS", "WAIT_CYC", "FUSE_CYC", "FUSE_N", "KERNEL_CYC", "IDLE_CYC",
+         "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC"]
+P = dict(zip(names, p[:len(names)]))
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
-for i, nm in enumerate(names):
-    print(f"{nm:12s} {p[i]:.4g}")
+for nm in names:
+    print(f"{nm:12s} {P[nm]:.4g}")
 nopt = n
-print("per option: strip rows %.0f, strip cyc %.3g, wait cyc %.3g, chain cyc %.3g" % (p[9]/nopt, p[8]/nopt, p[10]/nopt, p[17]/nopt))
-print("per task: fft %.0f cyc (n=%d, Lout avg %.0f), direct %.0f cyc (n=%d), kbuild %.0f (n=%d)" % (p[0]/max(p[1],1), p[1], p[15]/max(p[1],1), p[2]/max(p[3],1), p[3], p[4]/max(p[5],1), p[5]))
-print("worker busy frac: %.3f" % ((p[0]+p[2]+p[4]+p[6]) / max(p[13],1)))
+d = lambda a, b: a / max(b, 1)
+print("per option: chain %.3g cyc, strip %.3g cyc (%.0f rows), wait %.3g, fused %.3g (n=%.0f), issue %.3g"
+      % (P["CHAIN_CYC"] / nopt, P["STRIP_CYC"] / nopt, P["STRIP_ROWS"] / nopt, P["WAIT_CYC"] / nopt,
+         P["FUSE_CYC"] / nopt, P["FUSE_N"] / nopt, P["ISS_CYC"] / nopt))
+print("small tasks: fft n=%.0f avg %.0f cyc; direct n=%.0f avg %.0f; other n=%.0f avg %.0f"
+      % (P["FFT_N"], d(P["FFT_CYC"], P["FFT_N"]), P["DIR_N"], d(P["DIR_CYC"], P["DIR_N"]),
+         P["OTHER_N"], d(P["OTHER_CYC"], P["OTHER_N"])))
+print("big tasks: n=%.0f avg %.0f cyc" % (P["BIG_N"], d(P["BIG_CYC"], P["BIG_N"])))
+print("status nonzero:", int(np.sum(r.status != 0)))
