@@ -78,6 +78,12 @@ int fl_batch_launches(const fl_batch* b);
  * 5 C log2 C per complex transform + 5 per explicit cell), and the bytes the
  * last prepare / fetch moved H2D / D2H. */
 int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t* d2h_bytes, void* stream);
+/* After a run: the REFERENCE-ALGORITHMIC fp64 flops of the batch -- the work
+ * the reference decomposition at its base_cutoff performs (5 flops per
+ * projected cell of each reference strip; 5 N log2 N + 6 (N/2+1) per
+ * reference FFT jump of size N = next_pow2(L + M - 1)), counted live by the
+ * fast kernels as they walk the same recursion.  The roofline numerator. */
+int fl_batch_ref_flops(fl_batch* b, double* ref_flops, void* stream);
 void fl_batch_free(fl_batch* b);
 /* Scheduler profile counters of the last run (requires FL_PROFILE set in the
  * environment at run time; zeros otherwise): 56 uint64 slots, see PROF_* in
@@ -91,6 +97,26 @@ int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream);
  * taps in {2,3}; coefficients must be nonnegative (lattice / FD weights). */
 int fl_apply_linear_steps(const double* x, int64_t L, int taps, double c0, double c1, double c2, int64_t h,
                           double* y, void* stream);
+
+/* One boundary-tracking stage of the put from a given row state
+ * (bsm.py:504 solve_bsm_trapezoid / _advance_stage bsm.py:557-582).
+ * Grid: weights cd, cm, cu and spacing ds of a BsmDiscretization; base_cutoff
+ * as in the reference (work accounting only).  Input: boundary f and the
+ * continuation values of columns f+1 .. f+W (host, W >= 2h).  Output: new
+ * boundary *kp, values of columns kp+1 .. f+W-h into out_seg (capacity W+h),
+ * *status = 0 or a GeometryError code. */
+int fl_put_trapezoid(double cd, double cm, double cu, double ds, int64_t base_cutoff, int64_t f,
+                     const double* seg, int64_t W, int64_t h, double* out_seg, int64_t* kp, int32_t* status,
+                     void* stream);
+
+/* One trapezoid of the American call (american.py:298 solve_trapezoid):
+ * lattice S, K, wd, wu, lu (BinomialParams weight_down / weight_up / log_up),
+ * row i, boundary j, red run of columns first .. j (host), height h.
+ * Output: boundary *jp of row i-h and the red values of columns first .. jp
+ * into out_run (capacity j-first+1), *status = 0 or a GeometryError code. */
+int fl_call_trapezoid(double S, double K, double wd, double wu, double lu, int64_t base_cutoff, int64_t i,
+                      int64_t j, int64_t first, const double* run, int64_t h, double* out_run, int64_t* jp,
+                      int32_t* status, void* stream);
 
 /* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
  * roofline denominator bench.py reports against. */

@@ -40,7 +40,7 @@ _lib = None
 EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
-    "fl_apply_linear_steps",
+    "fl_batch_ref_flops", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
     "fl_probe_fp64",
 )
 
@@ -88,6 +88,12 @@ def lib():
         L.fl_batch_stats.restype = c_int
         L.fl_batch_profile.argtypes = [P, P, P]
         L.fl_batch_profile.restype = c_int
+        L.fl_batch_ref_flops.argtypes = [P, P, P]
+        L.fl_batch_ref_flops.restype = c_int
+        L.fl_put_trapezoid.argtypes = [d, d, d, d, i64, i64, P, i64, i64, P, P, P, P]
+        L.fl_put_trapezoid.restype = c_int
+        L.fl_call_trapezoid.argtypes = [d, d, d, d, d, i64, i64, i64, i64, P, i64, P, P, P, P]
+        L.fl_call_trapezoid.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
         _lib = L
@@ -231,7 +237,9 @@ class DeviceBatch:
         hb, db = ctypes.c_int64(0), ctypes.c_int64(0)
         _check(lib().fl_batch_stats(self._h, ctypes.byref(f), ctypes.byref(hb), ctypes.byref(db),
                                     ctypes.c_void_p(stream) if stream else None))
-        return {"fp64_flops": f.value, "h2d_bytes": hb.value, "d2h_bytes": db.value}
+        r = ctypes.c_double(0.0)
+        _check(lib().fl_batch_ref_flops(self._h, ctypes.byref(r), ctypes.c_void_p(stream) if stream else None))
+        return {"fp64_flops": f.value, "ref_flops": r.value, "h2d_bytes": hb.value, "d2h_bytes": db.value}
 
     def fetch(self, stream=None) -> BatchResult:
         n, cap = self.n, self.cap
@@ -297,3 +305,35 @@ def probe_fp64_tflops(stream=None) -> float:
     t = ctypes.c_double(0.0)
     _check(lib().fl_probe_fp64(ctypes.byref(t), ctypes.c_void_p(stream) if stream else None))
     return t.value
+
+
+def put_trapezoid(cd: float, cm: float, cu: float, ds: float, base_cutoff: int, f: int, seg: np.ndarray, h: int):
+    """fl_put_trapezoid: (new boundary, values of cols kp+1 .. f+W-h); raises on a status."""
+    seg = np.ascontiguousarray(seg, dtype=np.float64)
+    W = int(seg.shape[0])
+    out = np.empty(W + h)
+    kp = ctypes.c_int64(0)
+    st = ctypes.c_int32(0)
+    _check(lib().fl_put_trapezoid(float(cd), float(cm), float(cu), float(ds), int(base_cutoff), int(f), _ptr(seg),
+                                  W, int(h), _ptr(out), ctypes.byref(kp), ctypes.byref(st), None))
+    err = status_error(st.value)
+    if err is not None:
+        raise err
+    n_out = (f + W - h) - kp.value
+    return kp.value, out[:n_out].copy()
+
+
+def call_trapezoid(S: float, K: float, wd: float, wu: float, lu: float, base_cutoff: int, i: int, j: int,
+                   first: int, run: np.ndarray, h: int):
+    """fl_call_trapezoid: (new boundary jp, red values of cols first .. jp); raises on a status."""
+    run = np.ascontiguousarray(run, dtype=np.float64)
+    out = np.empty(max(int(run.shape[0]), 1))
+    jp = ctypes.c_int64(0)
+    st = ctypes.c_int32(0)
+    _check(lib().fl_call_trapezoid(float(S), float(K), float(wd), float(wu), float(lu), int(base_cutoff), int(i),
+                                   int(j), int(first), _ptr(run), int(h), _ptr(out), ctypes.byref(jp),
+                                   ctypes.byref(st), None))
+    err = status_error(st.value)
+    if err is not None:
+        raise err
+    return jp.value, out[:max(jp.value - first + 1, 0)].copy()

@@ -1,0 +1,86 @@
+"""Binomial-lattice pricers -- drop-in for ``fftlattice.binomial``.
+
+``fast_european`` (binomial.py:161-194), ``baseline_european`` (:80-91) and
+``baseline_american_call`` (:94-130) with the reference signatures, result
+types and exceptions; prices and boundary records come from the CUDA library
+(csrc/fl_euro.cu, csrc/fl_call.cu).  ``leaf_row`` is the reference's host
+helper (terminal-row payoffs) and stays numpy.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _pricing
+from .model import (
+    BinomialParams,
+    BoundarySeries,
+    GridRow,
+    OptionSpec,
+    UnsupportedCombinationError,
+    derive_binomial_params,
+)
+
+__all__ = [
+    "AmericanCallResult",
+    "leaf_row",
+    "baseline_european",
+    "baseline_american_call",
+    "fast_european",
+    "price_european_batch",
+]
+
+
+@dataclass(frozen=True, slots=True)
+class AmericanCallResult:
+    """Price plus first-exercise-column record (binomial.py:41-55).
+
+    ``rows`` / ``exercise_masks`` (the reference's keep_grid output) are not
+    produced by the GPU path and stay None.
+    """
+
+    price: float
+    boundaries: BoundarySeries
+    rows: list[np.ndarray] | None = None
+    exercise_masks: list[np.ndarray] | None = None
+
+
+def leaf_row(spec: OptionSpec, params: BinomialParams | None = None) -> GridRow:
+    """Terminal-row call values max(S u^(2j-T) - K, 0) (binomial.py:64-77)."""
+    p = derive_binomial_params(spec) if params is None else params
+    n = spec.steps
+    j = np.arange(n + 1, dtype=np.float64)
+    return GridRow(n, 0, np.maximum(spec.spot * np.exp((2.0 * j - n) * p.log_up) - spec.strike, 0.0))
+
+
+def baseline_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
+    """O(T^2) backward induction on the device (binomial.py:80-91)."""
+    _pricing.check_params(spec, params)
+    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.BASELINE, record=False)
+    return price
+
+
+def fast_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
+    """Gauged composed-kernel inner product on the device (binomial.py:161-194)."""
+    _pricing.check_params(spec, params)
+    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.FAST, record=False)
+    return price
+
+
+def baseline_american_call(spec: OptionSpec, params: BinomialParams | None = None, *,
+                           keep_grid: bool = False) -> AmericanCallResult:
+    """O(T^2) projected induction on the device, first green per row recorded
+    (binomial.py:94-130)."""
+    if keep_grid:
+        raise UnsupportedCombinationError("keep_grid=True (full-grid snapshots) is not produced by the GPU path")
+    _pricing.check_params(spec, params)
+    price, series = _pricing.price_one(_pricing.KIND_CALL, spec, method=_pricing.BASELINE)
+    return AmericanCallResult(price=price, boundaries=series)
+
+
+def price_european_batch(S, K, R, Y, V, E, T, *, method: str = "fast"):
+    """Batched European calls (one device call).  Returns (price, status)."""
+    m = _pricing.FAST if method == "fast" else _pricing.BASELINE
+    return _pricing.price_many(np.int8(_pricing.KIND_EURO), S, K, R, Y, V, E, T, method=m)

@@ -21,6 +21,7 @@ from .model import (
     GridRow,
     OptionSpec,
     StabilityError,
+    UnsupportedCombinationError,
     ValidationError,
     validate_spec,
 )
@@ -37,6 +38,7 @@ __all__ = [
     "baseline_put_fd",
     "solve_bsm_trapezoid",
     "fast_put_bsm",
+    "price_put_batch",
 ]
 
 #: Reference recursion cutoff (bsm.py:59); governs dispatch (T <= 2*cutoff
@@ -141,3 +143,66 @@ def initial_row(disc: BsmDiscretization) -> PutRowState:
             "the payoff row has no continuation cells; the spot is deep enough "
             "in the money that the price is strike - spot")
     return PutRowState(0, 0, GridRow(0, 1, np.zeros(width, dtype=np.float64)))
+
+
+def baseline_put_fd(spec: OptionSpec, lam: float = DEFAULT_LAMBDA, steps: int | None = None, *,
+                    record_rows: tuple[int, ...] | None = None) -> PutResult:
+    """O(T^2) projected march over the shrinking window, on the device; the
+    last green column of every row is recorded (bsm.py:273-338)."""
+    if record_rows:
+        raise UnsupportedCombinationError("record_rows snapshots are not produced by the GPU path")
+    from . import _pricing
+
+    price, series = _pricing.price_one(_pricing.KIND_PUT, spec, method=_pricing.BASELINE, lam=float(lam),
+                                       steps=steps)
+    return PutResult(price=price, boundaries=series)
+
+
+def fast_put_bsm(spec: OptionSpec, lam: float = DEFAULT_LAMBDA, steps: int | None = None, *,
+                 base_cutoff: int = DEFAULT_BSM_CUTOFF, parallel: bool = False,
+                 record_rows: bool = False) -> PutResult:
+    """American put by boundary-tracking FFT recursion on the device
+    (bsm.py:585-676): same dispatch (deep in the money -> K - S, T <= 2*cutoff
+    -> the O(T^2) march), same stage schedule, same handoff-row record.
+    ``parallel`` is accepted and has no effect on results."""
+    del parallel
+    if record_rows:
+        raise UnsupportedCombinationError("record_rows snapshots are not produced by the GPU path")
+    from . import _pricing
+
+    price, series = _pricing.price_one(_pricing.KIND_PUT, spec, method=_pricing.FAST, lam=float(lam),
+                                       steps=steps, put_cutoff=int(base_cutoff))
+    return PutResult(price=price, boundaries=series)
+
+
+def price_put_batch(S, K, R, V, E, T, *, lam: float = DEFAULT_LAMBDA, method: str = "fast",
+                    base_cutoff: int = DEFAULT_BSM_CUTOFF):
+    """Batched American puts (one device call, Y = 0).  Returns (price, status)."""
+    from . import _pricing
+
+    m = _pricing.FAST if method == "fast" else _pricing.BASELINE
+    S = np.asarray(S, dtype=np.float64)
+    return _pricing.price_many(np.int8(_pricing.KIND_PUT), S, K, R, np.zeros_like(S), V, E, T, method=m,
+                               lam=float(lam), put_cutoff=int(base_cutoff))
+
+
+def solve_bsm_trapezoid(disc: BsmDiscretization, state: PutRowState, height: int, *,
+                        base_cutoff: int = DEFAULT_BSM_CUTOFF, parallel: bool = False) -> PutRowState:
+    """Advance a put row state ``height`` steps on the device, tracking the
+    boundary (bsm.py:504-554): far jump + boundary recursion of one stage."""
+    del parallel
+    if height < 1:
+        raise GeometryError("height must be >= 1")
+    width = len(state.segment)
+    if width < 2 * height:
+        raise GeometryError(
+            f"segment holds {width} continuation values; advancing {height} steps requires at least "
+            f"{2 * height}")
+    if base_cutoff < 1:
+        raise ValidationError("base_cutoff", "base_cutoff must be >= 1")
+    from . import _native
+
+    kp, seg = _native.put_trapezoid(disc.coef_down, disc.coef_mid, disc.coef_up, disc.d_s, int(base_cutoff),
+                                    int(state.boundary), state.segment.values, int(height))
+    t = state.time_index + height
+    return PutRowState(time_index=t, boundary=kp, segment=GridRow(time_index=t, col_offset=kp + 1, values=seg))

@@ -289,7 +289,6 @@ int upload(fl_batch* b, cudaStream_t stream) {
   for (int32_t o : b->o_put_base) nmax_base = std::max(nmax_base, b->put[o].n * 2 + 2);
   for (int32_t o : b->o_call_base) nmax_base = std::max(nmax_base, b->call[o].n + 2);
   for (int32_t o : b->o_euro_base) nmax_base = std::max(nmax_base, b->euro[o].n + 2);
-  int occ = 1;
   if (!b->o_put_fast.empty()) {
     b->ws_put_stride = fl::put_ws_doubles(nmax_put, ksmax);
     const int nc = fl::put_chains_per_cta();
@@ -298,10 +297,10 @@ int upload(fl_batch* b, cudaStream_t stream) {
   }
   if (!b->o_call_fast.empty()) {
     b->ws_call_stride = fl::call_ws_doubles(nmax_call);
-    b->grid_call = std::min<int>((int)b->o_call_fast.size(), nsm * 2);
-    FL_CUDA(b->d_ws_call.ensure(sizeof(double) * b->ws_call_stride * b->grid_call));
+    const int nc = fl::call_chains_per_cta();
+    b->grid_call = std::min<int>(((int)b->o_call_fast.size() + nc - 1) / nc, nsm);
+    FL_CUDA(b->d_ws_call.ensure(sizeof(double) * b->ws_call_stride * b->grid_call * nc));
   }
-  (void)occ;
   const int64_t nbase = (int64_t)std::max({b->o_put_base.size(), b->o_call_base.size(), b->o_euro_base.size()});
   if (nbase > 0) {
     b->ws_base_stride = 3 * nmax_base + 16;
@@ -495,6 +494,98 @@ int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t*
   if (fp64_flops) *fp64_flops = (double)f;
   if (h2d_bytes) *h2d_bytes = (int64_t)b->h2d_bytes;
   if (d2h_bytes) *d2h_bytes = (int64_t)b->d2h_bytes;
+  return 0;
+}
+
+int fl_batch_ref_flops(fl_batch* b, double* ref_flops, void* stream) {
+  if (!b) return fail("fl_batch_ref_flops: null batch");
+  unsigned long long f = 0;
+  FL_CUDA(cudaMemcpyAsync(&f, b->d_stats.as<unsigned long long>() + 1, sizeof(f), cudaMemcpyDeviceToHost,
+                          (cudaStream_t)stream));
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (ref_flops) *ref_flops = (double)f;
+  return 0;
+}
+
+// Shared driver of the single-problem trapezoid entry points: device buffers
+// for one input row, one output row and one chain arena, freed on return.
+struct TrapBufs {
+  DevBuf in, out, meta, counter, ws, stats;
+  ~TrapBufs() {
+    for (DevBuf* b : {&in, &out, &meta, &counter, &ws, &stats}) b->release();
+  }
+};
+
+int fl_put_trapezoid(double cd, double cm, double cu, double ds, int64_t base_cutoff, int64_t f, const double* seg,
+                     int64_t W, int64_t h, double* out_seg, int64_t* kp, int32_t* status, void* stream) {
+  if (!seg || !out_seg || !kp || !status) return fail("fl_put_trapezoid: null pointer");
+  if (h < 1 || W < 2 * h) return fail("fl_put_trapezoid: need h >= 1 and W >= 2h");
+  if (h > (int64_t)1 << 30) return fail("fl_put_trapezoid: h too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  FL_CUDA(ensure_device_init(dev, st));
+  TrapBufs B;
+  const int64_t stride = fl::put_trap_ws_doubles(f, W, h);
+  FL_CUDA(B.in.ensure(sizeof(double) * W));
+  FL_CUDA(B.out.ensure(sizeof(double) * (W + h)));
+  FL_CUDA(B.meta.ensure(2 * sizeof(int64_t)));
+  FL_CUDA(B.counter.ensure(64));
+  FL_CUDA(B.ws.ensure(sizeof(double) * stride * fl::put_chains_per_cta()));
+  FL_CUDA(B.stats.ensure(2 * sizeof(unsigned long long)));
+  FL_CUDA(cudaMemcpyAsync(B.in.p, seg, sizeof(double) * W, cudaMemcpyHostToDevice, st));
+  fl::PutParams P{};
+  P.cd = cd; P.cm = cm; P.cu = cu; P.ds = ds; P.cutoff = (int32_t)std::min<int64_t>(base_cutoff, 1 << 30);
+  P.n = h; P.mode = fl::MODE_FAST;
+  FL_CUDA(fl::launch_put_trapezoid(P, f, W, h, B.in.as<double>(), B.out.as<double>(), B.meta.as<int64_t>(),
+                                   B.counter.as<int32_t>(), B.ws.as<double>(), stride, nullptr, st));
+  int64_t meta[2] = {0, 0};
+  FL_CUDA(cudaMemcpyAsync(meta, B.meta.p, sizeof(meta), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  *kp = meta[0];
+  *status = (int32_t)meta[1];
+  if (meta[1] == 0) {
+    const int64_t len = (f + W - h) - meta[0];
+    if (len < 0 || len > W + h) return fail("fl_put_trapezoid: inconsistent output length");
+    FL_CUDA(cudaMemcpy(out_seg, B.out.p, sizeof(double) * len, cudaMemcpyDeviceToHost));
+  }
+  return 0;
+}
+
+int fl_call_trapezoid(double S, double K, double wd, double wu, double lu, int64_t base_cutoff, int64_t i, int64_t j,
+                      int64_t first, const double* run, int64_t h, double* out_run, int64_t* jp, int32_t* status,
+                      void* stream) {
+  if (!run || !out_run || !jp || !status) return fail("fl_call_trapezoid: null pointer");
+  const int64_t width = j - first + 1;
+  if (h < 1 || width < h || h > i) return fail("fl_call_trapezoid: need 1 <= h <= min(run width, i)");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  FL_CUDA(ensure_device_init(dev, st));
+  TrapBufs B;
+  const int64_t stride = fl::call_trap_ws_doubles(width, h);
+  FL_CUDA(B.in.ensure(sizeof(double) * width));
+  FL_CUDA(B.out.ensure(sizeof(double) * width));
+  FL_CUDA(B.meta.ensure(2 * sizeof(int64_t)));
+  FL_CUDA(B.counter.ensure(64));
+  FL_CUDA(B.ws.ensure(sizeof(double) * stride * fl::call_chains_per_cta()));
+  FL_CUDA(cudaMemcpyAsync(B.in.p, run, sizeof(double) * width, cudaMemcpyHostToDevice, st));
+  fl::CallParams P{};
+  P.S = S; P.K = K; P.wd = wd; P.wu = wu; P.lu = lu; P.n = i;
+  P.cutoff = (int32_t)std::min<int64_t>(base_cutoff, 1 << 30);
+  P.mode = fl::MODE_FAST;
+  FL_CUDA(fl::launch_call_trapezoid(P, i, j, first, h, B.in.as<double>(), B.out.as<double>(), B.meta.as<int64_t>(),
+                                    B.counter.as<int32_t>(), B.ws.as<double>(), stride, nullptr, st));
+  int64_t meta[2] = {0, 0};
+  FL_CUDA(cudaMemcpyAsync(meta, B.meta.p, sizeof(meta), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  *jp = meta[0];
+  *status = (int32_t)meta[1];
+  if (meta[1] == 0) {
+    const int64_t len = meta[0] - first + 1;
+    if (len < 0 || len > width) return fail("fl_call_trapezoid: inconsistent output length");
+    if (len > 0) FL_CUDA(cudaMemcpy(out_run, B.out.p, sizeof(double) * len, cudaMemcpyDeviceToHost));
+  }
   return 0;
 }
 

@@ -1,38 +1,57 @@
 // fl_call.cu -- American call on the binomial lattice: device trapezoid
 // decomposition (replaces american.fast_american_call and its recursion,
-// american.py:201-530) and the O(T^2) projected induction (replaces
-// binomial.baseline_american_call / _accel.american_call_backward,
-// binomial.py:94-130, _accel.py:62-102).
+// american.py:201-530, and american.solve_trapezoid, american.py:298-358) and
+// the O(T^2) projected induction (replaces binomial.baseline_american_call /
+// _accel.american_call_backward, binomial.py:94-130, _accel.py:62-102).
 //
-// Same execution model as the put (fl_put.cu): a persistent CTA per option,
-// explicit CTA-uniform recursion stack, linear jumps through conv_fft,
-// nonlinear leaves on warp 0 (one cell per lane, first-green by warp min),
-// the ceil(sqrt(T))-row residual strip as a shared-memory CTA sweep.
+// Same execution model as the put (fl_put.cu, fl_sched.cuh): a chain warp
+// walks one option -- junction row, trapezoid loop, halving recursion -- and
+// keeps the nonlinear leaves (binomial_strip_sweep, one column per lane,
+// first green by warp min) and the nodes up to CALL_FUSE_H (in shared memory)
+// to itself; the left / mid / bottom linear jumps are worker tasks, the
+// junction row and the ceil(sqrt(T))-row residual strip are big-group tasks.
 #include <cstdint>
 
 #include "fl_common.cuh"
 #include "fl_conv.cuh"
 #include "fl_kernels.h"
+#include "fl_sched.cuh"
 #include "fl_strip.cuh"
 #include "host_params.h"
 
 namespace fl {
 
 constexpr int CALL_LEAF = 32;
+constexpr int CALL_FUSE_H = 2 * CALL_LEAF;
 constexpr int CALL_MAX_DEPTH = 28;
-constexpr int CALL_LOGN_MAX = 13;
-constexpr int CALL_SLOTS = smem_complex_slots(1 << (CALL_LOGN_MAX - 1));
-constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per thread (width <= 2048)
+constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per big-group thread (width <= 1024)
+constexpr int CALL_SEG = CALL_FUSE_H + 8;
+static_assert(2 * CALL_SEG + CALL_LEAF + 2 + 8 <= CHAIN_SCRATCH, "call fused node scratch");
 
-int64_t call_ws_doubles(int64_t n_max) { return 2 * (n_max + 8) + (2 * n_max + 16 * CALL_MAX_DEPTH) + 64; }
-int call_fast_smem_bytes() { return CALL_SLOTS * (int)sizeof(double2); }
+enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
+
+__host__ __device__ inline int64_t call_arena_doubles(int64_t row_len, int64_t h_max) {
+  return 2 * (row_len + 8) + (2 * h_max + 16 * CALL_MAX_DEPTH) + KTABLE_DOUBLES + 64;
+}
+int64_t call_ws_doubles(int64_t n_max) { return call_arena_doubles(n_max, n_max); }
 
 __device__ __forceinline__ int64_t first_green_rec(int64_t i, int64_t j) {  // american.py:361-363
   return j >= i ? INT64_MIN : j + 1;
 }
 
-// Leaf strip (binomial_strip_sweep with lo = j-h+1, height h, h <= 32):
-// lane l holds column lo+l.  Reads in_org[lo..j], writes out_org[lo..jp].
+// reference-algorithmic cost model; the reference strip's cell
+// count depends on the boundary path, estimated as 3/4 h^2 for h rows of width h
+__device__ __forceinline__ double call_ref_jump(int64_t L, int64_t M) {
+  int64_t N = 1;
+  int lg = 0;
+  while (N < L + M - 1) { N <<= 1; ++lg; }
+  return 5.0 * (double)N * (double)lg + 6.0 * (double)(N / 2 + 1);
+}
+
+// Leaf strip (binomial_strip_sweep with lo = j-h+1, height h <= 32) on the
+// chain warp: lane l holds column lo+l.  Reads in_org[lo..j], writes
+// out_org[lo..jp], returns jp.  Operation order as _accel.py:143-158
+// (unfused products and sums).
 __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict__ in_org,
                                   double* __restrict__ out_org, int64_t lo, int64_t top_row, int64_t j0,
                                   int height, double* cells) {
@@ -40,11 +59,11 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
   const int W = (int)(j0 - lo + 1);
   const int64_t col = lo + lane;
   double v = (lane < W) ? in_org[col] : 0.0;
-  const double e2_me = exp(2.0 * (double)lane * P.lu);         // e2[col - lo]
-  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);   // e2[col + 1 - lo]
-  // B[t] = S exp((2 lo - (top_row - t)) lu), t = 0..height: parent base of step t
-  const double Bl = P.S * exp((double)(2 * lo - (top_row - lane)) * P.lu);
-  const double B32 = P.S * exp((double)(2 * lo - (top_row - 32)) * P.lu);
+  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
+  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
+  // base(t) = S exp((2 lo - (top_row - t)) lu): lane t holds the parent base of step t
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
   int64_t j = j0;
   for (int s = 0; s < height; ++s) {
     if (j < lo) break;
@@ -56,9 +75,9 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
     const double right = __shfl_down_sync(FULL, v, 1);
     int fg = INT32_MAX;
     if (col <= top) {
-      const double vr = (col + 1 <= j) ? right : fma(bp, e2_nx, -P.K);
-      const double lin = fma(P.wd, v, P.wu * vr);
-      const double grn = fma(bc, e2_me, -P.K);
+      const double vr = (col + 1 <= j) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);
+      const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
+      const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
       if (lin >= grn) {
         v = lin;
       } else {
@@ -70,53 +89,7 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
     j = (fg == INT32_MAX) ? top : lo + fg - 1;
   }
   if (col <= j && lane < W) out_org[col] = v;
-  return j;
-}
-
-// Residual strip over the whole run (american.py:499-521): lo = 0, height = i,
-// CTA-wide in shared memory.  Returns j0 and leaves row values in sv.
-__device__ int64_t call_resid_cta(const CallParams& P, const double* row_org, int64_t i, int64_t j0, double* sv,
-                                  double* se2, int* s_fg, double* cells) {
-  const int64_t W = j0 + 1;
-  for (int64_t c = threadIdx.x; c <= W; c += CTA_THREADS) {
-    sv[c] = (c < W) ? row_org[c] : 0.0;
-    se2[c] = exp(2.0 * (double)c * P.lu);
-  }
-  __syncthreads();
-  int64_t j = j0;
-  for (int64_t s = 0; s < i; ++s) {
-    if (j < 0) break;
-    const int64_t parent = i - s, child = parent - 1;
-    const int64_t top = j < child ? j : child;
-    *cells += (double)(top + 1);
-    const double bc = P.S * exp((double)(0 - child) * P.lu);
-    const double bp = P.S * exp((double)(0 - parent) * P.lu);
-    if (threadIdx.x == 0) *s_fg = INT32_MAX;
-    // two-phase update (Jacobi): read all, sync, write
-    double nv[CALL_RESID_CPT];
-    int k = 0;
-    int myfg = INT32_MAX;
-    for (int64_t c = threadIdx.x; c <= top && k < CALL_RESID_CPT; c += CTA_THREADS, ++k) {
-      const double vr = (c + 1 <= j) ? sv[c + 1] : fma(bp, se2[c + 1], -P.K);
-      const double lin = fma(P.wd, sv[c], P.wu * vr);
-      const double grn = fma(bc, se2[c], -P.K);
-      if (lin >= grn) {
-        nv[k] = lin;
-      } else {
-        nv[k] = grn;
-        if (myfg == INT32_MAX) myfg = (int)c;
-      }
-    }
-    myfg = warp_min_i32(myfg);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0 && myfg != INT32_MAX) atomicMin(s_fg, myfg);
-    k = 0;
-    for (int64_t c = threadIdx.x; c <= top && k < CALL_RESID_CPT; c += CTA_THREADS, ++k) sv[c] = nv[k];
-    __syncthreads();
-    const int fg = *s_fg;
-    j = (fg == INT32_MAX) ? top : (int64_t)fg - 1;
-    __syncthreads();
-  }
+  __syncwarp();
   return j;
 }
 
@@ -129,42 +102,121 @@ struct CallFrame {
   int h, state;
 };
 
-__device__ __forceinline__ void cta_bcast(int64_t& v, int64_t* slot) {
-  if (threadIdx.x == 0) *slot = v;
-  __syncthreads();
-  v = *slot;
-  __syncthreads();
+struct CallChainCtx {
+  SchedShared* S;
+  int c;
+  Stencil st;
+  const double* kc;
+  double* frames;
+  double* scratch;
+  int64_t ref_cut;
+  double flops, ref_flops;
+  unsigned long long* prof;
+};
+
+__device__ __forceinline__ void call_ref_enter(CallChainCtx& X, int h, int ph) {
+  if (h > X.ref_cut) X.ref_flops += call_ref_jump(h, (h + 1) / 2 + 1);
+  else if (ph > X.ref_cut) X.ref_flops += 5.0 * 0.75 * (double)h * (double)h;
+}
+__device__ __forceinline__ void call_ref_bottom(CallChainCtx& X, int h, int64_t A) {
+  const int h2 = h - (h + 1) / 2;
+  if (h > X.ref_cut && A > h2) X.ref_flops += call_ref_jump(A, h2 + 1);
 }
 
-// _solve (american.py:201-257) with an explicit stack.  vals = in_org[j-h+1 .. j];
+__device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& P, const double* in_org,
+                                             double* out_org, int64_t i, int64_t j, int h) {
+  const long long t1 = clock64();
+  double cells = 0.0;
+  const int64_t jp = call_leaf_warp(P, in_org, out_org, j - h + 1, i, j, h, &cells);
+  X.flops += 5.0 * cells;
+  if (X.prof && lane_id() == 0) {
+    prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
+    prof_add(X.prof, PROF_STRIP_N, h);
+  }
+  return jp;
+}
+
+// Node with CALL_LEAF < h <= CALL_FUSE_H, whole on the chain warp in shared
+// memory (american.py:201-257 for one level).  vals = in_org[j-h+1 .. j];
 // writes out_org[j-h+1 .. jp]; returns jp.
-__device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0, int64_t j0, int h0,
-                              double* in_org, double* out_org, double* frames, int64_t arena0, double2* sbuf,
-                              int64_t* slot, int32_t* err, double* fl) {
+__device__ int64_t call_fused_node(CallChainCtx& X, const CallParams& P, int64_t i, int64_t j, const double* in_org,
+                                   double* out_org, int h, int ph, int32_t* err) {
+  const int64_t lo = j - h + 1;
+  const long long t0 = clock64();
+  wait_conflicts(*X.S, X.c, U(in_org + lo), U(in_org + j + 1), 0, 0, U(out_org + lo), U(out_org + j + 1));
+  if (X.prof && lane_id() == 0) prof_add(X.prof, PROF_WAIT_CYC, clock64() - t0);
+  const long long t1 = clock64();
+  const int h1 = (h + 1) / 2, h2 = h - h1;
+  call_ref_enter(X, h, ph);
+  double* s_in = X.scratch;              // cols lo .. j (+4 pad)
+  double* s_asm = X.scratch + CALL_SEG;  // cols lo .. jm (+4 pad)
+  double* s_w = X.scratch + 2 * CALL_SEG;
+  warp_stage(s_in, in_org + lo, h, h + 4);
+  const double* in_s = s_in - lo;
+  double* asm_s = s_asm - lo;
+  // mid: cols lo .. j-h1 of row i-h1
+  warp_stage(s_w, X.kc + (int64_t)h1 * h1, h1 + 1);
+  X.flops += warp_conv_direct(s_in, s_asm, h2, s_w, h1 + 1);
+  call_ref_enter(X, h1, h);
+  const int64_t jm = call_leaf(X, P, in_s, asm_s, i, j, h1);
+  if (jm < j - h1 || jm > j) { *err = FL_E_GEOMETRY | 1; return 0; }
+  const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
+  call_ref_bottom(X, h, A);
+  if (lane_id() < 4) asm_s[jm + 1 + lane_id()] = 0.0;
+  __syncwarp();
+  if (A > h2) {
+    warp_stage(s_w, X.kc + (int64_t)h2 * h2, h2 + 1);
+    X.flops += warp_conv_direct(s_asm, out_org + lo, A - h2, s_w, h2 + 1);
+  }
+  call_ref_enter(X, h2, h);
+  const int64_t jp = call_leaf(X, P, asm_s, out_org, i - h1, jm, h2);
+  if (jp < jm - h2 || jp > jm) { *err = FL_E_GEOMETRY | 2; return 0; }
+  if (X.prof && lane_id() == 0) {
+    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
+    prof_add(X.prof, PROF_FUSE_N, 1);
+  }
+  return jp;
+}
+
+__device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
+                                          int h) {
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.prof);
+}
+
+// _solve (american.py:201-257) with an explicit stack on the chain warp.
+// vals = in_org[j-h+1 .. j]; writes out_org[j-h+1 .. jp]; returns jp.
+__device__ int64_t call_solve(CallChainCtx& X, const CallParams& P, int64_t i0, int64_t j0, int h0, double* in_org,
+                              double* out_org, int32_t* err) {
   CallFrame stk[CALL_MAX_DEPTH];
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
-  stk[0].arena = arena0; stk[0].state = 0;
+  stk[0].arena = 0; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
   while (sp > 0) {
     CallFrame& F = stk[sp - 1];
     const int h = F.h;
     const int h1 = (h + 1) / 2, h2 = h - h1;
+    const int ph = (sp >= 2) ? stk[sp - 2].h : 0x7fffffff;
     if (F.state == 0) {
+      const int64_t lo = F.j - h + 1;
       if (h <= CALL_LEAF) {
-        int64_t jp = 0;
-        double cells = 0.0;
-        if (threadIdx.x < 32) jp = call_leaf_warp(P, F.in_org, F.out_org, F.j - h + 1, F.i, F.j, h, &cells);
-        cta_bcast(jp, slot);
-        *fl += 5.0 * cells;  // meaningful on thread 0 (the accumulating thread)
-        ret = jp;
+        wait_conflicts(*X.S, X.c, U(F.in_org + lo), U(F.in_org + F.j + 1), 0, 0, U(F.out_org + lo),
+                       U(F.out_org + F.j + 1));
+        call_ref_enter(X, h, ph);
+        ret = call_leaf(X, P, F.in_org, F.out_org, F.i, F.j, h);
         --sp;
         continue;
       }
-      const int64_t lo = F.j - h + 1;
-      F.asm_org = frames + F.arena - lo;
+      if (h <= CALL_FUSE_H) {
+        ret = call_fused_node(X, P, F.i, F.j, F.in_org, F.out_org, h, ph, err);
+        if (*err) return 0;
+        --sp;
+        continue;
+      }
+      call_ref_enter(X, h, ph);
+      F.asm_org = X.frames + F.arena - lo;
       // mid: cols lo .. j-h1 of row i-h1
-      *fl += conv_fft(F.in_org + lo, h, F.asm_org + lo, h2, h1, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+      call_conv(X, F.in_org + lo, h, F.asm_org + lo, h2, h1);
       F.state = 1;
       CallFrame& C = stk[sp];
       C.i = F.i; C.j = F.j; C.h = h1; C.in_org = F.in_org; C.out_org = F.asm_org;
@@ -172,12 +224,13 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       if (++sp >= CALL_MAX_DEPTH) { *err = FL_E_CAPACITY | 1; return 0; }
     } else if (F.state == 1) {
       const int64_t jm = ret;
-      if (jm < F.j - h1 || jm > F.j) { *err = FL_E_GEOMETRY | 1; return 0; }
+      if (jm < F.j - h1 || jm > F.j) { *err = FL_E_GEOMETRY | 3; return 0; }
       F.jm = jm;
       const int64_t lo = F.j - h + 1;
       const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
+      call_ref_bottom(X, h, A);
       // bottom: cols lo .. jm-h2 of row i-h
-      *fl += conv_fft(F.asm_org + lo, A, F.out_org + lo, A - h2, h2, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+      if (A > h2) call_conv(X, F.asm_org + lo, A, F.out_org + lo, A - h2, h2);
       F.state = 2;
       CallFrame& C = stk[sp];
       C.i = F.i - h1; C.j = jm; C.h = h2; C.in_org = F.asm_org; C.out_org = F.out_org;
@@ -185,7 +238,7 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
       ++sp;
     } else {
       const int64_t jp = ret;
-      if (jp < F.jm - h2 || jp > F.jm) { *err = FL_E_GEOMETRY | 2; return 0; }
+      if (jp < F.jm - h2 || jp > F.jm) { *err = FL_E_GEOMETRY | 4; return 0; }
       --sp;
     }
   }
@@ -193,101 +246,265 @@ __device__ int64_t call_solve(const CallParams& P, const Stencil& st, int64_t i0
 }
 
 __device__ void call_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, int64_t c) {
-  if (threadIdx.x == 0 && out.bt != nullptr && cnt < out.cap) {
+  if (lane_id() == 0 && out.bt != nullptr && cnt < out.cap) {
     out.bt[(int64_t)o * out.cap + cnt] = t;
     out.bc[(int64_t)o * out.cap + cnt] = c;
   }
   ++cnt;
 }
 
-__global__ void __launch_bounds__(CTA_THREADS, 2)
-call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
-                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
-  extern __shared__ double2 sbuf[];
-  __shared__ int s_work;
-  __shared__ int s_fg;
-  __shared__ int64_t s_slot;
-  double* arena = ws + (int64_t)blockIdx.x * ws_stride;
-  for (;;) {
-    if (threadIdx.x == 0) s_work = atomicAdd(counter, 1);
-    __syncthreads();
-    const int w = s_work;
-    __syncthreads();
-    if (w >= nwork) break;
-    const int o = order[w];
-    const CallParams P = opts[o];
-    const int64_t n = P.n;
-    double* rowA = arena;
-    double* rowB = arena + (n + 8);
-    double* frames = arena + 2 * (n + 8);
-    const Stencil st{P.wd, P.wu, 0.0, 1};
-    double flops = 0.0;
-    int32_t err = 0, cnt = 0;
-    call_record(out, o, cnt, n, first_green_rec(n, P.top_b));
-    int64_t i = n - 1, j = P.junc_j;
-    call_record(out, o, cnt, i, first_green_rec(i, j));
-    // junction row T-1 (american.py:412-422)
-    const int64_t start = P.top_b > 0 ? P.top_b : 0;
-    for (int64_t c = threadIdx.x; c <= j; c += CTA_THREADS) {
-      double v = 0.0;
-      if (c >= start) {
-        double l0 = P.S * exp((2.0 * (double)c - (double)n) * P.lu) - P.K;
-        double l1 = P.S * exp((2.0 * (double)(c + 1) - (double)n) * P.lu) - P.K;
-        l0 = l0 > 0.0 ? l0 : 0.0;
-        l1 = l1 > 0.0 ? l1 : 0.0;
-        v = fma(P.wd, l0, P.wu * l1);
-      }
-      rowA[c] = v;
+__device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams& P, int64_t row_len, int64_t h_max,
+                                         double* arena, double* scratch, unsigned long long* prof) {
+  double* frames = arena + 2 * (row_len + 8);
+  double* kc = frames + 2 * h_max + 16 * CALL_MAX_DEPTH;
+  const Stencil st{P.wd, P.wu, 0.0, 1};
+  build_kernel_table(kc, st, scratch);
+  return CallChainCtx{&S, c, st, kc, frames, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+}
+
+// The trapezoid loop from row i / boundary j down to the residual (american.py:486-498).
+__device__ void call_trapezoids(CallChainCtx& X, const CallParams& P, int64_t& i, int64_t& j, int64_t first,
+                                int64_t resid, double*& cur_org, double*& nxt_org, int32_t* err, const BatchOut* out,
+                                int o, int32_t* cnt) {
+  while (i > resid && j >= first) {
+    const int64_t hh = (j - first + 1 < i - resid) ? j - first + 1 : i - resid;
+    const int h = (int)hh;
+    // left: cols first .. j-h of row i-h (american.py:341-344)
+    const int64_t L = j - first + 1;
+    if (L > hh) {
+      X.ref_flops += call_ref_jump(L, hh + 1);
+      call_conv(X, cur_org + first, L, nxt_org + first, L - hh, h);
     }
-    __syncthreads();
-    const int64_t resid = (int64_t)floor(sqrt((double)(n - 1))) + 1;  // isqrt(n-1)+1 (exact below 2^52)
-    double* cur = rowA;
-    double* nxt = rowB;
-    while (i > resid && j >= 0) {
-      const int64_t hh = (j + 1 < i - resid) ? j + 1 : i - resid;
-      const int h = (int)hh;
-      // left: cols 0 .. j-h of row i-h (american.py:341-344)
-      if (j + 1 > hh) flops += conv_fft(cur, j + 1, nxt, j + 1 - hh, h, st, sbuf, CALL_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
-      const int64_t jp = call_solve(P, st, i, j, h, cur, nxt, frames, 0, sbuf, &s_slot, &err, &flops);
-      if (err) break;
-      i -= hh;
-      j = jp;
-      call_record(out, o, cnt, i, first_green_rec(i, j));
-      double* t = cur;
-      cur = nxt;
-      nxt = t;
-    }
-    double price = 0.0;
-    if (!err) {
-      if (j < 0) {
-        price = P.S - P.K;
-      } else {
-        double* sv = (double*)sbuf;
-        double* se2 = sv + (CALL_SLOTS);
-        if (j + 2 > CALL_SLOTS || j + 1 > (int64_t)CALL_RESID_CPT * CTA_THREADS) {
-          err = FL_E_CAPACITY | 2;
-        } else {
-          double cells = 0.0;
-          const int64_t j0 = call_resid_cta(P, cur, i, j, sv, se2, &s_fg, &cells);
-          flops += 5.0 * cells;
-          price = (j0 >= 0) ? sv[0] : P.S - P.K;
-          if (i > 0) call_record(out, o, cnt, 0, first_green_rec(0, j0));
-          __syncthreads();
-        }
-      }
-    }
-    if (threadIdx.x == 0) {
-      out.price[o] = err ? 0.0 : price;
-      out.status[o] = err;
-      if (out.bcount) out.bcount[o] = err ? 0 : cnt;
-      if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
-    }
-    __syncthreads();
+    const int64_t jp = call_solve(X, P, i, j, h, cur_org, nxt_org, err);
+    if (*err) return;
+    i -= hh;
+    j = jp;
+    if (out) call_record(*out, o, *cnt, i, first_green_rec(i, j));
+    double* t = cur_org;
+    cur_org = nxt_org;
+    nxt_org = t;
   }
 }
 
+// fast_american_call (american.py:471-530) for option o on chain warp c.
+__device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, int o, double* arena,
+                                  double* scratch, const BatchOut& out, double* chain_flops) {
+  const long long t_opt = clock64();
+  const int64_t n = P.n;
+  CallChainCtx X = call_chain_setup(S, c, P, n, n, arena, scratch, out.prof);
+  double* cur_org = arena;
+  double* nxt_org = arena + (n + 8);
+  int32_t err = 0, cnt = 0;
+  call_record(out, o, cnt, n, first_green_rec(n, P.top_b));
+  int64_t i = n - 1, j = P.junc_j;
+  call_record(out, o, cnt, i, first_green_rec(i, j));
+  {  // junction row T-1 (american.py:412-422) into row A
+    Task t;
+    t.kind = TK_CALL_INIT;
+    t.x = nullptr; t.w = nullptr; t.y = cur_org;
+    t.L = j + 1; t.Lout = 0;
+    t.c0 = P.wd; t.c1 = P.wu; t.c2 = P.lu; t.d0 = P.S;
+    t.i0 = n; t.i1 = P.top_b > 0 ? P.top_b : 0;
+    t.i2 = __double_as_longlong(P.K);  // K travels as a bit pattern
+    t.h = 0; t.span = 0;
+    issue(S, c, RING_BIG, t, 0, 0, U(cur_org), U(cur_org + j + 1));
+  }
+  const int64_t resid = (int64_t)floor(sqrt((double)(n - 1))) + 1;  // isqrt(n-1)+1 (exact below 2^52)
+  call_trapezoids(X, P, i, j, 0, resid, cur_org, nxt_org, &err, &out, o, &cnt);
+  double price = 0.0;
+  if (!err) {
+    if (j < 0) {
+      price = P.S - P.K;
+    } else if (j + 2 > BIG_SLOTS || j + 1 > (int64_t)CALL_RESID_CPT * BIG_THREADS) {
+      err = FL_E_CAPACITY | 2;
+    } else {
+      Task t;
+      t.kind = TK_CALL_RESID;
+      t.x = cur_org; t.y = nullptr; t.w = nullptr;
+      t.L = 0; t.Lout = 0;
+      t.c0 = P.wd; t.c1 = P.wu; t.c2 = P.lu; t.d0 = P.S;
+      t.i0 = i; t.i1 = j; t.i2 = __double_as_longlong(P.K);
+      t.h = 0; t.span = 0;
+      const int id = issue(S, c, RING_BIG, t, U(cur_org), U(cur_org + j + 1), 0, 0);
+      warp_wait_done(S, id);
+      const int64_t j0 = S.iresult[c];
+      price = (j0 >= 0) ? S.result[c] : P.S - P.K;
+      X.flops += 5.0 * S.result2[c];
+      X.ref_flops += 5.0 * S.result2[c];
+      if (i > 0) call_record(out, o, cnt, 0, first_green_rec(0, j0));
+    }
+  }
+  wait_all_own(S, c);
+  if (lane_id() == 0) {
+    out.price[o] = err ? 0.0 : price;
+    out.status[o] = err;
+    if (out.bcount) out.bcount[o] = err ? 0 : cnt;
+    if (out.flops) atomicAdd(out.flops + 1, (unsigned long long)X.ref_flops);
+    prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
+  }
+  *chain_flops += X.flops;
+}
+
+// Worker side of the call-specific tasks.
+__device__ double call_exec_task(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN,
+                                 const double2* tq, const Grp& g) {
+  if (t.kind == TK_CALL_INIT) {
+    const double wd = t.c0, wu = t.c1, lu = t.c2, S0 = t.d0, K = __longlong_as_double(t.i2);
+    const int64_t n = t.i0, start = t.i1;
+    double* row = t.y;
+    for (int64_t c = g.t; c < t.L; c += g.n) {
+      double v = 0.0;
+      if (t.x != nullptr) {
+        v = t.x[c];
+      } else if (c >= start) {
+        double l0 = __dsub_rn(__dmul_rn(S0, exp(__dmul_rn(__dsub_rn(2.0 * (double)c, (double)n), lu))), K);
+        double l1 = __dsub_rn(__dmul_rn(S0, exp(__dmul_rn(__dsub_rn(2.0 * (double)(c + 1), (double)n), lu))), K);
+        l0 = l0 > 0.0 ? l0 : 0.0;
+        l1 = l1 > 0.0 ? l1 : 0.0;
+        v = __dadd_rn(__dmul_rn(wd, l0), __dmul_rn(wu, l1));
+      }
+      row[c] = v;
+    }
+    return 0.0;
+  }
+  if (t.kind == TK_CALL_RESID) {
+    // residual strip over the whole run (american.py:499-521): lo = 0, height = i
+    const double wd = t.c0, wu = t.c1, lu = t.c2, S0 = t.d0, K = __longlong_as_double(t.i2);
+    const int64_t i = t.i0, j0 = t.i1;
+    const int64_t W = j0 + 1;
+    double* sv = (double*)sbuf;
+    double* se2 = sv + (W + 1);
+    int* s_fg = (int*)(se2 + (W + 1));
+    for (int64_t c = g.t; c <= W; c += g.n) {
+      sv[c] = (c < W) ? t.x[c] : 0.0;
+      se2[c] = exp(2.0 * (double)c * lu);
+    }
+    gsync(g);
+    int64_t j = j0;
+    double cells = 0.0;
+    for (int64_t s = 0; s < i; ++s) {
+      if (j < 0) break;
+      const int64_t parent = i - s, child = parent - 1;
+      const int64_t top = j < child ? j : child;
+      cells += (double)(top + 1);
+      const double bc = __dmul_rn(S0, exp((double)(0 - child) * lu));
+      const double bp = __dmul_rn(S0, exp((double)(0 - parent) * lu));
+      if (g.t == 0) *s_fg = INT32_MAX;
+      double nv[CALL_RESID_CPT];
+      int k = 0;
+      int myfg = INT32_MAX;
+      for (int64_t c = g.t; c <= top && k < CALL_RESID_CPT; c += g.n, ++k) {
+        const double vr = (c + 1 <= j) ? sv[c + 1] : __dsub_rn(__dmul_rn(bp, se2[c + 1]), K);
+        const double lin = __dadd_rn(__dmul_rn(wd, sv[c]), __dmul_rn(wu, vr));
+        const double grn = __dsub_rn(__dmul_rn(bc, se2[c]), K);
+        if (lin >= grn) {
+          nv[k] = lin;
+        } else {
+          nv[k] = grn;
+          if (myfg == INT32_MAX) myfg = (int)c;
+        }
+      }
+      myfg = warp_min_i32(myfg);
+      gsync(g);
+      if ((g.t & 31) == 0 && myfg != INT32_MAX) atomicMin(s_fg, myfg);
+      k = 0;
+      for (int64_t c = g.t; c <= top && k < CALL_RESID_CPT; c += g.n, ++k) sv[c] = nv[k];
+      gsync(g);
+      const int fg = *s_fg;
+      j = (fg == INT32_MAX) ? top : (int64_t)fg - 1;
+      gsync(g);
+    }
+    if (g.t == 0) {
+      S.result[t.chain] = sv[0];
+      S.iresult[t.chain] = j;
+      S.result2[t.chain] = cells;
+    }
+    return 5.0 * cells;
+  }
+  return exec_generic(t, sbuf, slots, logN, tq, g);
+}
+
+struct CallPricer {
+  const CallParams* opts;
+  const int32_t* order;
+  BatchOut out;
+  __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* flops) const {
+    const int o = order[w];
+    call_chain_option(S, c, opts[o], o, arena, scratch, out, flops);
+  }
+  __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
+                         const Grp& g) const {
+    return call_exec_task(S, t, sbuf, slots, logN, tq, g);
+  }
+};
+
+__global__ void __launch_bounds__(SCHED_THREADS, 1)
+call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
+                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
+  const CallPricer pr{opts, order, out};
+  sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
+}
+
 // ---------------------------------------------------------------------------
-// O(T^2) projected backward induction (american_call_backward).
+// solve_trapezoid (american.py:298-358): one trapezoid of height h from row i,
+// run = red values of cols first .. j.  Output: meta[0] = new boundary jp,
+// meta[1] = status, values of cols first .. jp of row i-h into out.
+
+struct CallTrapPricer {
+  CallParams P;
+  int64_t i, j, first, h;
+  const double* run;
+  double* out;
+  int64_t* meta;
+  unsigned long long* flops;
+  __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* fl) const {
+    const int64_t width = j - first + 1;
+    CallChainCtx X = call_chain_setup(S, c, P, width, h, arena, scratch, nullptr);
+    double* cur_org = arena - first;
+    double* nxt_org = arena + (width + 8) - first;
+    {  // load the run
+      Task t;
+      t.kind = TK_CALL_INIT;
+      t.x = run; t.w = nullptr; t.y = arena;
+      t.L = width; t.Lout = 0;
+      t.c0 = t.c1 = t.c2 = 0.0; t.d0 = 0.0;
+      t.i0 = t.i1 = t.i2 = 0; t.h = 0; t.span = 0;
+      issue(S, c, RING_BIG, t, 0, 0, U(arena), U(arena + width));
+    }
+    int32_t err = 0;
+    int64_t ii = i, jj = j;
+    // exactly one trapezoid: resid chosen so the loop runs once with height h
+    const int64_t hh = h;
+    const int64_t L = width;
+    if (L > hh) {
+      X.ref_flops += call_ref_jump(L, hh + 1);
+      call_conv(X, cur_org + first, L, nxt_org + first, L - hh, (int)hh);
+    }
+    const int64_t jp = call_solve(X, P, ii, jj, (int)hh, cur_org, nxt_org, &err);
+    wait_all_own(S, c);
+    const int64_t len = err ? 0 : jp - first + 1;
+    for (int64_t k = lane_id(); k < len; k += 32) out[k] = nxt_org[first + k];
+    if (lane_id() == 0) {
+      meta[0] = err ? 0 : jp;
+      meta[1] = err;
+      if (flops) atomicAdd(flops + 1, (unsigned long long)X.ref_flops);
+    }
+    *fl += X.flops;
+  }
+  __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
+                         const Grp& g) const {
+    return call_exec_task(S, t, sbuf, slots, logN, tq, g);
+  }
+};
+
+__global__ void __launch_bounds__(SCHED_THREADS, 1)
+call_trap_kernel(CallTrapPricer pr, int32_t* counter, double* __restrict__ ws, int64_t ws_stride) {
+  sched_body(pr, 1, counter, ws, ws_stride, pr.flops, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// O(T^2) projected backward induction (american_call_backward, _accel.py:62-102).
+// Unfused, left-to-right operation order as the reference: bit-identical.
 
 __global__ void __launch_bounds__(CTA_THREADS)
 call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
@@ -305,11 +522,11 @@ call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restr
   if (threadIdx.x == 0) s_fg = INT32_MAX;
   __syncthreads();
   for (int64_t j = threadIdx.x; j <= n; j += CTA_THREADS) {
-    const double u = exp((2.0 * (double)j - (double)n) * P.lu);
+    const double u = exp(__dmul_rn(__dsub_rn(2.0 * (double)j, (double)n), P.lu));
     u2[j] = u;
-    const double v = P.S * exp((2.0 * (double)j - (double)n) * P.lu) - P.K;  // leaf_row
+    const double v = __dsub_rn(__dmul_rn(P.S, u), P.K);  // leaf_row
     a[j] = v > 0.0 ? v : 0.0;
-    if (P.S * u - P.K > 0.0) atomicMin(&s_fg, (int)j);
+    if (v > 0.0) atomicMin(&s_fg, (int)j);
   }
   __syncthreads();
   auto put_rec = [&](int64_t row, int fg) {
@@ -323,11 +540,11 @@ call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restr
   for (int64_t i = n - 1; i >= 0; --i) {
     if (threadIdx.x == 0) s_fg = INT32_MAX;
     __syncthreads();
-    const double scale = P.S * exp((double)(n - i) * P.lu);
+    const double scale = __dmul_rn(P.S, exp((double)(n - i) * P.lu));
     int myfg = INT32_MAX;
     for (int64_t j = threadIdx.x; j <= i; j += CTA_THREADS) {
-      const double lin = fma(P.wd, a[j], P.wu * a[j + 1]);
-      const double grn = fma(scale, u2[j], -P.K);
+      const double lin = __dadd_rn(__dmul_rn(P.wd, a[j]), __dmul_rn(P.wu, a[j + 1]));
+      const double grn = __dsub_rn(__dmul_rn(scale, u2[j]), P.K);
       if (lin >= grn) {
         b[j] = lin;
       } else {
@@ -353,19 +570,45 @@ call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restr
   }
 }
 
+// ---------------------------------------------------------------------------
+// launchers
+
+static cudaError_t call_configure() {
+  static bool configured = false;
+  if (configured) return cudaSuccess;
+  const int smem = sched_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(call_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(call_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
+int call_chains_per_cta() { return NCHAIN; }
+
 cudaError_t launch_call_fast(const CallParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                              int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream) {
-  static bool configured = false;
-  const int smem = call_fast_smem_bytes();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(call_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  if (nwork <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  cudaError_t e = call_configure();
   if (e != cudaSuccess) return e;
-  call_fast_kernel<<<grid, CTA_THREADS, smem, stream>>>(opts, order, nwork, counter, ws, ws_stride, out);
+  if (nwork <= 0) return cudaSuccess;
+  e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  if (e != cudaSuccess) return e;
+  call_fast_kernel<<<grid, SCHED_THREADS, sched_smem_bytes(), stream>>>(opts, order, nwork, counter, ws, ws_stride,
+                                                                          out);
+  return cudaGetLastError();
+}
+
+int64_t call_trap_ws_doubles(int64_t width, int64_t h) { return call_arena_doubles(width, h); }
+
+cudaError_t launch_call_trapezoid(const CallParams& P, int64_t i, int64_t j, int64_t first, int64_t h,
+                                  const double* run, double* out, int64_t* meta, int32_t* counter, double* ws,
+                                  int64_t ws_stride, unsigned long long* flops, cudaStream_t stream) {
+  cudaError_t e = call_configure();
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  if (e != cudaSuccess) return e;
+  const CallTrapPricer pr{P, i, j, first, h, run, out, meta, flops};
+  call_trap_kernel<<<1, SCHED_THREADS, sched_smem_bytes(), stream>>>(pr, counter, ws, ws_stride);
   return cudaGetLastError();
 }
 

@@ -18,7 +18,7 @@ struct BatchOut {
   int64_t* bc;
   int32_t* bcount;
   int32_t cap;
-  unsigned long long* flops;  // executed fp64 flops of the fast kernels (accumulated), may be null
+  unsigned long long* flops;  // [0] executed fp64 flops, [1] reference-algorithmic flops (accumulated), may be null
   unsigned long long* prof;   // optional profile counters (PROF_* in fl_sched.cuh), may be null
 };
 
@@ -32,6 +32,10 @@ cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwo
                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
 cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, double* ws,
                                 int64_t ws_stride, BatchOut out, cudaStream_t stream);
+int64_t put_trap_ws_doubles(int64_t f, int64_t W, int64_t h);
+cudaError_t launch_put_trapezoid(const PutParams& P, int64_t f, int64_t W, int64_t h, const double* seg,
+                                 double* out, int64_t* meta, int32_t* counter, double* ws, int64_t ws_stride,
+                                 unsigned long long* flops, cudaStream_t stream);
 
 cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, BatchOut out,
                              cudaStream_t stream);
@@ -44,7 +48,11 @@ cudaError_t launch_linear_steps(const double* x, int64_t L, double* y, int64_t L
 
 // American call (fl_call.cu)
 int64_t call_ws_doubles(int64_t n_max);
-int call_fast_smem_bytes();
+int call_chains_per_cta();
+int64_t call_trap_ws_doubles(int64_t width, int64_t h);
+cudaError_t launch_call_trapezoid(const CallParams& P, int64_t i, int64_t j, int64_t first, int64_t h,
+                                  const double* run, double* out, int64_t* meta, int32_t* counter, double* ws,
+                                  int64_t ws_stride, unsigned long long* flops, cudaStream_t stream);
 cudaError_t launch_call_fast(const CallParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                              int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
 cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,

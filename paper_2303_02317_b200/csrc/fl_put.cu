@@ -1,10 +1,11 @@
 // fl_put.cu -- American put on the anchored BSM grid: device divide-and-conquer
-// (replaces bsm.fast_put_bsm and its recursion, bsm.py:402-713) and the O(T^2)
-// projected march (replaces bsm.baseline_put_fd / _accel.put_march_window,
-// bsm.py:273-338, _accel.py:163-200).
+// (replaces bsm.fast_put_bsm and its recursion, bsm.py:402-713, and
+// bsm.solve_bsm_trapezoid, bsm.py:504-582) and the O(T^2) projected march
+// (replaces bsm.baseline_put_fd / _accel.put_march_window, bsm.py:273-338,
+// _accel.py:163-200).
 //
-// Fast path: a persistent, warp-specialised CTA per SM (fl_sched.cuh).  Each
-// chain warp prices one option at a time, pulled from a global queue in
+// Fast path: the persistent warp-specialised CTA of fl_sched.cuh.  Each chain
+// warp prices one option at a time, pulled from a global queue in
 // decreasing-cost order:
 //   * the stage loop (bsm.py:639-665) and the _solve_q halving recursion
 //     (bsm.py:443-501) run on the chain warp with an explicit stack;
@@ -16,6 +17,12 @@
 //   * the apex finish (bsm.py:679-713) is a worker task over shared memory.
 // Row data live in a per-chain HBM arena, column-indexed, so the reference's
 // concatenations (upper|mid, lower|bottom, near|far) are free.
+//
+// Work accounting: besides the executed flops, every chain adds the
+// REFERENCE-ALGORITHMIC flops of its option (the reference's decomposition
+// at its base_cutoff: 5 flops per projected cell of each reference strip,
+// 5 N log2 N + 6 (N/2+1) per reference FFT jump of size N = next_pow2(L+M-1),
+// SURVEY 8(d)).  That is the numerator of the reported roofline fraction.
 #include <cstdint>
 
 #include "fl_common.cuh"
@@ -34,13 +41,23 @@ constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
 constexpr int FUSE_H = 2 * PUT_LEAF;                   // nodes up to this height are fused on the chain
 constexpr int PUT_MAX_DEPTH = 24;
-// chain scratch (doubles): fused-node input and assembled rows + staged weights
-constexpr int FUSE_SEG = 2 * FUSE_H + 8;
-constexpr int CHAIN_SCRATCH = 2 * FUSE_SEG + (2 * PUT_LEAF + 1) + 16 > 4 * DIRECT_H + 8
-                                  ? 2 * FUSE_SEG + (2 * PUT_LEAF + 1) + 16
-                                  : 4 * DIRECT_H + 8;
+constexpr int FUSE_SEG = 2 * FUSE_H + 8;  // fused-node row buffers (doubles, incl. zero pad)
+static_assert(2 * FUSE_SEG + 2 * PUT_LEAF + 1 + 8 <= CHAIN_SCRATCH, "fused node scratch");
+static_assert(2 * (2 * DIRECT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
-enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1 };
+enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD = TK_USER + 2 };
+
+// reference-algorithmic cost model
+__device__ __forceinline__ double ref_jump_flops(int64_t L, int64_t M) {
+  int64_t N = 1;
+  int lg = 0;
+  while (N < L + M - 1) { N <<= 1; ++lg; }
+  return 5.0 * (double)N * (double)lg + 6.0 * (double)(N / 2 + 1);
+}
+// projected cells of a reference strip of width W swept `rows` times (shrinking cone)
+__device__ __forceinline__ double ref_strip_flops(int64_t W, int64_t rows) {
+  return 5.0 * ((double)rows * (double)W - (double)rows * (double)(rows + 1));
+}
 
 struct PutFrame {
   int64_t f, km;
@@ -51,8 +68,9 @@ struct PutFrame {
   int h, state;
 };
 
+// Column window of a chain's stage / payoff buffers.
 struct PutLayout {
-  int64_t colbase;  // lowest column held in the stage / payoff buffers
+  int64_t colbase;  // lowest column held
   int64_t span;     // buffer length
 };
 
@@ -64,11 +82,22 @@ __host__ __device__ inline PutLayout put_layout(int64_t n, int64_t ks) {
   return L;
 }
 
+// trapezoid problem (solve_bsm_trapezoid): columns f-2h-1 .. f+W
+__host__ __device__ inline PutLayout put_trap_layout(int64_t f, int64_t W, int64_t h) {
+  PutLayout L;
+  L.colbase = f - 2 * h - 4 * FUSE_H - 16;
+  L.span = (f + W + 8) - L.colbase + 1;
+  return L;
+}
+
+__host__ __device__ inline int64_t put_arena_doubles(int64_t span, int64_t n_rows) {
+  return 3 * span + (2 * n_rows + 64 * PUT_MAX_DEPTH) + KTABLE_DOUBLES + 64;
+}
+
 // doubles needed per chain for a batch whose options have at most these sizes
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max) {
   const int64_t span = 2 * n_max + ks_pos_max + 4 * FUSE_H + 32;
-  const int64_t frames = 2 * n_max + 64 * PUT_MAX_DEPTH;
-  return 3 * span + frames + KTABLE_DOUBLES + 64;
+  return put_arena_doubles(span, n_max);
 }
 
 struct PutChainCtx {
@@ -79,9 +108,22 @@ struct PutChainCtx {
   double* frames;
   const double* pay_org;
   double* scratch;   // chain's shared scratch (CHAIN_SCRATCH doubles)
-  double flops;      // chain-side flops (lane-uniform)
+  int64_t ref_cut;   // the reference's base_cutoff (work accounting only)
+  double flops;      // executed chain-side flops (lane-uniform)
+  double ref_flops;  // reference-algorithmic flops (lane-uniform)
   unsigned long long* prof;
 };
+
+// Reference cost of a recursion node of height h whose parent has height ph:
+// the reference strips it whole if h <= cutoff (and its parent did not), else
+// it issues the mid jump here and the bottom jump once km is known.
+__device__ __forceinline__ void ref_node_enter(PutChainCtx& X, int h, int ph) {
+  if (h > X.ref_cut) X.ref_flops += ref_jump_flops(2 * (int64_t)h, 2 * (int64_t)((h + 1) / 2) + 1);
+  else if (ph > X.ref_cut) X.ref_flops += ref_strip_flops(4 * (int64_t)h + 2, h);
+}
+__device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A) {
+  if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
+}
 
 // Leaf strip on the chain warp.  in_org / out_org may address shared memory.
 __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
@@ -92,23 +134,23 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
     prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
     prof_add(X.prof, PROF_STRIP_N, height);
   }
-  const double W = (double)(hi - lo + 1);
-  X.flops += 5.0 * (W * height - (double)height * (height + 1));
+  X.flops += ref_strip_flops(hi - lo + 1, height);
   return kb;
 }
 
 // A node with PUT_LEAF < h <= FUSE_H done whole on the chain warp (bsm.py:443-501
 // for one level): input cols f+1..f+2h of in_org, output cols kp+1..f+h of out_org.
 // The mid jump, the first leaf, the assembled row and the bottom jump stay in
-// shared memory.  Returns kp (or NONE_SEEN-derived error through *err).
+// shared memory.
 __device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f, const double* in_org,
-                                  double* out_org, int h, int32_t* err) {
+                                  double* out_org, int h, int ph, int32_t* err) {
   const long long t0 = clock64();
   wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + f + 2 * h + 1), 0, 0, U(out_org + f - h),
                  U(out_org + f + h + 1));
   if (X.prof && lane_id() == 0) prof_add(X.prof, PROF_WAIT_CYC, clock64() - t0);
   const long long t1 = clock64();
   const int h1 = (h + 1) / 2, h2 = h - h1;
+  ref_node_enter(X, h, ph);
   double* s_in = X.scratch;                 // cols f+1 .. f+2h  (+4 pad)
   double* s_asm = X.scratch + FUSE_SEG;     // cols f-h1+1 .. f+2h-h1 (+4 pad)
   double* s_w = X.scratch + 2 * FUSE_SEG;   // staged weights
@@ -120,16 +162,19 @@ __device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f,
   warp_stage(s_w, X.kc + (int64_t)h1 * h1, M);
   X.flops += warp_conv_direct(s_in, asm_s + f + h1 + 1, 2 * (int64_t)(h - h1), s_w, M);
   // first half-height leaf
+  ref_node_enter(X, h1, h);
   const int64_t km = put_leaf(X, P, in_s, asm_s, f - 2 * h1 - 1, f + 2 * h1, f, h1);
   if (km == NONE_SEEN || km < f - h1 || km > f) { *err = FL_E_GEOMETRY | 1; return 0; }
   // bottom: cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
   const int64_t A = f + 2 * (int64_t)h - h1 - km;
+  ref_node_bottom(X, h, A);
   if (lane_id() < 4) asm_s[f + 2 * h - h1 + 1 + lane_id()] = 0.0;  // zero pad behind the assembled row
   __syncwarp();  // leaf stores visible to the whole warp
   M = 2 * h2 + 1;
   warp_stage(s_w, X.kc + (int64_t)h2 * h2, M);
   X.flops += warp_conv_direct(asm_s + km + 1, out_org + km + h2 + 1, A - 2 * (int64_t)h2, s_w, M);
   // second half-height leaf from the assembled row
+  ref_node_enter(X, h2, h);
   const int64_t kp = put_leaf(X, P, asm_s, out_org, km - 2 * h2 - 1, km + 2 * h2, km, h2);
   if (kp == NONE_SEEN || kp < km - h2 || kp > km) { *err = FL_E_GEOMETRY | 2; return 0; }
   if (X.prof && lane_id() == 0) {
@@ -155,10 +200,12 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
   while (sp > 0) {
     PutFrame& F = stk[sp - 1];
     const int h = F.h;
+    const int ph = (sp >= 2) ? stk[sp - 2].h : 0x7fffffff;
     if (F.state == 0) {
       if (h <= PUT_LEAF) {
         wait_conflicts(*X.S, X.c, U(F.in_org + F.f + 1), U(F.in_org + F.f + 2 * h + 1), 0, 0,
                        U(F.out_org + F.f - h), U(F.out_org + F.f + h + 1));
+        ref_node_enter(X, h, ph);
         const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
@@ -166,11 +213,12 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
         continue;
       }
       if (h <= FUSE_H) {
-        ret = put_fused_node(X, P, F.f, F.in_org, F.out_org, h, err);
+        ret = put_fused_node(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
         --sp;
         continue;
       }
+      ref_node_enter(X, h, ph);
       const int h1 = (h + 1) / 2;
       F.asm_org = X.frames + F.arena - (F.f - h1 + 1);
       // mid: cols f+h1+1 .. f+2h-h1 of row t+h1 from the 2h inputs
@@ -186,6 +234,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
       if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
       F.km = km;
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;  // assembled cols km+1 .. f+2h-h1
+      ref_node_bottom(X, h, A);
       // bottom: cols km+h2+1 .. f+h of row t+h
       put_conv(X, F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2);
       F.state = 2;
@@ -203,6 +252,18 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
   return ret;
 }
 
+// One stage (_advance_stage, bsm.py:557-582): far jump + boundary recursion,
+// cur -> nxt over hh rows.  Returns the new boundary.
+__device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int64_t red, int64_t hh,
+                             double* cur_org, double* nxt_org, int32_t* err) {
+  const int h = (int)hh;
+  if (red > 2 * hh) {  // far: cols f+h+1 .. f+red-h stay linear
+    X.ref_flops += ref_jump_flops(red, 2 * hh + 1);
+    put_conv(X, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h);
+  }
+  return put_solve_q(X, P, f, cur_org, nxt_org, h, err);
+}
+
 __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, int64_t c) {
   if (lane_id() == 0 && out.bt != nullptr && cnt < out.cap) {
     out.bt[(int64_t)o * out.cap + cnt] = t;
@@ -211,34 +272,40 @@ __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, 
   ++cnt;
 }
 
-// One option on chain warp c.
+// Arena: stage rows A | B | payoff table | recursion frames | kernel table.
+__device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P, const PutLayout& Lo,
+                                       int64_t n_rows, double* arena, double* scratch, unsigned long long* prof,
+                                       const double* init_src, int64_t init_col0, int64_t init_len) {
+  double* bufA = arena;
+  double* pay = arena + 2 * Lo.span;
+  double* frames = arena + 3 * Lo.span;
+  double* kc = frames + 2 * n_rows + 64 * PUT_MAX_DEPTH;
+  const Stencil st{P.cd, P.cm, P.cu, 2};
+  build_kernel_table(kc, st, scratch);
+  PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+  // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
+  // loaded with an initial segment (cols init_col0 .. +init_len)
+  Task t;
+  t.kind = TK_PUT_INIT;
+  t.x = init_src; t.w = nullptr;
+  t.y = bufA;
+  t.L = Lo.span;
+  t.i0 = Lo.colbase; t.i1 = init_col0 - Lo.colbase; t.i2 = init_len;
+  t.d0 = P.ds;
+  t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0; t.Lout = 0;
+  issue(S, c, RING_BIG, t, 0, 0, U(bufA), U(pay + Lo.span));
+  return X;
+}
+
+// fast_put_bsm's stage loop (bsm.py:626-676) for option o on chain warp c.
 __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
-                                 double* scratch, const BatchOut& out, double* chain_flops) {
+                                 double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
   const long long t_opt = clock64();
   const int64_t n = P.n, ks = P.ks;
   const PutLayout Lo = put_layout(n, ks);
-  double* bufA = arena;
-  double* bufB = arena + Lo.span;
-  double* pay = arena + 2 * Lo.span;
-  double* frames = arena + 3 * Lo.span;
-  double* kc = frames + 2 * n + 64 * PUT_MAX_DEPTH;
-  const Stencil st{P.cd, P.cm, P.cu, 2};
-  build_kernel_table(kc, st, scratch);
-  PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, 0.0, out.prof};
-  double* cur_org = bufA - Lo.colbase;
-  double* nxt_org = bufB - Lo.colbase;
-  // payoff table 1 - e^{col ds} (bsm.py:238-244) and the initial row (zeros on 1..ks+n)
-  {
-    Task t;
-    t.kind = TK_PUT_INIT;
-    t.x = nullptr; t.w = nullptr;
-    t.y = bufA;
-    t.L = Lo.span;
-    t.i0 = Lo.colbase; t.i1 = t.i2 = 0;
-    t.d0 = P.ds;
-    t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0; t.Lout = 0;
-    issue(S, c, RING_BIG, t, 0, 0, U(bufA), U(pay + Lo.span));
-  }
+  PutChainCtx X = put_chain_setup(S, c, P, Lo, n, arena, scratch, out.prof, nullptr, 0, 0);
+  double* cur_org = arena - Lo.colbase;
+  double* nxt_org = arena + Lo.span - Lo.colbase;
   int32_t err = 0, cnt = 0;
   int64_t m = 0, f = 0;
   double price = 0.0;
@@ -259,6 +326,8 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       const int id = issue(S, c, ring, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
       warp_wait_done(S, id);
       price = P.K * S.result[c];
+      const int64_t lo = (f < ks - rem ? f : ks - rem) - 1;
+      X.ref_flops += ref_strip_flops(ks + rem - lo + 1, rem);
       X.flops += 5.0 * ((double)rem * rem + rem);
       break;
     }
@@ -266,15 +335,13 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     if (hh < 1) {
       wait_conflicts(S, c, U(cur_org + f + 1), U(cur_org + f + 2), U(X.pay_org + f - 3), U(X.pay_org + f + 2),
                      U(nxt_org + f - 3), U(nxt_org + f + 2));
+      X.ref_flops += ref_strip_flops(red + 4, 1);
       const int64_t kb = put_leaf(X, P, cur_org, nxt_org, f - 3, f + 1, f, 1);
       if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
       f = kb;
       m += 1;
     } else {
-      const int h = (int)hh;
-      if (red > 2 * hh)  // far: cols f+h+1 .. ks+rem-h stay linear
-        put_conv(X, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h);
-      const int64_t kp = put_solve_q(X, P, f, cur_org, nxt_org, h, &err);
+      const int64_t kp = put_stage(X, P, f, red, hh, cur_org, nxt_org, &err);
       if (err) break;
       f = kp;
       m += hh;
@@ -292,6 +359,7 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
   *chain_flops += X.flops;
+  *ref_flops += X.ref_flops;
 }
 
 // Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
@@ -302,7 +370,8 @@ __device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, in
     double* A = t.y;
     double* pay = t.y + 2 * t.L;
     for (int64_t i = g.t; i < t.L; i += g.n) {
-      A[i] = 0.0;
+      const int64_t k = i - t.i1;  // position in the initial segment
+      A[i] = (t.x != nullptr && k >= 0 && k < t.i2) ? t.x[k] : 0.0;
       pay[i] = 1.0 - exp((double)(t.i0 + i) * t.d0);
     }
     return 0.0;
@@ -339,116 +408,74 @@ __device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, in
   return exec_generic(t, sbuf, slots, logN, tq, g);
 }
 
+struct PutPricer {
+  const PutParams* opts;
+  const int32_t* order;
+  BatchOut out;
+  __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* flops) const {
+    double ref = 0.0;
+    const int o = order[w];
+    put_chain_option(S, c, opts[o], o, arena, scratch, out, flops, &ref);
+    if (lane_id() == 0 && out.flops) atomicAdd(out.flops + 1, (unsigned long long)ref);
+  }
+  __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
+                         const Grp& g) const {
+    return put_exec_task(S, t, sbuf, slots, logN, tq, g);
+  }
+};
+
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
-  extern __shared__ double2 sdyn_raw[];
-  // dynamic shared memory: scheduler state | chain scratch | twiddles | FFT buffers
-  SchedShared& S = *reinterpret_cast<SchedShared*>(sdyn_raw);
-  double* chain_scratch = reinterpret_cast<double*>(sdyn_raw) + SCHED_SHARED_DOUBLES;
-  double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SCRATCH);  // quarter-wave twiddles
-  double2* bigbuf = tq + TWQ;                // big-group FFT buffer
-  double2* smallbuf = bigbuf + BIG_SLOTS;    // SMALL_WORKERS x SMALL_SLOTS
-  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
-  sched_init(S);
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  unsigned long long* prof = out.prof;
-  if (warp >= CHAIN_WARP0) {
-    // ---- chain warps (highest warp ids: the issue arbiter favours them)
-    const int c = warp - CHAIN_WARP0;
-    double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
-    double chain_flops = 0.0;
-    for (;;) {
-      int w = 0;
-      if (lane_id() == 0) w = atomicAdd(counter, 1);
-      w = __shfl_sync(FULL, w, 0);
-      if (w >= nwork) break;
-      const int o = order[w];
-      put_chain_option(S, c, opts[o], o, arena, chain_scratch + c * CHAIN_SCRATCH, out, &chain_flops);
-    }
-    if (lane_id() == 0 && out.flops) atomicAdd(out.flops, (unsigned long long)chain_flops);
-    int last = 0;
-    if (lane_id() == 0) last = (atomicSub(&S.chains_left, 1) == 1);
-    last = __shfl_sync(FULL, last, 0);
-    if (last) {
-      // last chain out: one EXIT per small worker and one for the big group
-      Task t;
-      t.kind = TK_EXIT;
-      t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
-      t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
-      t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
-      for (int k = 0; k < SMALL_WORKERS; ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
-      issue(S, c, RING_BIG, t, 0, 0, 0, 0);
-    }
-    return;
-  }
-  double flops = 0.0;
-  const long long t_start = clock64();
-  if (warp < BIG_WARPS) {
-    // ---- big group: one task at a time over BIG_THREADS threads
-    const Grp g{(int)threadIdx.x, BIG_THREADS, BIG_BAR};
-    __shared__ int s_idx;
-    for (;;) {
-      const long long t0 = clock64();
-      if (warp == 0) {
-        int idx = 0;
-        if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_BIG], 1);
-        idx = __shfl_sync(FULL, idx, 0);
-        worker_wait_ready(S, RING_BIG, idx);
-        if (lane_id() == 0) s_idx = idx;
-      }
-      gsync(g);
-      const int idx = s_idx;
-      const Task t = load_task(S.ring[RING_BIG][idx % QCAP]);
-      const long long t1 = clock64();
-      if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-      if (t.kind == TK_EXIT) break;
-      const double fl = put_exec_task(S, t, bigbuf, BIG_SLOTS, BIG_LOGN, tq, g);
-      flops += fl > 0 ? fl : 0.0;
-      gsync(g);
-      if (g.t == 0) {
-        publish_done(S, RING_BIG, idx);
-        prof_add(prof, PROF_BIG_CYC, clock64() - t1);
-        prof_add(prof, PROF_BIG_N, 1);
-      }
-    }
-  } else {
-    // ---- small workers: one warp per task
-    const int sw = warp - BIG_WARPS;
-    const Grp g{lane_id(), 32, -1};
-    double2* buf = smallbuf + sw * SMALL_SLOTS;
-    for (;;) {
-      const long long t0 = clock64();
-      int idx = 0;
-      if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_SMALL], 1);
-      idx = __shfl_sync(FULL, idx, 0);
-      worker_wait_ready(S, RING_SMALL, idx);
-      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
-      const long long t1 = clock64();
-      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-      if (t.kind == TK_EXIT) break;
-      const double fl = put_exec_task(S, t, buf, SMALL_SLOTS, SMALL_LOGN, tq, g);
-      flops += fl > 0 ? fl : 0.0;
-      __syncwarp();
-      if (lane_id() == 0) {
-        publish_done(S, RING_SMALL, idx);
-        if (prof) {
-          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
-          prof_add(prof, ps, clock64() - t1);
-          prof_add(prof, ps + 1, 1);
-        }
-      }
-    }
-  }
-  if ((threadIdx.x & 31) == 0 && (warp >= BIG_WARPS || warp == 0)) {
-    if (out.flops) atomicAdd(out.flops, (unsigned long long)flops);
-    prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
-  }
+  const PutPricer pr{opts, order, out};
+  sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
 
 // ---------------------------------------------------------------------------
-// O(T^2) projected march over the shrinking window (baseline_put_fd).
+// solve_bsm_trapezoid (bsm.py:504-554): one stage of height h from a given
+// row state (boundary f, continuation values on cols f+1 .. f+W).  Output:
+// meta[0] = new boundary kp, meta[1] = status, values of cols kp+1 .. f+W-h
+// into out[0 .. f+W-h-kp).
+
+struct PutTrapPricer {
+  PutParams P;  // cd, cm, cu, ds, cutoff used
+  int64_t f, W, h;
+  const double* seg;
+  double* out;
+  int64_t* meta;
+  unsigned long long* flops;
+  __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* fl) const {
+    const PutLayout Lo = put_trap_layout(f, W, h);
+    PutChainCtx X = put_chain_setup(S, c, P, Lo, 2 * h, arena, scratch, nullptr, seg, f + 1, W);
+    double* cur_org = arena - Lo.colbase;
+    double* nxt_org = arena + Lo.span - Lo.colbase;
+    int32_t err = 0;
+    const int64_t kp = put_stage(X, P, f, W, h, cur_org, nxt_org, &err);
+    wait_all_own(S, c);
+    const int64_t len = err ? 0 : (f + W - h) - kp;
+    for (int64_t i = lane_id(); i < len; i += 32) out[i] = nxt_org[kp + 1 + i];
+    if (lane_id() == 0) {
+      meta[0] = err ? 0 : kp;
+      meta[1] = err;
+      if (flops) atomicAdd(flops + 1, (unsigned long long)X.ref_flops);
+    }
+    *fl += X.flops;
+  }
+  __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
+                         const Grp& g) const {
+    return put_exec_task(S, t, sbuf, slots, logN, tq, g);
+  }
+};
+
+__global__ void __launch_bounds__(SCHED_THREADS, 1)
+put_trap_kernel(PutTrapPricer pr, int32_t* counter, double* __restrict__ ws, int64_t ws_stride) {
+  sched_body(pr, 1, counter, ws, ws_stride, pr.flops, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// O(T^2) projected march over the shrinking window (baseline_put_fd).  Same
+// unfused operation order as _accel.put_march_window (_accel.py:163-200), so
+// prices and boundaries are bit-identical to the reference.
 
 __global__ void __launch_bounds__(CTA_THREADS)
 put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
@@ -479,7 +506,9 @@ put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restric
   for (int64_t s = 1; s <= n; ++s) {
     int lg = -1;
     for (int64_t k = s + threadIdx.x; k <= W - 1 - s; k += CTA_THREADS) {
-      const double lin = fma(P.cd, a[k - 1], fma(P.cu, a[k + 1], P.cm * a[k]));
+      // cm*cur + cu*right + cd*left, left to right, no contraction
+      const double lin = __dadd_rn(__dadd_rn(__dmul_rn(P.cm, a[k]), __dmul_rn(P.cu, a[k + 1])),
+                                   __dmul_rn(P.cd, a[k - 1]));
       const double p = pay[k];
       const bool red = lin > p;
       b[k] = red ? lin : p;
@@ -510,25 +539,45 @@ put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restric
 // ---------------------------------------------------------------------------
 // launchers
 
-int put_fast_smem_bytes() {
-  return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SCRATCH) * (int)sizeof(double) +
-         (TWQ + BIG_SLOTS + SMALL_WORKERS * SMALL_SLOTS) * (int)sizeof(double2);
-}
+int put_fast_smem_bytes() { return sched_smem_bytes(); }
 int put_chains_per_cta() { return NCHAIN; }
+
+static cudaError_t put_configure() {
+  static bool configured = false;
+  if (configured) return cudaSuccess;
+  const int smem = sched_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(put_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(put_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
 
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream) {
-  static bool configured = false;
-  const int smem = put_fast_smem_bytes();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(put_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  if (nwork <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  cudaError_t e = put_configure();
   if (e != cudaSuccess) return e;
-  put_fast_kernel<<<grid, SCHED_THREADS, smem, stream>>>(opts, order, nwork, counter, ws, ws_stride, out);
+  if (nwork <= 0) return cudaSuccess;
+  e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  if (e != cudaSuccess) return e;
+  put_fast_kernel<<<grid, SCHED_THREADS, sched_smem_bytes(), stream>>>(opts, order, nwork, counter, ws, ws_stride,
+                                                                         out);
+  return cudaGetLastError();
+}
+
+int64_t put_trap_ws_doubles(int64_t f, int64_t W, int64_t h) {
+  return put_arena_doubles(put_trap_layout(f, W, h).span, 2 * h);
+}
+
+cudaError_t launch_put_trapezoid(const PutParams& P, int64_t f, int64_t W, int64_t h, const double* seg,
+                                 double* out, int64_t* meta, int32_t* counter, double* ws, int64_t ws_stride,
+                                 unsigned long long* flops, cudaStream_t stream) {
+  cudaError_t e = put_configure();
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
+  if (e != cudaSuccess) return e;
+  const PutTrapPricer pr{P, f, W, h, seg, out, meta, flops};
+  put_trap_kernel<<<1, SCHED_THREADS, sched_smem_bytes(), stream>>>(pr, counter, ws, ws_stride);
   return cudaGetLastError();
 }
 

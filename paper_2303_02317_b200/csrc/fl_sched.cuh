@@ -94,7 +94,9 @@ struct SchedShared {
   int claim[NRINGS];
   Pend pend[NCHAIN][PEND_CAP];
   int npend[NCHAIN];
-  double result[NCHAIN];
+  double result[NCHAIN];   // per-chain results of blocking tasks
+  double result2[NCHAIN];
+  int64_t iresult[NCHAIN];
   int chains_left;
 };
 
@@ -414,6 +416,131 @@ __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logN
     fl += warp_conv_direct(sx, t.y + k0, nk, sw, M);
   }
   return fl;
+}
+
+// ---------------------------------------------------------------------------
+// The persistent kernel body shared by the pricers.
+//
+// Pricer interface:
+//   __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* flops) const;
+//       price work item w on chain warp c (all 32 lanes call; scratch: CHAIN_SCRATCH
+//       doubles of shared memory owned by the warp, arena: the chain's HBM workspace)
+//   __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN,
+//                          const double2* tq, const Grp& g) const;
+//       execute one task (pricer-specific kinds, else exec_generic)
+
+constexpr int CHAIN_SCRATCH = 384;  // doubles of shared memory per chain warp
+
+__host__ __device__ constexpr int sched_smem_bytes() {
+  return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SCRATCH) * (int)sizeof(double) +
+         (TWQ + BIG_SLOTS + SMALL_WORKERS * SMALL_SLOTS) * (int)sizeof(double2);
+}
+
+template <class Pricer>
+__device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t* counter, double* ws,
+                                           int64_t ws_stride, unsigned long long* flops_out,
+                                           unsigned long long* prof) {
+  extern __shared__ double2 sdyn_raw[];
+  // dynamic shared memory: scheduler state | chain scratch | twiddles | FFT buffers
+  SchedShared& S = *reinterpret_cast<SchedShared*>(sdyn_raw);
+  double* chain_scratch = reinterpret_cast<double*>(sdyn_raw) + SCHED_SHARED_DOUBLES;
+  double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SCRATCH);  // quarter-wave twiddles
+  double2* bigbuf = tq + TWQ;              // big-group FFT buffer
+  double2* smallbuf = bigbuf + BIG_SLOTS;  // SMALL_WORKERS x SMALL_SLOTS
+  __shared__ int s_idx;
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
+  sched_init(S);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  if (warp >= CHAIN_WARP0) {
+    // ---- chain warps (highest warp ids)
+    const int c = warp - CHAIN_WARP0;
+    double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
+    double chain_flops = 0.0;
+    for (;;) {
+      int w = 0;
+      if (lane_id() == 0) w = atomicAdd(counter, 1);
+      w = __shfl_sync(FULL, w, 0);
+      if (w >= nwork) break;
+      pr.chain(S, c, w, arena, chain_scratch + c * CHAIN_SCRATCH, &chain_flops);
+    }
+    if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)chain_flops);
+    int last = 0;
+    if (lane_id() == 0) last = (atomicSub(&S.chains_left, 1) == 1);
+    last = __shfl_sync(FULL, last, 0);
+    if (last) {
+      // last chain out: one EXIT per small worker and one for the big group
+      Task t;
+      t.kind = TK_EXIT;
+      t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
+      t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
+      t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
+      for (int k = 0; k < SMALL_WORKERS; ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
+      issue(S, c, RING_BIG, t, 0, 0, 0, 0);
+    }
+    return;
+  }
+  double flops = 0.0;
+  const long long t_start = clock64();
+  if (warp < BIG_WARPS) {
+    // ---- big group: one task at a time over BIG_THREADS threads
+    const Grp g{(int)threadIdx.x, BIG_THREADS, BIG_BAR};
+    for (;;) {
+      const long long t0 = clock64();
+      if (warp == 0) {
+        int idx = 0;
+        if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_BIG], 1);
+        idx = __shfl_sync(FULL, idx, 0);
+        worker_wait_ready(S, RING_BIG, idx);
+        if (lane_id() == 0) s_idx = idx;
+      }
+      gsync(g);
+      const int idx = s_idx;
+      const Task t = load_task(S.ring[RING_BIG][idx % QCAP]);
+      const long long t1 = clock64();
+      if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+      if (t.kind == TK_EXIT) break;
+      const double fl = pr.exec(S, t, bigbuf, BIG_SLOTS, BIG_LOGN, tq, g);
+      flops += fl > 0 ? fl : 0.0;
+      gsync(g);
+      if (g.t == 0) {
+        publish_done(S, RING_BIG, idx);
+        prof_add(prof, PROF_BIG_CYC, clock64() - t1);
+        prof_add(prof, PROF_BIG_N, 1);
+      }
+    }
+  } else {
+    // ---- small workers: one warp per task
+    const int sw = warp - BIG_WARPS;
+    const Grp g{lane_id(), 32, -1};
+    double2* buf = smallbuf + sw * SMALL_SLOTS;
+    for (;;) {
+      const long long t0 = clock64();
+      int idx = 0;
+      if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_SMALL], 1);
+      idx = __shfl_sync(FULL, idx, 0);
+      worker_wait_ready(S, RING_SMALL, idx);
+      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
+      const long long t1 = clock64();
+      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+      if (t.kind == TK_EXIT) break;
+      const double fl = pr.exec(S, t, buf, SMALL_SLOTS, SMALL_LOGN, tq, g);
+      flops += fl > 0 ? fl : 0.0;
+      __syncwarp();
+      if (lane_id() == 0) {
+        publish_done(S, RING_SMALL, idx);
+        if (prof) {
+          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
+          prof_add(prof, ps, clock64() - t1);
+          prof_add(prof, ps + 1, 1);
+        }
+      }
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && (warp >= BIG_WARPS || warp == 0)) {
+    if (flops_out) atomicAdd(flops_out, (unsigned long long)flops);
+    prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
+  }
 }
 
 }  // namespace fl

@@ -1,0 +1,100 @@
+"""Composed-stencil operators -- drop-in for the hot-path part of ``fftlattice.fft``.
+
+``Kernel`` (fft.py:41-74), ``kernel_power`` (fft.py:203-260) and
+``apply_linear_steps`` (fft.py:263-329) with the reference signatures; the
+composition and the valid-mode correlation run on the device
+(``fl_apply_linear_steps``: truncated overlap-save FFT with the analytic
+stencil spectrum, csrc/fl_conv.cuh).  Supported kernels are the pricers' own:
+two or three nonnegative taps (lattice / FD weights); anything else raises
+``UnsupportedCombinationError`` instead of falling back to the CPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .model import (
+    GridRow,
+    InsufficientWidthError,
+    NumericalIntegrityError,
+    UnsupportedCombinationError,
+    ValidationError,
+)
+
+__all__ = ["Kernel", "kernel_power", "apply_linear_steps"]
+
+
+@dataclass(frozen=True, slots=True)
+class Kernel:
+    """One-step stencil: out[j] = sum_r weights[r] in[j + min_offset + r] (fft.py:41-74)."""
+
+    weights: np.ndarray
+    min_offset: int
+
+    def __post_init__(self) -> None:
+        arr = np.ascontiguousarray(self.weights, dtype=np.float64)
+        object.__setattr__(self, "weights", arr)
+        if arr.ndim != 1 or arr.shape[0] < 1:
+            raise ValidationError("weights", "kernel weights must be a nonempty 1-D array")
+
+    def __len__(self) -> int:
+        return int(self.weights.shape[0])
+
+    @property
+    def max_offset(self) -> int:
+        return self.min_offset + len(self) - 1
+
+
+def _device_taps(kernel: Kernel) -> tuple[int, float, float, float]:
+    w = kernel.weights
+    if len(w) not in (2, 3) or not np.all(np.isfinite(w)) or np.any(w < 0.0):
+        raise UnsupportedCombinationError(
+            "the GPU composes two- or three-tap kernels with nonnegative finite weights only")
+    c2 = float(w[2]) if len(w) == 3 else 0.0
+    return len(w), float(w[0]), float(w[1]), c2
+
+
+def kernel_power(kernel: Kernel, h: int) -> Kernel:
+    """h-fold composition of ``kernel`` (fft.py:203-260), computed on the device
+    as the composed correlation of a unit impulse."""
+    if h < 0:
+        raise ValidationError("h", "step count h must be >= 0")
+    if h == 0:
+        return Kernel(np.array([1.0]), 0)
+    if h == 1:
+        return Kernel(kernel.weights.copy(), kernel.min_offset)
+    taps, c0, c1, c2 = _device_taps(kernel)
+    m = h * (taps - 1) + 1
+    x = np.zeros(2 * m - 1)
+    x[m - 1] = 1.0
+    y = _native.apply_linear_steps(x, taps, c0, c1, c2, h)  # y[k] = W[m-1-k]
+    w = np.ascontiguousarray(y[::-1])
+    if not np.all(np.isfinite(w)):
+        raise NumericalIntegrityError(f"composed kernel overflowed for h={h}")
+    return Kernel(w, h * kernel.min_offset)
+
+
+def apply_linear_steps(row: GridRow, kernel: Kernel, h: int, *, direction: int = 1,
+                       composed: Kernel | None = None) -> GridRow:
+    """Advance ``row`` by h linear steps in one device correlation (fft.py:263-329).
+
+    ``composed`` (the reference's cache hook) is length-checked; the device
+    derives the composed weights itself."""
+    if h < 0:
+        raise ValidationError("h", "step count h must be >= 0")
+    if h == 0:
+        return GridRow(row.time_index, row.col_offset, row.values.copy())
+    expected_len = h * (len(kernel) - 1) + 1
+    if composed is not None and len(composed) != expected_len:
+        raise ValidationError("composed", "composed kernel length does not match h steps")
+    out_len = len(row) - expected_len + 1
+    if out_len < 1:
+        raise InsufficientWidthError(
+            f"run of {len(row)} columns is too narrow for {h} steps of a "
+            f"{len(kernel)}-point kernel (needs >= {expected_len})")
+    taps, c0, c1, c2 = _device_taps(kernel)
+    vals = _native.apply_linear_steps(row.values, taps, c0, c1, c2, h)
+    return GridRow(row.time_index + direction * h, row.col_offset - h * kernel.min_offset, vals)

@@ -160,6 +160,88 @@ def stratified_c5(per=2):
     return b.subset(np.asarray(idx))
 
 
+def ops_cases():
+    """Golden vectors for the exported sub-operators the reference tests drive
+    directly: kernel_power, apply_linear_steps, solve_bsm_trapezoid,
+    solve_trapezoid.  Saved as ops.npz with per-case keys."""
+    from fftlattice import american as ref_american
+
+    out = {}
+    O = fl.OptionSpec
+    rng = np.random.default_rng([99, 20261019])
+    # kernel_power / apply_linear_steps on the pricers' own stencils
+    put_disc = fl.discretize_bsm(O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 4096), 0.4)
+    bp = fl.derive_binomial_params(O(100.0, 95.0, 0.03, 0.05, 0.25, 180, 4096))
+    kernels = [("put", np.array([put_disc.coef_down, put_disc.coef_mid, put_disc.coef_up]), -1),
+               ("call", np.array([bp.weight_down, bp.weight_up]), 0)]
+    k = 0
+    for name, w, off in kernels:
+        for h in (2, 7, 33, 64, 65, 300, 1000, 5000):
+            kern = fl.Kernel(w, off)
+            out[f"kp{k}_w"] = w
+            out[f"kp{k}_off"] = np.asarray(off)
+            out[f"kp{k}_h"] = np.asarray(h)
+            out[f"kp{k}_out"] = fl.kernel_power(kern, h).weights
+            L = int(rng.integers(len(w) + h * (len(w) - 1), 3 * h * len(w) + 50))
+            row = fl.GridRow(5000, 3, rng.uniform(0.0, 1.0, L))
+            r = fl.apply_linear_steps(row, kern, h)
+            out[f"kp{k}_row"] = row.values
+            out[f"kp{k}_als"] = r.values
+            out[f"kp{k}_als_off"] = np.asarray(r.col_offset)
+            k += 1
+    out["n_kp"] = np.asarray(k)
+    # solve_bsm_trapezoid: two consecutive stages from the payoff row
+    k = 0
+    for spec, h0 in [(O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 4096), 700),
+                     (O(90.0, 110.0, 0.06, 0.0, 0.35, 500, 16384), 3000),
+                     (O(140.0, 100.0, 0.03, 0.0, 0.5, 60, 2048), 100),
+                     (O(100.0, 100.0, 0.04, 0.0, 0.25, 180, 1024), 37)]:
+        disc = fl.discretize_bsm(spec, 0.4)
+        st = fl.initial_row(disc)
+        for h in (h0, max(1, h0 // 3)):
+            if len(st.segment) < 2 * h:
+                break
+            nxt = fl.solve_bsm_trapezoid(disc, st, h)
+            out[f"pt{k}_coef"] = np.array([disc.coef_down, disc.coef_mid, disc.coef_up, disc.d_s])
+            out[f"pt{k}_f"] = np.asarray(st.boundary)
+            out[f"pt{k}_t"] = np.asarray(st.time_index)
+            out[f"pt{k}_seg"] = st.segment.values
+            out[f"pt{k}_h"] = np.asarray(h)
+            out[f"pt{k}_kp"] = np.asarray(nxt.boundary)
+            out[f"pt{k}_out"] = nxt.segment.values
+            st = nxt
+            k += 1
+    out["n_pt"] = np.asarray(k)
+    # solve_trapezoid: the first trapezoid after the junction row, and the next one
+    k = 0
+    for spec in [O(100.0, 95.0, 0.03, 0.05, 0.25, 180, 4096), O(120.0, 100.0, 0.04, 0.02, 0.35, 300, 16384),
+                 O(80.0, 110.0, 0.02, 0.04, 0.45, 90, 2048)]:
+        p = fl.derive_binomial_params(spec)
+        top = fl.top_row_state(spec, p)
+        junc = ref_american._junction_row(spec, p, top)
+        i, j, vals = junc.time_index, junc.boundary, junc.segment.values
+        resid = math.isqrt(spec.steps - 1) + 1
+        for _ in range(2):
+            if not (i > resid and j >= 0):
+                break
+            h = min(j + 1, i - resid)
+            prob = fl.TrapezoidProblem(i, j, h, fl.GridRow(i, 0, vals))
+            st = fl.solve_trapezoid(spec, prob, p)
+            out[f"ct{k}_spec"] = np.array([spec.spot, spec.strike, spec.rate, spec.dividend_yield,
+                                           spec.volatility, spec.days_to_expiry, spec.steps], dtype=np.float64)
+            out[f"ct{k}_i"] = np.asarray(i)
+            out[f"ct{k}_j"] = np.asarray(j)
+            out[f"ct{k}_h"] = np.asarray(h)
+            out[f"ct{k}_run"] = vals
+            out[f"ct{k}_jp"] = np.asarray(st.boundary)
+            out[f"ct{k}_out"] = st.segment.values
+            i, j, vals = st.time_index, st.boundary, st.segment.values
+            k += 1
+    out["n_ct"] = np.asarray(k)
+    np.savez_compressed(os.path.join(HERE, "ops.npz"), **out)
+    print(f"ops: {int(out['n_kp'])} kernel cases, {int(out['n_pt'])} put stages, {int(out['n_ct'])} trapezoids")
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     want = lambda k: not which or k in which  # noqa: E731
@@ -183,3 +265,5 @@ if __name__ == "__main__":
         save("c4_fast", b.subset(np.r_[0:4, 64:68]), "fast")
     if want("c5"):
         save("c5_fast", stratified_c5(), "fast")
+    if want("ops"):
+        ops_cases()

@@ -1,0 +1,153 @@
+"""GPU parity of the drop-in Python API (the reference's own entry points and
+exported sub-operators) against golden vectors produced by the reference.
+
+Prices: |d| <= 1e-9 max(|ref|, K); rescaled put rows (values in [0, 1]) and
+call rows: |d| <= 1e-9 max(1, K); composed kernels: |d| <= 1e-12 max|W|
+(the reference's own FFT round-off is ~1e-16 max|W|); boundaries equal except
+a +-1 shift at a near-tie."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, price_close
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    return np.load(os.path.join(GOLDEN, "ops.npz"))
+
+
+def test_kernel_power_and_apply_linear_steps(ops):
+    import paper_2303_02317_b200 as fl
+
+    for k in range(int(ops["n_kp"])):
+        w, off, h = ops[f"kp{k}_w"], int(ops[f"kp{k}_off"]), int(ops[f"kp{k}_h"])
+        kern = fl.Kernel(w, off)
+        got = fl.kernel_power(kern, h)
+        ref = ops[f"kp{k}_out"]
+        assert got.min_offset == h * off
+        assert got.weights.shape == ref.shape
+        assert np.max(np.abs(got.weights - ref)) <= 1e-12 * np.max(np.abs(ref)), (k, h)
+        row = fl.GridRow(5000, 3, ops[f"kp{k}_row"])
+        r = fl.apply_linear_steps(row, kern, h)
+        ref_r = ops[f"kp{k}_als"]
+        assert r.col_offset == int(ops[f"kp{k}_als_off"]) and r.time_index == 5000 + h
+        assert np.max(np.abs(r.values - ref_r)) <= 1e-12 * max(1.0, np.max(np.abs(ref_r))), (k, h)
+
+
+def test_apply_linear_steps_errors():
+    import paper_2303_02317_b200 as fl
+
+    k = fl.Kernel(np.array([0.5, 0.5]), 0)
+    with pytest.raises(fl.InsufficientWidthError):
+        fl.apply_linear_steps(fl.GridRow(0, 0, np.ones(3)), k, 5)
+    with pytest.raises(fl.ValidationError):
+        fl.apply_linear_steps(fl.GridRow(0, 0, np.ones(3)), k, -1)
+    with pytest.raises(fl.UnsupportedCombinationError):
+        fl.kernel_power(fl.Kernel(np.array([0.5, -0.1, 0.6]), -1), 4)
+    out = fl.apply_linear_steps(fl.GridRow(5, 0, np.array([1.0, 2.0, 4.0])), k, 1, direction=-1)
+    assert out.time_index == 4 and out.col_offset == 0
+    assert np.allclose(out.values, [1.5, 3.0], rtol=0, atol=1e-15)
+
+
+def _close_rows(got, ref, scale):
+    return got.shape == ref.shape and (got.size == 0 or np.max(np.abs(got - ref)) <= 1e-9 * scale)
+
+
+def test_solve_bsm_trapezoid(ops):
+    import paper_2303_02317_b200 as fl
+    from paper_2303_02317_b200 import _native
+
+    for k in range(int(ops["n_pt"])):
+        cd, cm, cu, ds = ops[f"pt{k}_coef"]
+        f, h = int(ops[f"pt{k}_f"]), int(ops[f"pt{k}_h"])
+        kp, seg = _native.put_trapezoid(cd, cm, cu, ds, 128, f, ops[f"pt{k}_seg"], h)
+        kp_ref, ref = int(ops[f"pt{k}_kp"]), ops[f"pt{k}_out"]
+        assert abs(kp - kp_ref) <= 1, (k, kp, kp_ref)
+        if kp == kp_ref:
+            assert _close_rows(seg, ref, 1.0), (k, np.max(np.abs(seg - ref)))
+        # through the drop-in signature
+        disc = fl.BsmDiscretization(0, 0.0, 0.0, 0.0, ds, 0, 0.4, cd, cm, cu)
+        st = fl.PutRowState(int(ops[f"pt{k}_t"]), f, fl.GridRow(int(ops[f"pt{k}_t"]), f + 1, ops[f"pt{k}_seg"]))
+        nxt = fl.solve_bsm_trapezoid(disc, st, h)
+        assert nxt.time_index == st.time_index + h and nxt.boundary == kp
+        assert nxt.segment.first_col == kp + 1
+
+
+def test_solve_bsm_trapezoid_errors():
+    import paper_2303_02317_b200 as fl
+
+    disc = fl.discretize_bsm(fl.OptionSpec(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024))
+    st = fl.initial_row(disc)
+    with pytest.raises(fl.GeometryError):
+        fl.solve_bsm_trapezoid(disc, st, 0)
+    with pytest.raises(fl.GeometryError):
+        fl.solve_bsm_trapezoid(disc, st, len(st.segment))
+    with pytest.raises(fl.ValidationError):
+        fl.solve_bsm_trapezoid(disc, st, 8, base_cutoff=0)
+
+
+def test_solve_trapezoid(ops):
+    import paper_2303_02317_b200 as fl
+
+    for k in range(int(ops["n_ct"])):
+        S, K, R, Y, V, E, T = ops[f"ct{k}_spec"]
+        spec = fl.OptionSpec(S, K, R, Y, V, E, int(T))
+        i, j, h = int(ops[f"ct{k}_i"]), int(ops[f"ct{k}_j"]), int(ops[f"ct{k}_h"])
+        prob = fl.TrapezoidProblem(i, j, h, fl.GridRow(i, 0, ops[f"ct{k}_run"]))
+        st = fl.solve_trapezoid(spec, prob)
+        jp_ref, ref = int(ops[f"ct{k}_jp"]), ops[f"ct{k}_out"]
+        assert st.time_index == i - h
+        assert abs(st.boundary - jp_ref) <= 1, (k, st.boundary, jp_ref)
+        if st.boundary == jp_ref:
+            assert _close_rows(st.segment.values, ref, max(1.0, K)), (k, np.max(np.abs(st.segment.values - ref)))
+
+
+def test_single_spec_pricers_match_golden():
+    """fast_* / baseline_* through the reference signatures on the edge set."""
+    import paper_2303_02317_b200 as fl
+
+    for name, method in (("edge_fast", "fast"), ("edge_baseline", "baseline")):
+        g = golden(name)
+        for i in range(g.n):
+            spec = fl.OptionSpec(*g.args(i))
+            kind = int(g.kind[i])
+            ek = str(g.err_kind[i])
+            try:
+                if kind == 0:
+                    p = fl.fast_european(spec) if method == "fast" else fl.baseline_european(spec)
+                    series = None
+                elif kind == 1:
+                    r = fl.fast_american_call(spec) if method == "fast" else fl.baseline_american_call(spec)
+                    p, series = r.price, r.boundaries
+                else:
+                    r = fl.fast_put_bsm(spec) if method == "fast" else fl.baseline_put_fd(spec)
+                    p, series = r.price, r.boundaries
+            except (fl.PricingError, ValueError) as e:
+                assert type(e).__name__ == ek, (name, i, type(e).__name__, ek)
+                fld = getattr(e, "field", getattr(e, "weight", ""))
+                assert (fld or "") == str(g.err_field[i]), (name, i, fld, g.err_field[i])
+                continue
+            assert ek == "", (name, i, ek)
+            assert price_close(p, g.price[i], g.K[i]), (name, i, p, g.price[i])
+            if series is not None:
+                t, c = g.boundary(i)
+                assert np.array_equal(series.times, t), (name, i)
+                assert np.array_equal(series.columns, c), (name, i)
+
+
+def test_batch_helpers():
+    import paper_2303_02317_b200 as fl
+
+    g = golden("c3_fast")
+    sl = slice(0, 32)
+    price, status = fl.price_put_batch(g.S[sl], g.K[sl], g.R[sl], g.V[sl], g.E[sl], g.T[sl])
+    assert np.all(status == 0)
+    for i in range(32):
+        assert price_close(price[i], g.price[i], g.K[i])
