@@ -60,6 +60,19 @@ int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double*
                    int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
                    int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
 
+/* Host-only (no CUDA call): the per-option constants and dispatch the batch
+ * entry points derive, for inspection and CPU-side parity tests.
+ *   mode[i]: -1 error, 0 device D&C, 1 O(T^2) baseline, 2 closed price,
+ *            3 European (American call the reference prices as European)
+ *   EURO: dparams = {wd, wu, gauged wu e^{2 lu}, lu}     (binomial.py:161-194)
+ *   CALL: dparams = {wd, wu, lu, closed price}, iparams = {terminal boundary,
+ *         row T-1 boundary}                             (american.py:260-470)
+ *   PUT:  dparams = {cd, cm, cu, ds}, iparams = {k*}    (bsm.py:150-229, 585-625)
+ * dparams: n x 4 doubles, iparams: n x 2 int64. */
+int fl_inspect(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R, const double* Y,
+               const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
+               int64_t put_cutoff, int32_t* status, int32_t* mode, double* dparams, int64_t* iparams);
+
 /* Device-resident batches (for repeated pricing and benchmarking): prepare
  * does the host-side parameter derivation and the H2D copy once; run only
  * enqueues the kernels on `stream` (inputs and outputs stay in HBM); fetch

@@ -40,7 +40,7 @@ _lib = None
 EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
-    "fl_batch_ref_flops", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
+    "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
     "fl_probe_fp64",
 )
 
@@ -88,6 +88,8 @@ def lib():
         L.fl_batch_stats.restype = c_int
         L.fl_batch_profile.argtypes = [P, P, P]
         L.fl_batch_profile.restype = c_int
+        L.fl_inspect.argtypes = [i64, P, P, P, P, P, P, P, P, d, i64, i64, P, P, P, P]
+        L.fl_inspect.restype = c_int
         L.fl_batch_ref_flops.argtypes = [P, P, P]
         L.fl_batch_ref_flops.restype = c_int
         L.fl_put_trapezoid.argtypes = [d, d, d, d, i64, i64, P, i64, i64, P, P, P, P]
@@ -337,3 +339,16 @@ def call_trapezoid(S: float, K: float, wd: float, wu: float, lu: float, base_cut
     if err is not None:
         raise err
     return jp.value, out[:max(jp.value - first + 1, 0)].copy()
+
+
+def inspect(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128):
+    """Host-only derivation the batch entry points perform (fl_inspect):
+    (status[n], mode[n], dparams[n, 4], iparams[n, 2]).  No CUDA involved."""
+    n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
+    status = np.zeros(n, dtype=np.int32)
+    mode = np.zeros(n, dtype=np.int32)
+    dp = np.zeros((n, 4))
+    ip = np.zeros((n, 2), dtype=np.int64)
+    _check(lib().fl_inspect(n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), float(lam),
+                            int(call_cutoff), int(put_cutoff), _ptr(status), _ptr(mode), _ptr(dp), _ptr(ip)))
+    return status, mode, dp, ip

@@ -497,6 +497,40 @@ int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t*
   return 0;
 }
 
+int fl_inspect(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R, const double* Y,
+               const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
+               int64_t put_cutoff, int32_t* status, int32_t* mode, double* dparams, int64_t* iparams) {
+  if (n < 0 || !kind || !S || !K || !R || !Y || !V || !E || !T || !status || !mode || !dparams || !iparams)
+    return fail("fl_inspect: null pointer");
+  for (int64_t i = 0; i < n; ++i) {
+    const fl::SpecIn s{S[i], K[i], R[i], Y[i], V[i], E[i], T[i]};
+    double* d = dparams + 4 * i;
+    int64_t* q = iparams + 2 * i;
+    d[0] = d[1] = d[2] = d[3] = 0.0;
+    q[0] = q[1] = 0;
+    int32_t st = 0, md = fl::MODE_ERROR;
+    if (kind[i] == FL_KIND_EURO) {
+      fl::EuroParams e;
+      st = fl::prep_euro(s, e);
+      if (!st) { md = fl::MODE_FAST; d[0] = e.wd; d[1] = e.wu; d[2] = e.bg; d[3] = e.lu; }
+    } else if (kind[i] == FL_KIND_CALL) {
+      fl::CallParams c;
+      fl::EuroParams e;
+      st = fl::prep_call(s, call_cutoff, c, e);
+      if (!st) { md = c.mode; d[0] = c.wd; d[1] = c.wu; d[2] = c.lu; d[3] = c.price; q[0] = c.top_b; q[1] = c.junc_j; }
+    } else if (kind[i] == FL_KIND_PUT) {
+      fl::PutParams p;
+      st = fl::prep_put(s, lam, put_cutoff, p);
+      if (!st) { md = p.mode; d[0] = p.cd; d[1] = p.cm; d[2] = p.cu; d[3] = p.ds; q[0] = p.ks; }
+    } else {
+      st = FL_E_VALIDATION;
+    }
+    status[i] = st;
+    mode[i] = st ? fl::MODE_ERROR : md;
+  }
+  return 0;
+}
+
 int fl_batch_ref_flops(fl_batch* b, double* ref_flops, void* stream) {
   if (!b) return fail("fl_batch_ref_flops: null batch");
   unsigned long long f = 0;
