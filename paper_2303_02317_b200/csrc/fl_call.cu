@@ -26,7 +26,8 @@ constexpr int CALL_FUSE_H = 2 * CALL_LEAF;
 constexpr int CALL_MAX_DEPTH = 28;
 constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per big-group thread (width <= 1024)
 constexpr int CALL_SEG = CALL_FUSE_H + 8;
-static_assert(2 * CALL_SEG + CALL_LEAF + 2 + 8 <= CHAIN_SCRATCH, "call fused node scratch");
+static_assert(2 * CALL_SEG <= CHAIN_SCRATCH, "call fused node scratch");
+static_assert(CALL_LEAF <= KSMEM_M, "fused-node weights come from the chain's shared table");
 
 enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
 
@@ -148,28 +149,29 @@ __device__ int64_t call_fused_node(CallChainCtx& X, const CallParams& P, int64_t
   const long long t1 = clock64();
   const int h1 = (h + 1) / 2, h2 = h - h1;
   call_ref_enter(X, h, ph);
-  double* s_in = X.scratch;              // cols lo .. j (+4 pad)
-  double* s_asm = X.scratch + CALL_SEG;  // cols lo .. jm (+4 pad)
-  double* s_w = X.scratch + 2 * CALL_SEG;
-  warp_stage(s_in, in_org + lo, h, h + 4);
+  double* s_in = X.scratch;              // cols lo .. j
+  double* s_asm = X.scratch + CALL_SEG;  // cols lo .. jm
+  const double* tbl = X.scratch + CHAIN_SCRATCH;
+  warp_stage(s_in, in_org + lo, h);
   const double* in_s = s_in - lo;
   double* asm_s = s_asm - lo;
-  // mid: cols lo .. j-h1 of row i-h1
-  warp_stage(s_w, X.kc + (int64_t)h1 * h1, h1 + 1);
-  X.flops += warp_conv_direct(s_in, s_asm, h2, s_w, h1 + 1);
+  // mid (helper): cols lo .. j-h1 of row i-h1, overlapping the first leaf
+  int tk = helper_post(*X.S, X.c, s_in, s_asm, h2, tbl + h1 * h1, h1 + 1);
+  X.flops += 2.0 * h2 * (h1 + 1);
   call_ref_enter(X, h1, h);
   const int64_t jm = call_leaf(X, P, in_s, asm_s, i, j, h1);
+  helper_wait(*X.S, X.c, tk);
   if (jm < j - h1 || jm > j) { *err = FL_E_GEOMETRY | 1; return 0; }
   const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
   call_ref_bottom(X, h, A);
-  if (lane_id() < 4) asm_s[jm + 1 + lane_id()] = 0.0;
-  __syncwarp();
-  if (A > h2) {
-    warp_stage(s_w, X.kc + (int64_t)h2 * h2, h2 + 1);
-    X.flops += warp_conv_direct(s_asm, out_org + lo, A - h2, s_w, h2 + 1);
+  tk = -1;
+  if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h, overlapping the second leaf
+    tk = helper_post(*X.S, X.c, s_asm, out_org + lo, (int)(A - h2), tbl + h2 * h2, h2 + 1);
+    X.flops += 2.0 * (A - h2) * (h2 + 1);
   }
   call_ref_enter(X, h2, h);
   const int64_t jp = call_leaf(X, P, asm_s, out_org, i - h1, jm, h2);
+  if (tk >= 0) helper_wait(*X.S, X.c, tk);
   if (jp < jm - h2 || jp > jm) { *err = FL_E_GEOMETRY | 2; return 0; }
   if (X.prof && lane_id() == 0) {
     prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
@@ -259,6 +261,7 @@ __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams
   double* kc = frames + 2 * h_max + 16 * CALL_MAX_DEPTH;
   const Stencil st{P.wd, P.wu, 0.0, 1};
   build_kernel_table(kc, st, scratch);
+  load_kernel_smem(scratch + CHAIN_SCRATCH, kc);
   return CallChainCtx{&S, c, st, kc, frames, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
 }
 

@@ -42,7 +42,8 @@ constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a le
 constexpr int FUSE_H = 2 * PUT_LEAF;                   // nodes up to this height are fused on the chain
 constexpr int PUT_MAX_DEPTH = 24;
 constexpr int FUSE_SEG = 2 * FUSE_H + 8;  // fused-node row buffers (doubles, incl. zero pad)
-static_assert(2 * FUSE_SEG + 2 * PUT_LEAF + 1 + 8 <= CHAIN_SCRATCH, "fused node scratch");
+static_assert(2 * FUSE_SEG + 4 * FUSE_H + 2 <= CHAIN_SCRATCH, "fused node scratch");
+static_assert(PUT_LEAF <= KSMEM_M, "fused-node weights come from the chain's shared table");
 static_assert(2 * (2 * DIRECT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
 enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD = TK_USER + 2 };
@@ -125,23 +126,30 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
 }
 
-// Leaf strip on the chain warp.  in_org / out_org may address shared memory.
+// Leaf strip on the chain warp.  in_org / out_org / pay_org may address shared memory.
 __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
-                                            double* out_org, int64_t lo, int64_t hi, int64_t f, int height) {
+                                            double* out_org, const double* pay_org, int64_t lo, int64_t hi,
+                                            int64_t f, int height) {
   const long long t1 = clock64();
-  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, X.pay_org, lo, hi, f, height, P.cd, P.cm, P.cu);
+  long long tm[2] = {0, 0};
+  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
+                                             X.prof ? tm : nullptr);
   if (X.prof && lane_id() == 0) {
     prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
     prof_add(X.prof, PROF_STRIP_N, height);
+    prof_add(X.prof, PROF_STRIP_LOOP, tm[1]);
+    prof_add(X.prof, PROF_LEAF_LOAD, tm[0] - t1);
   }
   X.flops += ref_strip_flops(hi - lo + 1, height);
   return kb;
 }
 
-// A node with PUT_LEAF < h <= FUSE_H done whole on the chain warp (bsm.py:443-501
-// for one level): input cols f+1..f+2h of in_org, output cols kp+1..f+h of out_org.
-// The mid jump, the first leaf, the assembled row and the bottom jump stay in
-// shared memory.
+// A node with PUT_LEAF < h <= FUSE_H done whole in shared memory
+// (bsm.py:443-501 for one level): input cols f+1..f+2h of in_org, output cols
+// kp+1..f+h of out_org.  The input row and the payoff of cols f-2h-1..f+2h are
+// staged once; the chain runs the two half-height leaves while its helper
+// warp runs the mid jump (overlapping the first leaf) and the bottom jump
+// (overlapping the second), from the chain's shared copy of W_1..W_32.
 __device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f, const double* in_org,
                                   double* out_org, int h, int ph, int32_t* err) {
   const long long t0 = clock64();
@@ -151,36 +159,50 @@ __device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f,
   const long long t1 = clock64();
   const int h1 = (h + 1) / 2, h2 = h - h1;
   ref_node_enter(X, h, ph);
-  double* s_in = X.scratch;                 // cols f+1 .. f+2h  (+4 pad)
-  double* s_asm = X.scratch + FUSE_SEG;     // cols f-h1+1 .. f+2h-h1 (+4 pad)
-  double* s_w = X.scratch + 2 * FUSE_SEG;   // staged weights
-  warp_stage(s_in, in_org + f + 1, 2 * h, 2 * h + 4);
-  const double* in_s = s_in - (f + 1);      // column origins of the shared rows
+  double* s_in = X.scratch;                  // cols f+1 .. f+2h
+  double* s_asm = X.scratch + FUSE_SEG;      // cols f-h1+1 .. f+2h-h1
+  double* s_pay = X.scratch + 2 * FUSE_SEG;  // payoff of cols f-2h-1 .. f+2h
+  const double* tbl = X.scratch + CHAIN_SCRATCH;
+  const int64_t plo = f - 2 * (int64_t)h - 1;
+  for (int i = lane_id(); i < 4 * h + 2; i += 32) {  // one round trip for both rows
+    if (i < 2 * h) s_in[i] = in_org[f + 1 + i];
+    s_pay[i] = X.pay_org[plo + i];
+  }
+  __syncwarp();
+  const double* in_s = s_in - (f + 1);  // column origins of the shared rows
   double* asm_s = s_asm - (f - h1 + 1);
-  // mid: cols f+h1+1 .. f+2h-h1 of row t+h1
-  int M = 2 * h1 + 1;
-  warp_stage(s_w, X.kc + (int64_t)h1 * h1, M);
-  X.flops += warp_conv_direct(s_in, asm_s + f + h1 + 1, 2 * (int64_t)(h - h1), s_w, M);
-  // first half-height leaf
+  const double* pay_s = s_pay - plo;
+  const long long t2 = clock64();
+  // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first leaf
+  const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
+  int tk = helper_post(*X.S, X.c, s_in, asm_s + f + h1 + 1, Lmid, tbl + h1 * h1, Mmid);
+  X.flops += 2.0 * Lmid * Mmid;
   ref_node_enter(X, h1, h);
-  const int64_t km = put_leaf(X, P, in_s, asm_s, f - 2 * h1 - 1, f + 2 * h1, f, h1);
+  const int64_t km = put_leaf(X, P, in_s, asm_s, pay_s, f - 2 * h1 - 1, f + 2 * h1, f, h1);
+  const long long t3 = clock64();
+  helper_wait(*X.S, X.c, tk);
+  const long long t4 = clock64();
   if (km == NONE_SEEN || km < f - h1 || km > f) { *err = FL_E_GEOMETRY | 1; return 0; }
-  // bottom: cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
+  // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
   const int64_t A = f + 2 * (int64_t)h - h1 - km;
   ref_node_bottom(X, h, A);
-  if (lane_id() < 4) asm_s[f + 2 * h - h1 + 1 + lane_id()] = 0.0;  // zero pad behind the assembled row
-  __syncwarp();  // leaf stores visible to the whole warp
-  M = 2 * h2 + 1;
-  warp_stage(s_w, X.kc + (int64_t)h2 * h2, M);
-  X.flops += warp_conv_direct(asm_s + km + 1, out_org + km + h2 + 1, A - 2 * (int64_t)h2, s_w, M);
+  const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
+  tk = helper_post(*X.S, X.c, asm_s + km + 1, out_org + km + h2 + 1, Lbot, tbl + h2 * h2, Mbot);
+  X.flops += 2.0 * Lbot * Mbot;
   // second half-height leaf from the assembled row
   ref_node_enter(X, h2, h);
-  const int64_t kp = put_leaf(X, P, asm_s, out_org, km - 2 * h2 - 1, km + 2 * h2, km, h2);
-  if (kp == NONE_SEEN || kp < km - h2 || kp > km) { *err = FL_E_GEOMETRY | 2; return 0; }
+  const int64_t kp = put_leaf(X, P, asm_s, out_org, pay_s, km - 2 * h2 - 1, km + 2 * h2, km, h2);
+  const long long t5 = clock64();
+  helper_wait(*X.S, X.c, tk);
   if (X.prof && lane_id() == 0) {
-    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
+    const long long t6 = clock64();
+    prof_add(X.prof, PROF_F_STAGE, t2 - t1);
+    prof_add(X.prof, PROF_F_MID, t4 - t3);
+    prof_add(X.prof, PROF_F_BOT, t6 - t5);
+    prof_add(X.prof, PROF_FUSE_CYC, t6 - t1);
     prof_add(X.prof, PROF_FUSE_N, 1);
   }
+  if (kp == NONE_SEEN || kp < km - h2 || kp > km) { *err = FL_E_GEOMETRY | 2; return 0; }
   return kp;
 }
 
@@ -206,7 +228,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
         wait_conflicts(*X.S, X.c, U(F.in_org + F.f + 1), U(F.in_org + F.f + 2 * h + 1), 0, 0,
                        U(F.out_org + F.f - h), U(F.out_org + F.f + h + 1));
         ref_node_enter(X, h, ph);
-        const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
+        const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, X.pay_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
         --sp;
@@ -282,6 +304,7 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   double* kc = frames + 2 * n_rows + 64 * PUT_MAX_DEPTH;
   const Stencil st{P.cd, P.cm, P.cu, 2};
   build_kernel_table(kc, st, scratch);
+  load_kernel_smem(scratch + CHAIN_SCRATCH, kc);
   PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
   // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
   // loaded with an initial segment (cols init_col0 .. +init_len)
@@ -336,7 +359,7 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       wait_conflicts(S, c, U(cur_org + f + 1), U(cur_org + f + 2), U(X.pay_org + f - 3), U(X.pay_org + f + 2),
                      U(nxt_org + f - 3), U(nxt_org + f + 2));
       X.ref_flops += ref_strip_flops(red + 4, 1);
-      const int64_t kb = put_leaf(X, P, cur_org, nxt_org, f - 3, f + 1, f, 1);
+      const int64_t kb = put_leaf(X, P, cur_org, nxt_org, X.pay_org, f - 3, f + 1, f, 1);
       if (kb == NONE_SEEN || kb < f - 1 || kb > f) { err = FL_E_GEOMETRY | 5; break; }
       f = kb;
       m += 1;

@@ -31,13 +31,41 @@
 
 namespace fl {
 
+// Warp layout (a warp's SM sub-partition, SMSP, is warp_id % 4):
+//   warps 0-3    big group (SMSP 0-3)
+//   warps 4-11   small workers (two per SMSP)
+//   warps 12-13  chain warps (SMSP 0, 1)
+//   warps 14-15  helper warps, one per chain (SMSP 2, 3): the chain's private
+//                co-processor for the direct correlations of its fused nodes,
+//                driven through a shared-memory mailbox (no ring, no deps scan)
+// (Isolating the chains on SMSPs of their own was measured: no gain.)
 constexpr int NCHAIN = 2;
-constexpr int BIG_WARPS = 4;
-constexpr int BIG_THREADS = 32 * BIG_WARPS;
 constexpr int SMALL_WORKERS = 8;
-constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + NCHAIN;
+constexpr int BIG_WARPS = 4;
+constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + 2 * NCHAIN;
+constexpr int BIG_THREADS = 32 * BIG_WARPS;
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
-constexpr int CHAIN_WARP0 = BIG_WARPS + SMALL_WORKERS;
+enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_SMALL = 2, ROLE_HELPER = 3 };
+
+__device__ __forceinline__ int warp_role(int w, int* rank) {
+  if (w >= BIG_WARPS + SMALL_WORKERS + NCHAIN) { *rank = w - BIG_WARPS - SMALL_WORKERS - NCHAIN; return ROLE_HELPER; }
+  if (w >= BIG_WARPS + SMALL_WORKERS) { *rank = w - BIG_WARPS - SMALL_WORKERS; return ROLE_CHAIN; }
+  if (w < BIG_WARPS) { *rank = w; return ROLE_BIG; }
+  *rank = w - BIG_WARPS;
+  return ROLE_SMALL;
+}
+
+// Mailbox between chain warp c and its helper: one direct correlation
+// y[k] = sum_r w[r] x[k+r], k < Lout, at a time (seq > done while pending).
+struct Mailbox {
+  const double* x;
+  double* y;
+  const double* w;
+  int Lout, M;
+  volatile int seq;   // last posted request (-1: exit)
+  volatile int done;  // last completed request
+};
+
 constexpr int NRINGS = 2;
 #ifndef FL_QCAP
 #define FL_QCAP 64
@@ -47,6 +75,12 @@ constexpr int NRINGS = 2;
 #endif
 #ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to one warp
 #define FL_SMALL_MW 320
+#endif
+#ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
+#define FL_IDLE_NS 512
+#endif
+#ifndef FL_HELPER_NS  // longest back-off sleep of an idle helper poll
+#define FL_HELPER_NS 128
 #endif
 constexpr int QCAP = FL_QCAP;  // per ring
 constexpr int BIG_BAR = 1;
@@ -97,6 +131,8 @@ struct SchedShared {
   double result[NCHAIN];   // per-chain results of blocking tasks
   double result2[NCHAIN];
   int64_t iresult[NCHAIN];
+  Mailbox mb[NCHAIN];
+  unsigned long long* prof;  // profile counters (null unless FL_PROFILE)
   int chains_left;
 };
 
@@ -111,6 +147,9 @@ enum : int {
   PROF_FFT_CYC = 0, PROF_FFT_N, PROF_DIR_CYC, PROF_DIR_N, PROF_OTHER_CYC, PROF_OTHER_N, PROF_BIG_CYC, PROF_BIG_N,
   PROF_STRIP_CYC, PROF_STRIP_N, PROF_WAIT_CYC, PROF_FUSE_CYC, PROF_FUSE_N, PROF_KERNEL_CYC, PROF_IDLE_CYC,
   PROF_ISS_CYC, PROF_CHAIN_CYC, PROF_DEPWAIT_CYC,
+  // detail (chain side)
+  PROF_ISS_SCAN, PROF_ISS_STALL, PROF_ISS_SLOT, PROF_F_STAGE, PROF_F_MID, PROF_F_BOT, PROF_STRIP_LOOP,
+  PROF_LEAF_LOAD,
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
@@ -128,7 +167,32 @@ __device__ void sched_init(SchedShared& S) {
     S.claim[threadIdx.x] = 0;
   }
   if (threadIdx.x == 0) S.chains_left = NCHAIN;
-  if (threadIdx.x < NCHAIN) S.npend[threadIdx.x] = 0;
+  if (threadIdx.x < NCHAIN) {
+    S.npend[threadIdx.x] = 0;
+    S.mb[threadIdx.x].seq = 0;
+    S.mb[threadIdx.x].done = 0;
+  }
+}
+
+// Chain side of the mailbox (all lanes call): post a correlation, returns its ticket.
+__device__ __forceinline__ int helper_post(SchedShared& S, int c, const double* x, double* y, int Lout,
+                                           const double* w, int M) {
+  Mailbox& m = S.mb[c];
+  const int t = m.seq + 1;
+  __threadfence_block();  // every lane's writes to x (shared) ...
+  __syncwarp();           // ... are done before lane 0 publishes
+  if (threadIdx.x % 32 == 0) {
+    m.x = x; m.y = y; m.w = w; m.Lout = Lout; m.M = M;
+    __threadfence_block();
+    m.seq = t;
+  }
+  __syncwarp();
+  return t;
+}
+
+__device__ __forceinline__ void helper_wait(SchedShared& S, int c, int ticket) {
+  while (__shfl_sync(0xffffffffu, S.mb[c].done, 0) < ticket) __nanosleep(8);
+  __threadfence_block();
 }
 
 __device__ __forceinline__ bool overlap(uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) {
@@ -197,8 +261,11 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
                      uintptr_t whi) {
   int deps[NDEP];
   int nd;
+  const long long t0 = S.prof ? clock64() : 0;
+  long long t1 = 0, t2 = 0;
   for (;;) {
     nd = scan_conflicts(S, c, rlo, rhi, 0, 0, wlo, whi, deps, NDEP);
+    if (S.prof && t1 == 0) t1 = clock64();
     if (nd <= NDEP) break;
     warp_wait_done(S, deps[0]);  // too many: retire the oldest conflict first
   }
@@ -212,8 +279,15 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
   int idx = 0;
   if (lane_id() == 0) idx = atomicAdd(&S.reserve[ring], 1);
   idx = __shfl_sync(FULL, idx, 0);
+  if (S.prof) t2 = clock64();
   // the slot's previous occupant must be finished
   while (!__shfl_sync(FULL, (int)(S.done[ring][idx % QCAP] >= idx - QCAP), 0)) __nanosleep(64);
+  if (S.prof && lane_id() == 0) {
+    const long long t3 = clock64();
+    prof_add(S.prof, PROF_ISS_SCAN, t1 - t0);
+    prof_add(S.prof, PROF_ISS_STALL, t2 - t1);
+    prof_add(S.prof, PROF_ISS_SLOT, t3 - t2);
+  }
   const int id = (ring << 28) | (idx & 0x0fffffff);  // ring in bits 28..31
   if (lane_id() == 0) {
     Task& s = S.ring[ring][idx % QCAP];
@@ -291,49 +365,52 @@ __device__ void build_kernel_table(double* kc, const Stencil& st, double* scratc
   __threadfence_block();
 }
 
-// y[k] = sum_{r<M} w[r] x[k+r], k < Lout, on the calling warp.  x and w may be
-// generic (shared or global) pointers.  Register-blocked: lane l produces the
-// B = 4 consecutive outputs 4l..4l+3 of each 128-output pass, sliding a
-// 4-element window of x through registers (2 loads per 4 multiply-adds).
-__device__ double warp_conv_direct(const double* __restrict__ x, double* __restrict__ y, int64_t Lout,
-                                   const double* __restrict__ w, int M) {
+// y[k] = sum_{r<M} w[r] x[k+r], k < Lout, on the calling warp (x, w normally
+// in shared memory).  Lane l produces outputs k0+l+32j (j < B) of a pass:
+// consecutive lanes read consecutive x (bank-conflict free), w[r] is a
+// broadcast, and every output keeps two partial sums (even / odd taps) to
+// halve its dependent DFMA chain.  Reads x only inside [0, Lout+M-1).
+template <int B>
+__device__ __forceinline__ void conv_direct_pass(const double* __restrict__ x, double* __restrict__ y, int64_t k0,
+                                                 int64_t Lout, const double* __restrict__ w, int M) {
   const int lane = lane_id();
-  for (int64_t k0 = 0; k0 < Lout; k0 += 128) {
-    const int64_t kb = k0 + 4 * lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    if (kb < Lout) {
-      const double* xk = x + kb;
-      double x0 = xk[0], x1 = xk[1], x2 = xk[2];
-      int r = 0;
-#pragma unroll 2
-      for (; r + 3 < M; r += 4) {
-        // taps r..r+3 with the window rotating through x0..x3 (no register moves)
-        double x3 = xk[r + 3];
-        double wr = w[r];
-        a0 = fma(wr, x0, a0); a1 = fma(wr, x1, a1); a2 = fma(wr, x2, a2); a3 = fma(wr, x3, a3);
-        x0 = xk[r + 4];
-        wr = w[r + 1];
-        a0 = fma(wr, x1, a0); a1 = fma(wr, x2, a1); a2 = fma(wr, x3, a2); a3 = fma(wr, x0, a3);
-        x1 = xk[r + 5];
-        wr = w[r + 2];
-        a0 = fma(wr, x2, a0); a1 = fma(wr, x3, a1); a2 = fma(wr, x0, a2); a3 = fma(wr, x1, a3);
-        x2 = xk[r + 6];
-        wr = w[r + 3];
-        a0 = fma(wr, x3, a0); a1 = fma(wr, x0, a1); a2 = fma(wr, x1, a2); a3 = fma(wr, x2, a3);
-      }
-      for (; r < M; ++r) {  // tail taps (window restarts from memory)
-        const double wr = w[r];
-        a0 = fma(wr, xk[r], a0);
-        a1 = fma(wr, xk[r + 1], a1);
-        a2 = fma(wr, xk[r + 2], a2);
-        a3 = fma(wr, xk[r + 3], a3);
-      }
-      y[kb] = a0;
-      if (kb + 1 < Lout) y[kb + 1] = a1;
-      if (kb + 2 < Lout) y[kb + 2] = a2;
-      if (kb + 3 < Lout) y[kb + 3] = a3;
+  double ae[B], ao[B];
+  const double* xp[B];
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const int64_t k = k0 + lane + 32 * j;
+    xp[j] = x + (k < Lout ? k : Lout - 1);
+    ae[j] = 0.0;
+    ao[j] = 0.0;
+  }
+  int r = 0;
+#pragma unroll 4
+  for (; r + 1 < M; r += 2) {
+    const double w0 = w[r], w1 = w[r + 1];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      ae[j] = fma(w0, xp[j][r], ae[j]);
+      ao[j] = fma(w1, xp[j][r + 1], ao[j]);
     }
   }
+  if (r < M) {
+    const double w0 = w[r];
+#pragma unroll
+    for (int j = 0; j < B; ++j) ae[j] = fma(w0, xp[j][r], ae[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    const int64_t k = k0 + lane + 32 * j;
+    if (k < Lout) y[k] = ae[j] + ao[j];
+  }
+}
+
+__device__ double warp_conv_direct(const double* __restrict__ x, double* __restrict__ y, int64_t Lout,
+                                   const double* __restrict__ w, int M) {
+  int64_t k0 = 0;
+  for (; Lout - k0 > 64; k0 += 128) conv_direct_pass<4>(x, y, k0, Lout, w, M);
+  if (Lout - k0 > 32) conv_direct_pass<2>(x, y, k0, Lout, w, M);
+  else if (Lout > k0) conv_direct_pass<1>(x, y, k0, Lout, w, M);
   __syncwarp();
   return 2.0 * (double)Lout * (double)M;
 }
@@ -376,7 +453,13 @@ __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const doubl
 // (warp-uniform; called by one warp).
 __device__ __forceinline__ void worker_wait_ready(SchedShared& S, int ring, int idx) {
   Task& s = S.ring[ring][idx % QCAP];
-  while (__shfl_sync(FULL, s.seq, 0) != idx) __nanosleep(20);
+  // idle poll with exponential backoff: spinning warps steal issue slots and
+  // shared-memory (MIO) bandwidth from the chains' shuffles
+  unsigned ns = 16;
+  while (__shfl_sync(FULL, s.seq, 0) != idx) {
+    __nanosleep(ns);
+    ns = ns < FL_IDLE_NS ? 2 * ns : ns;
+  }
   __threadfence_block();
   const int nd = s.ndep;
   for (int i = 0; i < nd; ++i) warp_wait_done(S, s.dep[i]);
@@ -429,10 +512,21 @@ __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logN
 //                          const double2* tq, const Grp& g) const;
 //       execute one task (pricer-specific kinds, else exec_generic)
 
-constexpr int CHAIN_SCRATCH = 384;  // doubles of shared memory per chain warp
+constexpr int CHAIN_SCRATCH = 544;  // doubles of shared-memory scratch per chain warp
+// followed by the chain's copy of the composed weights W_1..W_KSMEM_M (slot m at m*m)
+constexpr int KSMEM_M = 32;
+constexpr int KSMEM_DOUBLES = ((KSMEM_M + 1) * (KSMEM_M + 1) + 1) & ~1;
+constexpr int CHAIN_SMEM = CHAIN_SCRATCH + KSMEM_DOUBLES;
+
+// Copy W_1..W_KSMEM_M of a kernel table (global, slot m at kc + m*m) into the
+// chain's shared copy (all lanes of the chain warp call).
+__device__ __forceinline__ void load_kernel_smem(double* dst, const double* kc) {
+  for (int i = lane_id(); i < (KSMEM_M + 1) * (KSMEM_M + 1); i += 32) dst[i] = kc[i];
+  __syncwarp();
+}
 
 __host__ __device__ constexpr int sched_smem_bytes() {
-  return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SCRATCH) * (int)sizeof(double) +
+  return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SMEM) * (int)sizeof(double) +
          (TWQ + BIG_SLOTS + SMALL_WORKERS * SMALL_SLOTS) * (int)sizeof(double2);
 }
 
@@ -444,17 +538,47 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   // dynamic shared memory: scheduler state | chain scratch | twiddles | FFT buffers
   SchedShared& S = *reinterpret_cast<SchedShared*>(sdyn_raw);
   double* chain_scratch = reinterpret_cast<double*>(sdyn_raw) + SCHED_SHARED_DOUBLES;
-  double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SCRATCH);  // quarter-wave twiddles
+  double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SMEM);  // quarter-wave twiddles
   double2* bigbuf = tq + TWQ;              // big-group FFT buffer
   double2* smallbuf = bigbuf + BIG_SLOTS;  // SMALL_WORKERS x SMALL_SLOTS
   __shared__ int s_idx;
   for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
   sched_init(S);
+  if (threadIdx.x == 0) S.prof = prof;
   __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  if (warp >= CHAIN_WARP0) {
-    // ---- chain warps (highest warp ids)
-    const int c = warp - CHAIN_WARP0;
+  int rank = 0;
+  const int role = warp_role(threadIdx.x >> 5, &rank);
+  if (role == ROLE_HELPER) {
+    // ---- helper warp of chain `rank`: direct correlations posted via the mailbox
+    Mailbox& m = S.mb[rank];
+    double flops = 0.0;
+    int last = 0;
+    for (;;) {
+      int sq;
+      unsigned ns = 8;
+      while ((sq = __shfl_sync(FULL, m.seq, 0)) == last) {
+        __nanosleep(ns);
+        ns = ns < FL_HELPER_NS ? 2 * ns : ns;
+      }
+      if (sq < 0) break;
+      __threadfence_block();
+      const volatile Mailbox& vm = m;
+      const double* x = vm.x;
+      double* y = vm.y;
+      const double* w = vm.w;
+      const int Lout = vm.Lout, M = vm.M;
+      flops += warp_conv_direct(x, y, Lout, w, M);
+      __threadfence_block();
+      __syncwarp();
+      if (lane_id() == 0) m.done = sq;
+      last = sq;
+    }
+    if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
+    return;
+  }
+  if (role == ROLE_CHAIN) {
+    // ---- chain warps
+    const int c = rank;
     double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
     double chain_flops = 0.0;
     for (;;) {
@@ -462,7 +586,11 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       if (lane_id() == 0) w = atomicAdd(counter, 1);
       w = __shfl_sync(FULL, w, 0);
       if (w >= nwork) break;
-      pr.chain(S, c, w, arena, chain_scratch + c * CHAIN_SCRATCH, &chain_flops);
+      pr.chain(S, c, w, arena, chain_scratch + c * CHAIN_SMEM, &chain_flops);
+    }
+    if (lane_id() == 0) {  // release this chain's helper
+      __threadfence_block();
+      S.mb[c].seq = -1;
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)chain_flops);
     int last = 0;
@@ -482,12 +610,12 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   }
   double flops = 0.0;
   const long long t_start = clock64();
-  if (warp < BIG_WARPS) {
+  if (role == ROLE_BIG) {
     // ---- big group: one task at a time over BIG_THREADS threads
-    const Grp g{(int)threadIdx.x, BIG_THREADS, BIG_BAR};
+    const Grp g{rank * 32 + lane_id(), BIG_THREADS, BIG_BAR};
     for (;;) {
       const long long t0 = clock64();
-      if (warp == 0) {
+      if (rank == 0) {
         int idx = 0;
         if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_BIG], 1);
         idx = __shfl_sync(FULL, idx, 0);
@@ -511,7 +639,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     }
   } else {
     // ---- small workers: one warp per task
-    const int sw = warp - BIG_WARPS;
+    const int sw = rank;
     const Grp g{lane_id(), 32, -1};
     double2* buf = smallbuf + sw * SMALL_SLOTS;
     for (;;) {
@@ -537,7 +665,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       }
     }
   }
-  if ((threadIdx.x & 31) == 0 && (warp >= BIG_WARPS || warp == 0)) {
+  if (lane_id() == 0 && (role == ROLE_SMALL || rank == 0)) {
     if (flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
   }

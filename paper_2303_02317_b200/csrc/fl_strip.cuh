@@ -82,6 +82,87 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
   return kb;
 }
 
+// put_strip_warp restricted to the columns that can still change.  The put
+// boundary drops by 0 or 1 column per row (bsm.py:420-427 enforces it: the
+// reference raises GeometryError otherwise), so at row s every column below
+// f-s is an exercise cell: its projected value is its payoff (deep in the
+// exercise region lin - payoff ~ -omega*dtau, far from any rounding tie).
+// The strip therefore only needs the frame [f-h-1, hi] (3h+2 columns instead
+// of 4h+2), with the payoff of column f-h-2 as the fixed left neighbour.
+// Same per-cell arithmetic and the same returned boundary / outputs as
+// put_strip_warp.  The green mask is formed on the final row only.
+template <int CPL>
+__device__ int64_t put_strip_v2(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                const double* __restrict__ pay_org, int64_t hi, int64_t f, int height, double cd,
+                                double cm, double cu, long long* tm = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t lo = f - height - 1;
+  double v[CPL], p[CPL];
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
+  }
+  const double edge = pay_org[lo - 1];  // fixed left neighbour of the frame (an exercise cell)
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(v[0] + p[0] + edge == 12345.678 ? 1 : 0); }
+  unsigned green = 0;
+  for (int s = 1; s <= height; ++s) {
+    const double up = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double right = __shfl_down_sync(FULL, v[0], 1);
+    const double left = (lane == 0) ? edge : up;
+    double nv[CPL];
+    if (s < height) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double l = (c == 0) ? left : v[c - 1];
+        const double r = (c == CPL - 1) ? right : v[c + 1];
+        const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+        nv[c] = lin > p[c] ? lin : p[c];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double l = (c == 0) ? left : v[c - 1];
+        const double r = (c == CPL - 1) ? right : v[c + 1];
+        const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+        const bool red = lin > p[c];
+        nv[c] = red ? lin : p[c];
+        green |= (red ? 0u : 1u) << c;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
+  // last green inside the final valid range [f-h-1, hi-h]
+  const int64_t vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = v[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
 // Time-tiled variant of put_strip_warp: lanes exchange K halo cells per side
 // once per K rows (instead of one cell per side per row) and advance K rows on
 // an extended register tile, recomputing the halo cone redundantly.  One

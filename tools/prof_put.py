@@ -15,7 +15,8 @@ p = db.profile().astype(np.float64)
 # must match the PROF_* enum in csrc/fl_sched.cuh
 names = ["FFT_CYC", "FFT_N", "DIR_CYC", "DIR_N", "OTHER_CYC", "OTHER_N", "BIG_CYC", "BIG_N",
          "STRIP_CYC", "STRIP_ROWS", "WAIT_CYC", "FUSE_CYC", "FUSE_N", "KERNEL_CYC", "IDLE_CYC",
-         "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC"]
+         "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC", "ISS_SCAN", "ISS_STALL", "ISS_SLOT", "F_STAGE", "F_MID",
+         "F_BOT", "STRIP_LOOP", "LEAF_LOAD"]
 P = dict(zip(names, p[:len(names)]))
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
 for nm in names:
@@ -29,4 +30,11 @@ print("small tasks: fft n=%.0f avg %.0f cyc; direct n=%.0f avg %.0f; other n=%.0
       % (P["FFT_N"], d(P["FFT_CYC"], P["FFT_N"]), P["DIR_N"], d(P["DIR_CYC"], P["DIR_N"]),
          P["OTHER_N"], d(P["OTHER_CYC"], P["OTHER_N"])))
 print("big tasks: n=%.0f avg %.0f cyc" % (P["BIG_N"], d(P["BIG_CYC"], P["BIG_N"])))
+ntask = P["FFT_N"] + P["DIR_N"] + P["OTHER_N"] + P["BIG_N"]
+print("issue per task: scan %.0f stall %.0f slot %.0f (tasks/option %.0f)" % (
+    d(P["ISS_SCAN"], ntask), d(P["ISS_STALL"], ntask), d(P["ISS_SLOT"], ntask), ntask / nopt))
+print("fused per node: stage %.0f mid %.0f bottom %.0f" % (d(P["F_STAGE"], P["FUSE_N"]), d(P["F_MID"], P["FUSE_N"]),
+                                                          d(P["F_BOT"], P["FUSE_N"])))
+print("strip: loop %.1f cyc/row, load %.0f cyc/leaf (leaves/option %.0f)" % (
+    d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"] / 28.0), P["STRIP_ROWS"] / 28.0 / nopt))
 print("status nonzero:", int(np.sum(r.status != 0)))
