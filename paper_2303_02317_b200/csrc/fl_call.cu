@@ -7,7 +7,7 @@
 // Same execution model as the put (fl_put.cu, fl_sched.cuh): a chain warp
 // walks one option -- junction row, trapezoid loop, halving recursion -- and
 // keeps the nonlinear leaves (binomial_strip_sweep, one column per lane,
-// first green by warp min) and the nodes up to CALL_FUSE_H (in shared memory)
+// first green by warp min) and whole subtrees up to CALL_HS (in shared memory)
 // to itself; the left / mid / bottom linear jumps are worker tasks, the
 // junction row and the ceil(sqrt(T))-row residual strip are big-group tasks.
 #include <cstdint>
@@ -22,12 +22,13 @@
 namespace fl {
 
 constexpr int CALL_LEAF = 32;
-constexpr int CALL_FUSE_H = 2 * CALL_LEAF;
+constexpr int CALL_HS = 128;  // recursion subtrees of height <= CALL_HS run whole in shared memory
 constexpr int CALL_MAX_DEPTH = 28;
 constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per big-group thread (width <= 1024)
-constexpr int CALL_SEG = CALL_FUSE_H + 8;
-static_assert(2 * CALL_SEG <= CHAIN_SCRATCH, "call fused node scratch");
-static_assert(CALL_LEAF <= KSMEM_M, "fused-node weights come from the chain's shared table");
+constexpr int CSUB_IN = 0, CSUB_ASM0 = CALL_HS + 8, CSUB_ASM1 = CSUB_ASM0 + CALL_HS + 8;
+static_assert(CSUB_ASM1 + CALL_HS / 2 + 8 <= CHAIN_SCRATCH, "call subtree scratch");
+static_assert(CALL_HS <= 4 * CALL_LEAF, "two asm levels cover a subtree");
+static_assert(CALL_HS / 2 <= DIRECT_H, "subtree correlations use the direct kernel table");
 
 enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
 
@@ -137,47 +138,86 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
   return jp;
 }
 
-// Node with CALL_LEAF < h <= CALL_FUSE_H, whole on the chain warp in shared
-// memory (american.py:201-257 for one level).  vals = in_org[j-h+1 .. j];
-// writes out_org[j-h+1 .. jp]; returns jp.
-__device__ int64_t call_fused_node(CallChainCtx& X, const CallParams& P, int64_t i, int64_t j, const double* in_org,
-                                   double* out_org, int h, int ph, int32_t* err) {
-  const int64_t lo = j - h + 1;
+struct CallSubFrame {
+  int64_t i, j, jm;
+  const double* in;
+  double* out;
+  double* asmo;
+  int h, state, tk, tk0;
+};
+
+// A recursion subtree of height h0 <= CALL_HS done whole in shared memory
+// (american.py:201-257 below this node): vals = in_org[j0-h0+1 .. j0] staged
+// once; the chain runs the leaf strips while its helper warp runs every mid /
+// bottom correlation (overlapping the node's first / second child).  Writes
+// out_org[j0-h0+1 .. jp]; returns jp.
+__device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0, int64_t j0, const double* in_org,
+                                double* out_org, int h0, int ph0, int32_t* err) {
+  const int64_t lo0 = j0 - h0 + 1;
   const long long t0 = clock64();
-  wait_conflicts(*X.S, X.c, U(in_org + lo), U(in_org + j + 1), 0, 0, U(out_org + lo), U(out_org + j + 1));
-  if (X.prof && lane_id() == 0) prof_add(X.prof, PROF_WAIT_CYC, clock64() - t0);
+  wait_conflicts(*X.S, X.c, U(in_org + lo0), U(in_org + j0 + 1), 0, 0, U(out_org + lo0), U(out_org + j0 + 1));
   const long long t1 = clock64();
-  const int h1 = (h + 1) / 2, h2 = h - h1;
-  call_ref_enter(X, h, ph);
-  double* s_in = X.scratch;              // cols lo .. j
-  double* s_asm = X.scratch + CALL_SEG;  // cols lo .. jm
-  const double* tbl = X.scratch + CHAIN_SCRATCH;
-  warp_stage(s_in, in_org + lo, h);
-  const double* in_s = s_in - lo;
-  double* asm_s = s_asm - lo;
-  // mid (helper): cols lo .. j-h1 of row i-h1, overlapping the first leaf
-  int tk = helper_post(*X.S, X.c, s_in, s_asm, h2, tbl + h1 * h1, h1 + 1);
-  X.flops += 2.0 * h2 * (h1 + 1);
-  call_ref_enter(X, h1, h);
-  const int64_t jm = call_leaf(X, P, in_s, asm_s, i, j, h1);
-  helper_wait(*X.S, X.c, tk);
-  if (jm < j - h1 || jm > j) { *err = FL_E_GEOMETRY | 1; return 0; }
-  const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
-  call_ref_bottom(X, h, A);
-  tk = -1;
-  if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h, overlapping the second leaf
-    tk = helper_post(*X.S, X.c, s_asm, out_org + lo, (int)(A - h2), tbl + h2 * h2, h2 + 1);
-    X.flops += 2.0 * (A - h2) * (h2 + 1);
+  double* s_in = X.scratch + CSUB_IN;
+  warp_stage(s_in, in_org + lo0, h0);
+  long long twait = 0;
+  CallSubFrame stk[4];
+  stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in = s_in - lo0; stk[0].out = out_org; stk[0].state = 0;
+  int sp = 1;
+  int64_t ret = 0;
+  while (sp > 0) {
+    CallSubFrame& F = stk[sp - 1];
+    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
+    const int ph = (sp >= 2) ? stk[sp - 2].h : ph0;
+    const int64_t lo = F.j - h + 1;
+    if (F.state == 0) {
+      call_ref_enter(X, h, ph);
+      if (h <= CALL_LEAF) {
+        ret = call_leaf(X, P, F.in, F.out, F.i, F.j, h);
+        --sp;
+        continue;
+      }
+      F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : CSUB_ASM1) - lo;
+      // mid (helper): cols lo .. j-h1 of row i-h1
+      F.tk = helper_post(*X.S, X.c, F.in + lo, F.asmo + lo, h2, X.kc + (int64_t)h1 * h1, h1 + 1, &F.tk0);
+      X.flops += 2.0 * h2 * (h1 + 1);
+      F.state = 1;
+      CallSubFrame& C = stk[sp++];
+      C.i = F.i; C.j = F.j; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
+    } else if (F.state == 1) {
+      const int64_t jm = ret;
+      if (jm < F.j - h1 || jm > F.j) { *err = FL_E_GEOMETRY | 1; return 0; }
+      F.jm = jm;
+      const long long tw = clock64();
+      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      twait += clock64() - tw;
+      const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
+      call_ref_bottom(X, h, A);
+      F.tk = -1;
+      if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h
+        F.tk = helper_post(*X.S, X.c, F.asmo + lo, F.out + lo, (int)(A - h2), X.kc + (int64_t)h2 * h2, h2 + 1, &F.tk0);
+        X.flops += 2.0 * (A - h2) * (h2 + 1);
+      }
+      F.state = 2;
+      CallSubFrame& C = stk[sp++];
+      C.i = F.i - h1; C.j = jm; C.h = h2; C.in = F.asmo; C.out = F.out; C.state = 0;
+    } else {
+      const int64_t jp = ret;
+      if (jp < F.jm - h2 || jp > F.jm) { *err = FL_E_GEOMETRY | 2; return 0; }
+      if (F.tk >= 0) {
+        const long long tw = clock64();
+        helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+        twait += clock64() - tw;
+      }
+      --sp;
+    }
   }
-  call_ref_enter(X, h2, h);
-  const int64_t jp = call_leaf(X, P, asm_s, out_org, i - h1, jm, h2);
-  if (tk >= 0) helper_wait(*X.S, X.c, tk);
-  if (jp < jm - h2 || jp > jm) { *err = FL_E_GEOMETRY | 2; return 0; }
   if (X.prof && lane_id() == 0) {
+    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
+    prof_add(X.prof, PROF_F_MID, twait);
     prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
     prof_add(X.prof, PROF_FUSE_N, 1);
   }
-  return jp;
+  return ret;
 }
 
 __device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
@@ -201,16 +241,8 @@ __device__ int64_t call_solve(CallChainCtx& X, const CallParams& P, int64_t i0, 
     const int ph = (sp >= 2) ? stk[sp - 2].h : 0x7fffffff;
     if (F.state == 0) {
       const int64_t lo = F.j - h + 1;
-      if (h <= CALL_LEAF) {
-        wait_conflicts(*X.S, X.c, U(F.in_org + lo), U(F.in_org + F.j + 1), 0, 0, U(F.out_org + lo),
-                       U(F.out_org + F.j + 1));
-        call_ref_enter(X, h, ph);
-        ret = call_leaf(X, P, F.in_org, F.out_org, F.i, F.j, h);
-        --sp;
-        continue;
-      }
-      if (h <= CALL_FUSE_H) {
-        ret = call_fused_node(X, P, F.i, F.j, F.in_org, F.out_org, h, ph, err);
+      if (h <= CALL_HS) {
+        ret = call_subtree(X, P, F.i, F.j, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
         --sp;
         continue;
@@ -261,7 +293,6 @@ __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams
   double* kc = frames + 2 * h_max + 16 * CALL_MAX_DEPTH;
   const Stencil st{P.wd, P.wu, 0.0, 1};
   build_kernel_table(kc, st, scratch);
-  load_kernel_smem(scratch + CHAIN_SCRATCH, kc);
   return CallChainCtx{&S, c, st, kc, frames, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
 }
 

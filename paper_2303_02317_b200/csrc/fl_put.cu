@@ -39,11 +39,22 @@ namespace fl {
 #endif
 constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
-constexpr int FUSE_H = 2 * PUT_LEAF;                   // nodes up to this height are fused on the chain
+#ifndef FL_PUT_HS
+#define FL_PUT_HS 128
+#endif
+// recursion subtrees of height <= PUT_HS run whole in the chain's shared memory
+constexpr int PUT_HS = FL_PUT_HS;
+constexpr int PUT_MARGIN = 2 * PUT_HS + 32;  // columns below the lowest boundary kept in the stage buffers
 constexpr int PUT_MAX_DEPTH = 24;
-constexpr int FUSE_SEG = 2 * FUSE_H + 8;  // fused-node row buffers (doubles, incl. zero pad)
-static_assert(2 * FUSE_SEG + 4 * FUSE_H + 2 <= CHAIN_SCRATCH, "fused node scratch");
-static_assert(PUT_LEAF <= KSMEM_M, "fused-node weights come from the chain's shared table");
+// shared layout of a subtree: payoff (4 HS + 2) | input row (2 HS) | asm level 0 (2 HS) | asm level 1 (HS)
+constexpr int SUB_PAY = 0;
+constexpr int SUB_IN = SUB_PAY + 4 * PUT_HS + 8;
+constexpr int SUB_ASM0 = SUB_IN + 2 * PUT_HS + 8;
+constexpr int SUB_ASM1 = SUB_ASM0 + 2 * PUT_HS + 8;
+constexpr int SUB_END = SUB_ASM1 + PUT_HS + 8;
+static_assert(SUB_END <= CHAIN_SCRATCH, "subtree scratch");
+static_assert(PUT_HS <= 4 * PUT_LEAF, "two asm levels cover a subtree");
+static_assert(PUT_HS / 2 <= DIRECT_H, "subtree correlations use the direct kernel table");
 static_assert(2 * (2 * DIRECT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
 enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD = TK_USER + 2 };
@@ -78,7 +89,7 @@ struct PutLayout {
 __host__ __device__ inline PutLayout put_layout(int64_t n, int64_t ks) {
   PutLayout L;
   const int64_t lowest = (ks - n < -n ? ks - n : -n);
-  L.colbase = lowest - 4 * FUSE_H - 16;
+  L.colbase = lowest - PUT_MARGIN;
   L.span = (ks + n + 8) - L.colbase + 1;
   return L;
 }
@@ -86,7 +97,7 @@ __host__ __device__ inline PutLayout put_layout(int64_t n, int64_t ks) {
 // trapezoid problem (solve_bsm_trapezoid): columns f-2h-1 .. f+W
 __host__ __device__ inline PutLayout put_trap_layout(int64_t f, int64_t W, int64_t h) {
   PutLayout L;
-  L.colbase = f - 2 * h - 4 * FUSE_H - 16;
+  L.colbase = f - 2 * h - PUT_MARGIN;
   L.span = (f + W + 8) - L.colbase + 1;
   return L;
 }
@@ -97,7 +108,7 @@ __host__ __device__ inline int64_t put_arena_doubles(int64_t span, int64_t n_row
 
 // doubles needed per chain for a batch whose options have at most these sizes
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max) {
-  const int64_t span = 2 * n_max + ks_pos_max + 4 * FUSE_H + 32;
+  const int64_t span = 2 * n_max + ks_pos_max + PUT_MARGIN + 16;
   return put_arena_doubles(span, n_max);
 }
 
@@ -144,66 +155,99 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   return kb;
 }
 
-// A node with PUT_LEAF < h <= FUSE_H done whole in shared memory
-// (bsm.py:443-501 for one level): input cols f+1..f+2h of in_org, output cols
-// kp+1..f+h of out_org.  The input row and the payoff of cols f-2h-1..f+2h are
-// staged once; the chain runs the two half-height leaves while its helper
-// warp runs the mid jump (overlapping the first leaf) and the bottom jump
-// (overlapping the second), from the chain's shared copy of W_1..W_32.
-__device__ int64_t put_fused_node(PutChainCtx& X, const PutParams& P, int64_t f, const double* in_org,
-                                  double* out_org, int h, int ph, int32_t* err) {
+struct SubFrame {
+  int64_t f, km;
+  const double* in;
+  double* out;
+  double* asmo;
+  int h, state, tk, tk0;
+};
+
+// A recursion subtree of height h0 <= PUT_HS done whole in shared memory
+// (bsm.py:443-501 below this node): input cols f0+1..f0+2h0 of in_org, output
+// cols kp+1..f0+h0 of out_org.  The input row and the payoff of cols
+// f0-2h0-1..f0+2h0 are staged once; the chain walks the subtree running the
+// leaf strips, while its helper warp runs every mid / bottom correlation from
+// shared memory (a node's mid overlaps its first child, its bottom its second).
+__device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
+                               double* out_org, int h0, int ph0, int32_t* err) {
   const long long t0 = clock64();
-  wait_conflicts(*X.S, X.c, U(in_org + f + 1), U(in_org + f + 2 * h + 1), 0, 0, U(out_org + f - h),
-                 U(out_org + f + h + 1));
-  if (X.prof && lane_id() == 0) prof_add(X.prof, PROF_WAIT_CYC, clock64() - t0);
+  wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
+                 U(out_org + f0 + h0 + 1));
   const long long t1 = clock64();
-  const int h1 = (h + 1) / 2, h2 = h - h1;
-  ref_node_enter(X, h, ph);
-  double* s_in = X.scratch;                  // cols f+1 .. f+2h
-  double* s_asm = X.scratch + FUSE_SEG;      // cols f-h1+1 .. f+2h-h1
-  double* s_pay = X.scratch + 2 * FUSE_SEG;  // payoff of cols f-2h-1 .. f+2h
-  const double* tbl = X.scratch + CHAIN_SCRATCH;
-  const int64_t plo = f - 2 * (int64_t)h - 1;
-  for (int i = lane_id(); i < 4 * h + 2; i += 32) {  // one round trip for both rows
-    if (i < 2 * h) s_in[i] = in_org[f + 1 + i];
-    s_pay[i] = X.pay_org[plo + i];
-  }
-  __syncwarp();
-  const double* in_s = s_in - (f + 1);  // column origins of the shared rows
-  double* asm_s = s_asm - (f - h1 + 1);
+  double* s_pay = X.scratch + SUB_PAY;
+  double* s_in = X.scratch + SUB_IN;
+  const int64_t plo = f0 - 2 * (int64_t)h0 - 1;
+  warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
+  warp_stage_nb<(4 * PUT_HS + 2 + 31) / 32>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
   const double* pay_s = s_pay - plo;
   const long long t2 = clock64();
-  // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first leaf
-  const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
-  int tk = helper_post(*X.S, X.c, s_in, asm_s + f + h1 + 1, Lmid, tbl + h1 * h1, Mmid);
-  X.flops += 2.0 * Lmid * Mmid;
-  ref_node_enter(X, h1, h);
-  const int64_t km = put_leaf(X, P, in_s, asm_s, pay_s, f - 2 * h1 - 1, f + 2 * h1, f, h1);
-  const long long t3 = clock64();
-  helper_wait(*X.S, X.c, tk);
-  const long long t4 = clock64();
-  if (km == NONE_SEEN || km < f - h1 || km > f) { *err = FL_E_GEOMETRY | 1; return 0; }
-  // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
-  const int64_t A = f + 2 * (int64_t)h - h1 - km;
-  ref_node_bottom(X, h, A);
-  const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
-  tk = helper_post(*X.S, X.c, asm_s + km + 1, out_org + km + h2 + 1, Lbot, tbl + h2 * h2, Mbot);
-  X.flops += 2.0 * Lbot * Mbot;
-  // second half-height leaf from the assembled row
-  ref_node_enter(X, h2, h);
-  const int64_t kp = put_leaf(X, P, asm_s, out_org, pay_s, km - 2 * h2 - 1, km + 2 * h2, km, h2);
-  const long long t5 = clock64();
-  helper_wait(*X.S, X.c, tk);
+  long long twait = 0, tpost = 0;
+  SubFrame stk[4];
+  stk[0].f = f0; stk[0].h = h0; stk[0].in = s_in - (f0 + 1); stk[0].out = out_org; stk[0].state = 0;
+  int sp = 1;
+  int64_t ret = 0;
+  while (sp > 0) {
+    SubFrame& F = stk[sp - 1];
+    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
+    const int ph = (sp >= 2) ? stk[sp - 2].h : ph0;
+    if (F.state == 0) {
+      ref_node_enter(X, h, ph);
+      if (h <= PUT_LEAF) {
+        const int64_t kb = put_leaf(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
+        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
+        ret = kb;
+        --sp;
+        continue;
+      }
+      F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : SUB_ASM1) - (F.f - h1 + 1);
+      // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
+      const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
+      const long long tp = clock64();
+      F.tk = helper_post(*X.S, X.c, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, X.kc + (int64_t)h1 * h1, Mmid,
+                         &F.tk0);
+      tpost += clock64() - tp;
+      X.flops += 2.0 * Lmid * Mmid;
+      F.state = 1;
+      SubFrame& C = stk[sp++];
+      C.f = F.f; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
+    } else if (F.state == 1) {
+      const int64_t km = ret;
+      if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
+      F.km = km;
+      const long long tw = clock64();
+      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      twait += clock64() - tw;
+      // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
+      const int64_t A = F.f + 2 * (int64_t)h - h1 - km;
+      ref_node_bottom(X, h, A);
+      const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
+      const long long tp = clock64();
+      F.tk = helper_post(*X.S, X.c, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, X.kc + (int64_t)h2 * h2, Mbot,
+                         &F.tk0);
+      tpost += clock64() - tp;
+      X.flops += 2.0 * Lbot * Mbot;
+      F.state = 2;
+      SubFrame& C = stk[sp++];
+      C.f = km; C.h = h2; C.in = F.asmo; C.out = F.out; C.state = 0;
+    } else {
+      const int64_t kp = ret;
+      if (kp < F.km - h2 || kp > F.km) { *err = FL_E_GEOMETRY | 3; return 0; }
+      const long long tw = clock64();
+      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      twait += clock64() - tw;
+      --sp;
+    }
+  }
   if (X.prof && lane_id() == 0) {
-    const long long t6 = clock64();
+    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
     prof_add(X.prof, PROF_F_STAGE, t2 - t1);
-    prof_add(X.prof, PROF_F_MID, t4 - t3);
-    prof_add(X.prof, PROF_F_BOT, t6 - t5);
-    prof_add(X.prof, PROF_FUSE_CYC, t6 - t1);
+    prof_add(X.prof, PROF_F_MID, twait);
+    prof_add(X.prof, PROF_F_BOT, tpost);
+    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
     prof_add(X.prof, PROF_FUSE_N, 1);
   }
-  if (kp == NONE_SEEN || kp < km - h2 || kp > km) { *err = FL_E_GEOMETRY | 2; return 0; }
-  return kp;
+  return ret;
 }
 
 __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
@@ -224,18 +268,8 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     const int h = F.h;
     const int ph = (sp >= 2) ? stk[sp - 2].h : 0x7fffffff;
     if (F.state == 0) {
-      if (h <= PUT_LEAF) {
-        wait_conflicts(*X.S, X.c, U(F.in_org + F.f + 1), U(F.in_org + F.f + 2 * h + 1), 0, 0,
-                       U(F.out_org + F.f - h), U(F.out_org + F.f + h + 1));
-        ref_node_enter(X, h, ph);
-        const int64_t kb = put_leaf(X, P, F.in_org, F.out_org, X.pay_org, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
-        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
-        ret = kb;
-        --sp;
-        continue;
-      }
-      if (h <= FUSE_H) {
-        ret = put_fused_node(X, P, F.f, F.in_org, F.out_org, h, ph, err);
+      if (h <= PUT_HS) {
+        ret = put_subtree(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
         --sp;
         continue;
@@ -304,7 +338,6 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   double* kc = frames + 2 * n_rows + 64 * PUT_MAX_DEPTH;
   const Stencil st{P.cd, P.cm, P.cu, 2};
   build_kernel_table(kc, st, scratch);
-  load_kernel_smem(scratch + CHAIN_SCRATCH, kc);
   PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
   // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
   // loaded with an initial segment (cols init_col0 .. +init_len)

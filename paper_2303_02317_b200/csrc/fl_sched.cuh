@@ -33,37 +33,48 @@ namespace fl {
 
 // Warp layout (a warp's SM sub-partition, SMSP, is warp_id % 4):
 //   warps 0-3    big group (SMSP 0-3)
-//   warps 4-11   small workers (two per SMSP)
-//   warps 12-13  chain warps (SMSP 0, 1)
-//   warps 14-15  helper warps, one per chain (SMSP 2, 3): the chain's private
-//                co-processor for the direct correlations of its fused nodes,
-//                driven through a shared-memory mailbox (no ring, no deps scan)
+//   warps 4-9    small workers
+//   warps 10-11  chain warps (SMSP 2, 3)
+//   warps 12-15  helper warps, two per chain: the chain's private
+//                co-processors for the direct correlations of its shared-memory
+//                subtrees, fed through a request ring (no deps scan)
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
 constexpr int NCHAIN = 2;
-constexpr int SMALL_WORKERS = 8;
+constexpr int NHELP = 2;  // helper warps per chain
+constexpr int SMALL_WORKERS = 6;
 constexpr int BIG_WARPS = 4;
-constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + 2 * NCHAIN;
+constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + NCHAIN * (1 + NHELP);
 constexpr int BIG_THREADS = 32 * BIG_WARPS;
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
 enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_SMALL = 2, ROLE_HELPER = 3 };
 
 __device__ __forceinline__ int warp_role(int w, int* rank) {
-  if (w >= BIG_WARPS + SMALL_WORKERS + NCHAIN) { *rank = w - BIG_WARPS - SMALL_WORKERS - NCHAIN; return ROLE_HELPER; }
-  if (w >= BIG_WARPS + SMALL_WORKERS) { *rank = w - BIG_WARPS - SMALL_WORKERS; return ROLE_CHAIN; }
+  constexpr int C0 = BIG_WARPS + SMALL_WORKERS, H0 = C0 + NCHAIN;
+  if (w >= H0) { *rank = w - H0; return ROLE_HELPER; }  // helper rank: chain = rank / NHELP
+  if (w >= C0) { *rank = w - C0; return ROLE_CHAIN; }
   if (w < BIG_WARPS) { *rank = w; return ROLE_BIG; }
   *rank = w - BIG_WARPS;
   return ROLE_SMALL;
 }
 
-// Mailbox between chain warp c and its helper: one direct correlation
-// y[k] = sum_r w[r] x[k+r], k < Lout, at a time (seq > done while pending).
-struct Mailbox {
+// Request ring between chain warp c and its helpers: direct correlations
+// y[k] = sum_r w[r] x[k+r], k < Lout.  Requests posted together are
+// independent (the chain waits for a request's inputs before posting it), so
+// the helpers take them in posting order and finish them in any order; a
+// ticket t is complete when done[t % HQ] >= t.
+constexpr int HQ = 16;
+struct HReq {
   const double* x;
   double* y;
   const double* w;
   int Lout, M;
-  volatile int seq;   // last posted request (-1: exit)
-  volatile int done;  // last completed request
+};
+struct Mailbox {
+  HReq q[HQ];
+  volatile int done[HQ];
+  volatile int seq;  // last posted request
+  int claim;         // last claimed request
+  volatile int quit;
 };
 
 constexpr int NRINGS = 2;
@@ -75,6 +86,9 @@ constexpr int NRINGS = 2;
 #endif
 #ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to one warp
 #define FL_SMALL_MW 320
+#endif
+#ifndef FL_POST_FENCE  // 1: CTA fences around helper posts (0: in-order shared stores + compiler barrier)
+#define FL_POST_FENCE 1
 #endif
 #ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
 #define FL_IDLE_NS 512
@@ -170,29 +184,10 @@ __device__ void sched_init(SchedShared& S) {
   if (threadIdx.x < NCHAIN) {
     S.npend[threadIdx.x] = 0;
     S.mb[threadIdx.x].seq = 0;
-    S.mb[threadIdx.x].done = 0;
+    S.mb[threadIdx.x].claim = 0;
+    S.mb[threadIdx.x].quit = 0;
+    for (int k = 0; k < HQ; ++k) S.mb[threadIdx.x].done[k] = (k == 0) ? 0 : k - HQ;  // ticket t's slot predecessor t-HQ is done
   }
-}
-
-// Chain side of the mailbox (all lanes call): post a correlation, returns its ticket.
-__device__ __forceinline__ int helper_post(SchedShared& S, int c, const double* x, double* y, int Lout,
-                                           const double* w, int M) {
-  Mailbox& m = S.mb[c];
-  const int t = m.seq + 1;
-  __threadfence_block();  // every lane's writes to x (shared) ...
-  __syncwarp();           // ... are done before lane 0 publishes
-  if (threadIdx.x % 32 == 0) {
-    m.x = x; m.y = y; m.w = w; m.Lout = Lout; m.M = M;
-    __threadfence_block();
-    m.seq = t;
-  }
-  __syncwarp();
-  return t;
-}
-
-__device__ __forceinline__ void helper_wait(SchedShared& S, int c, int ticket) {
-  while (__shfl_sync(0xffffffffu, S.mb[c].done, 0) < ticket) __nanosleep(8);
-  __threadfence_block();
 }
 
 __device__ __forceinline__ bool overlap(uintptr_t a0, uintptr_t a1, uintptr_t b0, uintptr_t b1) {
@@ -202,6 +197,51 @@ __device__ __forceinline__ bool overlap(uintptr_t a0, uintptr_t a1, uintptr_t b0
 __device__ __forceinline__ bool task_done(const SchedShared& S, int id) {
   const int r = (int)((unsigned)id >> 28), idx = id & 0x0fffffff;
   return S.done[r][idx % QCAP] >= idx;
+}
+
+// Chain side of the request ring (all lanes call): post one correlation,
+// returns its ticket.
+__device__ __forceinline__ int helper_post1(SchedShared& S, int c, const double* x, double* y, int Lout,
+                                            const double* w, int M) {
+  Mailbox& m = S.mb[c];
+  const int t = m.seq + 1;
+  while (__shfl_sync(0xffffffffu, m.done[t % HQ], 0) < t - HQ) __nanosleep(16);  // slot still busy
+#if FL_POST_FENCE
+  __threadfence_block();  // every lane's writes to x (shared) ...
+#endif
+  __syncwarp();           // ... are done before lane 0 publishes
+  if (threadIdx.x % 32 == 0) {
+    HReq& r = m.q[t % HQ];
+    r.x = x; r.y = y; r.w = w; r.Lout = Lout; r.M = M;
+#if FL_POST_FENCE
+    __threadfence_block();
+#else
+    asm volatile("" ::: "memory");  // shared-memory stores of one warp are performed in order
+#endif
+    m.seq = t;
+  }
+  __syncwarp();
+  return t;
+}
+
+constexpr int HCHUNK = 64;  // outputs per helper request (large correlations are split)
+
+// Post a correlation as chunks of HCHUNK outputs; returns the last ticket
+// (its tickets are last-nchunks+1 .. last; see helper_wait_range).
+__device__ __forceinline__ int helper_post(SchedShared& S, int c, const double* x, double* y, int Lout,
+                                           const double* w, int M, int* first) {
+  int t = 0;
+  *first = S.mb[c].seq + 1;
+  for (int k0 = 0; k0 < Lout; k0 += HCHUNK)
+    t = helper_post1(S, c, x + k0, y + k0, (Lout - k0 < HCHUNK) ? Lout - k0 : HCHUNK, w, M);
+  if (Lout <= 0) t = *first - 1;
+  return t;
+}
+
+__device__ __forceinline__ void helper_wait_range(SchedShared& S, int c, int first, int last) {
+  for (int t = first; t <= last; ++t)
+    while (__shfl_sync(0xffffffffu, S.mb[c].done[t % HQ], 0) < t) __nanosleep(8);
+  __threadfence_block();
 }
 
 // All lanes of the calling warp spin (warp-uniform, keeps the warp converged).
@@ -417,13 +457,31 @@ __device__ double warp_conv_direct(const double* __restrict__ x, double* __restr
 
 // Stage n doubles from global into warp-owned shared memory (all loads in
 // flight), zero-filling up to n_total (warp_conv_direct reads 3 past its window).
-__device__ __forceinline__ void warp_stage(double* dst, const double* src, int n, int n_total = -1) {
+// Loads are batched 8 per lane into registers before the stores, so a stage of
+// up to 256 values costs one memory round trip (a load / store interleave
+// would serialise on possible aliasing).
+template <int NB>
+__device__ __forceinline__ void warp_stage_nb(double* __restrict__ dst, const double* __restrict__ src, int n,
+                                              int n_total) {
   if (n_total < n) n_total = n;
-  for (int base = 0; base < n_total; base += 32) {
-    const int i = base + lane_id();
-    if (i < n_total) dst[i] = (i < n) ? src[i] : 0.0;
+  const int lane = lane_id();
+  for (int base = 0; base < n_total; base += 32 * NB) {
+    double v[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int i = base + 32 * k + lane;
+      v[k] = (i < n) ? src[i] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int i = base + 32 * k + lane;
+      if (i < n_total) dst[i] = v[k];
+    }
   }
   __syncwarp();
+}
+__device__ __forceinline__ void warp_stage(double* dst, const double* src, int n, int n_total = -1) {
+  warp_stage_nb<8>(dst, src, n, n_total);
 }
 
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
@@ -512,18 +570,8 @@ __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logN
 //                          const double2* tq, const Grp& g) const;
 //       execute one task (pricer-specific kinds, else exec_generic)
 
-constexpr int CHAIN_SCRATCH = 544;  // doubles of shared-memory scratch per chain warp
-// followed by the chain's copy of the composed weights W_1..W_KSMEM_M (slot m at m*m)
-constexpr int KSMEM_M = 32;
-constexpr int KSMEM_DOUBLES = ((KSMEM_M + 1) * (KSMEM_M + 1) + 1) & ~1;
-constexpr int CHAIN_SMEM = CHAIN_SCRATCH + KSMEM_DOUBLES;
-
-// Copy W_1..W_KSMEM_M of a kernel table (global, slot m at kc + m*m) into the
-// chain's shared copy (all lanes of the chain warp call).
-__device__ __forceinline__ void load_kernel_smem(double* dst, const double* kc) {
-  for (int i = lane_id(); i < (KSMEM_M + 1) * (KSMEM_M + 1); i += 32) dst[i] = kc[i];
-  __syncwarp();
-}
+constexpr int CHAIN_SCRATCH = 1200;  // doubles of shared-memory scratch per chain warp
+constexpr int CHAIN_SMEM = CHAIN_SCRATCH;
 
 __host__ __device__ constexpr int sched_smem_bytes() {
   return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SMEM) * (int)sizeof(double) +
@@ -549,29 +597,31 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   int rank = 0;
   const int role = warp_role(threadIdx.x >> 5, &rank);
   if (role == ROLE_HELPER) {
-    // ---- helper warp of chain `rank`: direct correlations posted via the mailbox
-    Mailbox& m = S.mb[rank];
+    // ---- helper warp of chain rank / NHELP: correlations from its request ring
+    Mailbox& m = S.mb[rank / NHELP];
     double flops = 0.0;
-    int last = 0;
     for (;;) {
-      int sq;
+      int t = 0;
+      if (lane_id() == 0) t = atomicAdd(&m.claim, 1) + 1;
+      t = __shfl_sync(FULL, t, 0);
       unsigned ns = 8;
-      while ((sq = __shfl_sync(FULL, m.seq, 0)) == last) {
+      bool quit = false;
+      while (__shfl_sync(FULL, m.seq, 0) < t) {
+        if (__shfl_sync(FULL, m.quit, 0)) { quit = true; break; }
         __nanosleep(ns);
         ns = ns < FL_HELPER_NS ? 2 * ns : ns;
       }
-      if (sq < 0) break;
+      if (quit) break;
       __threadfence_block();
-      const volatile Mailbox& vm = m;
-      const double* x = vm.x;
-      double* y = vm.y;
-      const double* w = vm.w;
-      const int Lout = vm.Lout, M = vm.M;
+      const volatile HReq& r = m.q[t % HQ];
+      const double* x = r.x;
+      double* y = r.y;
+      const double* w = r.w;
+      const int Lout = r.Lout, M = r.M;
       flops += warp_conv_direct(x, y, Lout, w, M);
       __threadfence_block();
       __syncwarp();
-      if (lane_id() == 0) m.done = sq;
-      last = sq;
+      if (lane_id() == 0) m.done[t % HQ] = t;
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     return;
@@ -588,9 +638,9 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       if (w >= nwork) break;
       pr.chain(S, c, w, arena, chain_scratch + c * CHAIN_SMEM, &chain_flops);
     }
-    if (lane_id() == 0) {  // release this chain's helper
+    if (lane_id() == 0) {  // release this chain's helper (all its requests were waited for)
       __threadfence_block();
-      S.mb[c].seq = -1;
+      S.mb[c].quit = 1;
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)chain_flops);
     int last = 0;
