@@ -28,12 +28,12 @@ constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per big-group thread
 constexpr int CSUB_IN = 0, CSUB_ASM0 = CALL_HS + 8, CSUB_ASM1 = CSUB_ASM0 + CALL_HS + 8;
 static_assert(CSUB_ASM1 + CALL_HS / 2 + 8 <= CHAIN_SCRATCH, "call subtree scratch");
 static_assert(CALL_HS <= 4 * CALL_LEAF, "two asm levels cover a subtree");
-static_assert(CALL_HS / 2 <= DIRECT_H, "subtree correlations use the direct kernel table");
+static_assert(CALL_HS / 2 <= KT_H, "subtree correlations use the kernel table");
 
 enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
 
 __host__ __device__ inline int64_t call_arena_doubles(int64_t row_len, int64_t h_max) {
-  return 2 * (row_len + 8) + (2 * h_max + 16 * CALL_MAX_DEPTH) + KTABLE_DOUBLES + 64;
+  return 2 * (row_len + 8) + 2 * (2 * h_max + 16 * CALL_MAX_DEPTH) + KTABLE_DOUBLES + 64;
 }
 int64_t call_ws_doubles(int64_t n_max) { return call_arena_doubles(n_max, n_max); }
 
@@ -109,7 +109,9 @@ struct CallChainCtx {
   int c;
   Stencil st;
   const double* kc;
-  double* frames;
+  double* frames;   // two copies of the frame arena, alternated per depth (see fl_put.cu)
+  int64_t fstride;
+  uint32_t tog;
   double* scratch;
   int64_t ref_cut;
   double flops, ref_flops;
@@ -248,7 +250,9 @@ __device__ int64_t call_solve(CallChainCtx& X, const CallParams& P, int64_t i0, 
         continue;
       }
       call_ref_enter(X, h, ph);
-      F.asm_org = X.frames + F.arena - lo;
+      const int d = sp - 1;
+      X.tog ^= 1u << d;
+      F.asm_org = X.frames + (((X.tog >> d) & 1u) ? X.fstride : 0) + F.arena - lo;
       // mid: cols lo .. j-h1 of row i-h1
       call_conv(X, F.in_org + lo, h, F.asm_org + lo, h2, h1);
       F.state = 1;
@@ -290,10 +294,11 @@ __device__ void call_record(const BatchOut& out, int o, int32_t& cnt, int64_t t,
 __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams& P, int64_t row_len, int64_t h_max,
                                          double* arena, double* scratch, unsigned long long* prof) {
   double* frames = arena + 2 * (row_len + 8);
-  double* kc = frames + 2 * h_max + 16 * CALL_MAX_DEPTH;
+  const int64_t fstride = 2 * h_max + 16 * CALL_MAX_DEPTH;
+  double* kc = frames + 2 * fstride;
   const Stencil st{P.wd, P.wu, 0.0, 1};
   build_kernel_table(kc, st, scratch);
-  return CallChainCtx{&S, c, st, kc, frames, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+  return CallChainCtx{&S, c, st, kc, frames, fstride, 0u, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
 }
 
 // The trapezoid loop from row i / boundary j down to the residual (american.py:486-498).
@@ -307,7 +312,7 @@ __device__ void call_trapezoids(CallChainCtx& X, const CallParams& P, int64_t& i
     const int64_t L = j - first + 1;
     if (L > hh) {
       X.ref_flops += call_ref_jump(L, hh + 1);
-      call_conv(X, cur_org + first, L, nxt_org + first, L - hh, h);
+      chain_conv(*X.S, X.c, X.st, cur_org + first, L, nxt_org + first, L - hh, h, X.kc, X.prof, true);
     }
     const int64_t jp = call_solve(X, P, i, j, h, cur_org, nxt_org, err);
     if (*err) return;

@@ -40,22 +40,25 @@ namespace fl {
 constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
 #ifndef FL_PUT_HS
-#define FL_PUT_HS 128
+#define FL_PUT_HS 256
 #endif
 // recursion subtrees of height <= PUT_HS run whole in the chain's shared memory
 constexpr int PUT_HS = FL_PUT_HS;
 constexpr int PUT_MARGIN = 2 * PUT_HS + 32;  // columns below the lowest boundary kept in the stage buffers
 constexpr int PUT_MAX_DEPTH = 24;
-// shared layout of a subtree: payoff (4 HS + 2) | input row (2 HS) | asm level 0 (2 HS) | asm level 1 (HS)
+// shared layout of a subtree: payoff (4 HS + 2) | input row (2 HS) | assembled rows of depth
+// 0, 1, 2 (2 HS, HS, HS / 2)
 constexpr int SUB_PAY = 0;
 constexpr int SUB_IN = SUB_PAY + 4 * PUT_HS + 8;
 constexpr int SUB_ASM0 = SUB_IN + 2 * PUT_HS + 8;
 constexpr int SUB_ASM1 = SUB_ASM0 + 2 * PUT_HS + 8;
-constexpr int SUB_END = SUB_ASM1 + PUT_HS + 8;
+constexpr int SUB_ASM2 = SUB_ASM1 + PUT_HS + 8;
+constexpr int SUB_END = SUB_ASM2 + PUT_HS / 2 + 8;
+constexpr int SUB_DEPTH = 5;
 static_assert(SUB_END <= CHAIN_SCRATCH, "subtree scratch");
-static_assert(PUT_HS <= 4 * PUT_LEAF, "two asm levels cover a subtree");
-static_assert(PUT_HS / 2 <= DIRECT_H, "subtree correlations use the direct kernel table");
-static_assert(2 * (2 * DIRECT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
+static_assert(PUT_HS <= 8 * PUT_LEAF, "three asm levels cover a subtree");
+static_assert(PUT_HS / 2 <= KT_H, "subtree correlations use the kernel table");
+static_assert(2 * (2 * KT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
 enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD = TK_USER + 2 };
 
@@ -103,7 +106,7 @@ __host__ __device__ inline PutLayout put_trap_layout(int64_t f, int64_t W, int64
 }
 
 __host__ __device__ inline int64_t put_arena_doubles(int64_t span, int64_t n_rows) {
-  return 3 * span + (2 * n_rows + 64 * PUT_MAX_DEPTH) + KTABLE_DOUBLES + 64;
+  return 3 * span + 2 * (2 * n_rows + 64 * PUT_MAX_DEPTH) + KTABLE_DOUBLES + 64;
 }
 
 // doubles needed per chain for a batch whose options have at most these sizes
@@ -117,7 +120,10 @@ struct PutChainCtx {
   int c;
   Stencil st;
   const double* kc;  // composed weights W_1..W_DIRECT_H (slot m at kc + m*m)
-  double* frames;
+  double* frames;     // two copies of the recursion-frame arena (frames, frames + fstride) ...
+  int64_t fstride;
+  uint32_t tog;       // ... alternated per depth, so consecutive nodes of one depth never
+                      // share assembled-row memory (no false WAR dependencies between them)
   const double* pay_org;
   double* scratch;   // chain's shared scratch (CHAIN_SCRATCH doubles)
   int64_t ref_cut;   // the reference's base_cutoff (work accounting only)
@@ -179,11 +185,11 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   double* s_in = X.scratch + SUB_IN;
   const int64_t plo = f0 - 2 * (int64_t)h0 - 1;
   warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
-  warp_stage_nb<(4 * PUT_HS + 2 + 31) / 32>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+  warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
   const double* pay_s = s_pay - plo;
   const long long t2 = clock64();
   long long twait = 0, tpost = 0;
-  SubFrame stk[4];
+  SubFrame stk[SUB_DEPTH];
   stk[0].f = f0; stk[0].h = h0; stk[0].in = s_in - (f0 + 1); stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
@@ -200,7 +206,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
         --sp;
         continue;
       }
-      F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : SUB_ASM1) - (F.f - h1 + 1);
+      F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : sp == 2 ? SUB_ASM1 : SUB_ASM2) - (F.f - h1 + 1);
       // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
       const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
       const long long tp = clock64();
@@ -276,7 +282,9 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
       }
       ref_node_enter(X, h, ph);
       const int h1 = (h + 1) / 2;
-      F.asm_org = X.frames + F.arena - (F.f - h1 + 1);
+      const int d = sp - 1;
+      X.tog ^= 1u << d;
+      F.asm_org = X.frames + (((X.tog >> d) & 1u) ? X.fstride : 0) + F.arena - (F.f - h1 + 1);
       // mid: cols f+h1+1 .. f+2h-h1 of row t+h1 from the 2h inputs
       put_conv(X, F.in_org + F.f + 1, 2 * (int64_t)h, F.asm_org + F.f + h1 + 1, 2 * (int64_t)(h - h1), h1);
       F.state = 1;
@@ -315,7 +323,7 @@ __device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int6
   const int h = (int)hh;
   if (red > 2 * hh) {  // far: cols f+h+1 .. f+red-h stay linear
     X.ref_flops += ref_jump_flops(red, 2 * hh + 1);
-    put_conv(X, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h);
+    chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc, X.prof, true);
   }
   return put_solve_q(X, P, f, cur_org, nxt_org, h, err);
 }
@@ -335,10 +343,11 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   double* bufA = arena;
   double* pay = arena + 2 * Lo.span;
   double* frames = arena + 3 * Lo.span;
-  double* kc = frames + 2 * n_rows + 64 * PUT_MAX_DEPTH;
+  const int64_t fstride = 2 * n_rows + 64 * PUT_MAX_DEPTH;
+  double* kc = frames + 2 * fstride;
   const Stencil st{P.cd, P.cm, P.cu, 2};
   build_kernel_table(kc, st, scratch);
-  PutChainCtx X{&S, c, st, kc, frames, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+  PutChainCtx X{&S, c, st, kc, frames, fstride, 0u, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
   // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
   // loaded with an initial segment (cols init_col0 .. +init_len)
   Task t;

@@ -40,8 +40,8 @@ namespace fl {
 //                subtrees, fed through a request ring (no deps scan)
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
 constexpr int NCHAIN = 2;
-constexpr int NHELP = 2;  // helper warps per chain
-constexpr int SMALL_WORKERS = 6;
+constexpr int NHELP = 4;  // helper warps per chain
+constexpr int SMALL_WORKERS = 2;
 constexpr int BIG_WARPS = 4;
 constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + NCHAIN * (1 + NHELP);
 constexpr int BIG_THREADS = 32 * BIG_WARPS;
@@ -77,7 +77,7 @@ struct Mailbox {
   volatile int quit;
 };
 
-constexpr int NRINGS = 2;
+constexpr int NRINGS = 3;
 #ifndef FL_QCAP
 #define FL_QCAP 64
 #endif
@@ -98,7 +98,12 @@ constexpr int NRINGS = 2;
 #endif
 constexpr int QCAP = FL_QCAP;  // per ring
 constexpr int BIG_BAR = 1;
-constexpr int DIRECT_H = FL_DIRECT_H;
+constexpr int DIRECT_H = FL_DIRECT_H;  // direct-correlation TASKS for kernels up to this height
+#ifndef FL_KT_H  // composed weights W_1..W_KT_H are tabulated per option (subtree correlations)
+#define FL_KT_H 128
+#endif
+constexpr int KT_H = FL_KT_H;
+static_assert(KT_H >= DIRECT_H, "direct tasks read the table");
 constexpr int BIG_LOGN = 13;    // big-group FFT blocks <= 8192 real points
 constexpr int SMALL_LOGN = 10;  // small-worker FFT blocks <= 1024 real points
 constexpr int BIG_SLOTS = smem_complex_slots(1 << (BIG_LOGN - 1));
@@ -112,7 +117,11 @@ enum : int {
   TK_USER = 8,  // pricer-specific tasks start here
 };
 
-enum : int { RING_SMALL = 0, RING_BIG = 1 };
+// RING_LOW: big-group tasks with lots of slack (the stage-level far / left
+// jumps), split into chunks and taken only when RING_BIG is empty, so the
+// latency-critical mid / bottom jumps never queue behind them.
+enum : int { RING_SMALL = 0, RING_BIG = 1, RING_LOW = 2 };
+constexpr int64_t LOW_CHUNK = 8192;  // outputs per RING_LOW task
 
 struct Task {
   const double* x;
@@ -164,6 +173,9 @@ enum : int {
   // detail (chain side)
   PROF_ISS_SCAN, PROF_ISS_STALL, PROF_ISS_SLOT, PROF_F_STAGE, PROF_F_MID, PROF_F_BOT, PROF_STRIP_LOOP,
   PROF_LEAF_LOAD,
+  // conflict waits by cause: read-after-write / write-after-read-or-write, small / big ring
+  PROF_W_RAW_S, PROF_W_RAW_B, PROF_W_WAR_S, PROF_W_WAR_B, PROF_W_N, PROF_W_SUML, PROF_W_SUMH, PROF_W_FFT,
+  PROF_W_MAXL,
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
@@ -253,27 +265,31 @@ __device__ __forceinline__ void warp_wait_done(const SchedShared& S, int id) {
 // The chain's unfinished tasks conflicting with the given ranges, in issue
 // order, into out[0..min(n,cap)); returns n.
 __device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
-                              uintptr_t w0, uintptr_t w1, int* out, int cap) {
+                              uintptr_t w0, uintptr_t w1, int* out, int cap, int* rawf = nullptr) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
   int n = 0;
   for (int base = first; base < np; base += 32) {  // warp-uniform trip count
     const int i = base + lane_id();
-    bool hit = false;
+    bool hit = false, raw = false;
     int id = 0;
     if (i < np) {
       const Pend& p = S.pend[c][i % PEND_CAP];
       id = p.id;
-      const bool raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
+      raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
       const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
       hit = (raw || war) && !task_done(S, id);
     }
     unsigned m = __ballot_sync(FULL, hit);
+    const unsigned rm = __ballot_sync(FULL, raw);
     while (m) {
       const int l = __ffs(m) - 1;
       m &= m - 1;
       const int v = __shfl_sync(FULL, id, l);
-      if (n < cap) out[n] = v;
+      if (n < cap) {
+        out[n] = v;
+        if (rawf) rawf[n] = (rm >> l) & 1;
+      }
       ++n;
     }
   }
@@ -284,12 +300,37 @@ __device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr
 // about to read (r0/r1, r2/r3) and write (w0/w1).
 __device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                                uintptr_t w0, uintptr_t w1) {
-  int ids[8];
+  int ids[8], rawf[8];
   for (;;) {
-    const int n = scan_conflicts(S, c, r0, r1, r2, r3, w0, w1, ids, 8);
+    const int n = scan_conflicts(S, c, r0, r1, r2, r3, w0, w1, ids, 8, rawf);
     if (n == 0) break;
     const int m = n < 8 ? n : 8;
-    for (int i = 0; i < m; ++i) warp_wait_done(S, ids[i]);
+    for (int i = 0; i < m; ++i) {
+      const long long t0 = S.prof ? clock64() : 0;
+      if (S.prof && lane_id() == 0 && rawf[i]) {
+        const int rg = (int)((unsigned)ids[i] >> 28), ix = ids[i] & 0x0fffffff;
+        const Task& tk = S.ring[rg][ix % QCAP];
+        prof_add(S.prof, PROF_W_SUML, (unsigned long long)tk.L);
+        prof_add(S.prof, PROF_W_SUMH, (unsigned long long)tk.h);
+        prof_add(S.prof, PROF_W_FFT, tk.kind == TK_FFT ? 1ull : 0ull);
+        if ((unsigned long long)tk.L > S.prof[PROF_W_MAXL]) {  // debug: describe the longest waited task
+          S.prof[PROF_W_MAXL] = tk.L;
+          S.prof[PROF_W_MAXL + 1] = tk.Lout;
+          S.prof[PROF_W_MAXL + 2] = tk.h;
+          S.prof[PROF_W_MAXL + 3] = (unsigned long long)(tk.y - tk.x);
+        }
+        // histogram of waited-task h: slots +4 .. +8 for h <= 64, 128, 256, 512, larger
+        const int hb = tk.h <= 64 ? 0 : tk.h <= 128 ? 1 : tk.h <= 256 ? 2 : tk.h <= 512 ? 3 : 4;
+        prof_add(S.prof, PROF_W_MAXL + 4 + hb, 1);
+        prof_add(S.prof, PROF_W_MAXL + 9 + hb, (unsigned long long)tk.L);
+      }
+      warp_wait_done(S, ids[i]);
+      if (S.prof && lane_id() == 0) {
+        const int big = ((unsigned)ids[i] >> 28) == RING_BIG;
+        prof_add(S.prof, (rawf[i] ? PROF_W_RAW_S : PROF_W_WAR_S) + big, clock64() - t0);
+        prof_add(S.prof, PROF_W_N, 1);
+      }
+    }
     if (n <= 8) break;
   }
   __syncwarp();
@@ -366,26 +407,26 @@ __device__ __forceinline__ int fft_ring(const Stencil& st, int h) {
 // the one-step stencil -- all terms nonnegative, ~m ulp relative accuracy
 // (tighter than the reference's FFT power).
 
-constexpr int64_t KTABLE_DOUBLES = (int64_t)(DIRECT_H + 2) * (DIRECT_H + 2) * 2;
+constexpr int64_t KTABLE_DOUBLES = (int64_t)(KT_H + 2) * (KT_H + 2) * 2;
 
 // scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
 __device__ void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
   const int lane = lane_id();
   const int span = st.span;
   double* a = scratch;
-  double* b = scratch + (2 * DIRECT_H + 2);
-  for (int base = 0; base < 2 * DIRECT_H + 2; base += 32) {
+  double* b = scratch + (2 * KT_H + 2);
+  for (int base = 0; base < 2 * KT_H + 2; base += 32) {
     const int i = base + lane;
-    if (i < 2 * DIRECT_H + 2) a[i] = (i == 0) ? st.c0 : (i == 1) ? st.c1 : (i == 2 && span == 2) ? st.c2 : 0.0;
+    if (i < 2 * KT_H + 2) a[i] = (i == 0) ? st.c0 : (i == 1) ? st.c1 : (i == 2 && span == 2) ? st.c2 : 0.0;
   }
   __syncwarp();
-  for (int m = 1; m <= DIRECT_H; ++m) {
+  for (int m = 1; m <= KT_H; ++m) {
     const int M = m * span + 1;
     for (int base = 0; base < M; base += 32) {  // store W_m
       const int r = base + lane;
       if (r < M) kc[m * m + r] = a[r];
     }
-    if (m == DIRECT_H) break;
+    if (m == KT_H) break;
     const int M2 = M + span;
     for (int base = 0; base < M2; base += 32) {  // W_{m+1}[r] = sum_t c_t W_m[r-t]
       const int r = base + lane;
@@ -487,7 +528,7 @@ __device__ __forceinline__ void warp_stage(double* dst, const double* src, int n
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
 // or an FFT task, on the small or big ring.
 __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
-                           int64_t Lout, int h, const double* kc, unsigned long long* prof) {
+                           int64_t Lout, int h, const double* kc, unsigned long long* prof, bool low = false) {
   if (Lout <= 0) return;
   Task t;
   t.c0 = st.c0; t.c1 = st.c1; t.c2 = st.c2; t.span = st.span; t.h = h;
@@ -502,7 +543,17 @@ __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const doubl
   } else {
     t.kind = TK_FFT;
     t.w = nullptr;
-    issue(S, c, fft_ring(st, h), t, U(x), U(x + L), U(y), U(y + Lout));
+    const int ring = fft_ring(st, h);
+    if (low && ring == RING_BIG) {
+      const int64_t span = L - Lout;  // taps - 1
+      for (int64_t k0 = 0; k0 < Lout; k0 += LOW_CHUNK) {
+        const int64_t n = (Lout - k0 < LOW_CHUNK) ? Lout - k0 : LOW_CHUNK;
+        t.x = x + k0; t.L = n + span; t.y = y + k0; t.Lout = n;
+        issue(S, c, RING_LOW, t, U(t.x), U(t.x + t.L), U(t.y), U(t.y + n));
+      }
+    } else {
+      issue(S, c, ring, t, U(x), U(x + L), U(y), U(y + Lout));
+    }
   }
   if (prof && lane_id() == 0) prof_add(prof, PROF_ISS_CYC, clock64() - t0);
 }
@@ -570,7 +621,7 @@ __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logN
 //                          const double2* tq, const Grp& g) const;
 //       execute one task (pricer-specific kinds, else exec_generic)
 
-constexpr int CHAIN_SCRATCH = 1200;  // doubles of shared-memory scratch per chain warp
+constexpr int CHAIN_SCRATCH = 2480;  // doubles of shared-memory scratch per chain warp
 constexpr int CHAIN_SMEM = CHAIN_SCRATCH;
 
 __host__ __device__ constexpr int sched_smem_bytes() {
@@ -589,7 +640,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SMEM);  // quarter-wave twiddles
   double2* bigbuf = tq + TWQ;              // big-group FFT buffer
   double2* smallbuf = bigbuf + BIG_SLOTS;  // SMALL_WORKERS x SMALL_SLOTS
-  __shared__ int s_idx;
+  __shared__ int s_idx, s_ring;
   for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
   sched_init(S);
   if (threadIdx.x == 0) S.prof = prof;
@@ -666,15 +717,27 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     for (;;) {
       const long long t0 = clock64();
       if (rank == 0) {
-        int idx = 0;
-        if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_BIG], 1);
-        idx = __shfl_sync(FULL, idx, 0);
-        worker_wait_ready(S, RING_BIG, idx);
-        if (lane_id() == 0) s_idx = idx;
+        // the big group is the only consumer of RING_BIG / RING_LOW: claim the
+        // oldest urgent task, else the oldest low-priority one
+        int ring = -1, idx = 0;
+        unsigned ns = 16;
+        for (;;) {
+          int r = -1, i = 0;
+          if (lane_id() == 0) {
+            if (S.claim[RING_BIG] < *(volatile int*)&S.reserve[RING_BIG]) { r = RING_BIG; i = S.claim[RING_BIG]++; }
+            else if (S.claim[RING_LOW] < *(volatile int*)&S.reserve[RING_LOW]) { r = RING_LOW; i = S.claim[RING_LOW]++; }
+          }
+          r = __shfl_sync(FULL, r, 0);
+          if (r >= 0) { ring = r; idx = __shfl_sync(FULL, i, 0); break; }
+          __nanosleep(ns);
+          ns = ns < FL_IDLE_NS ? 2 * ns : ns;
+        }
+        worker_wait_ready(S, ring, idx);
+        if (lane_id() == 0) { s_idx = idx; s_ring = ring; }
       }
       gsync(g);
-      const int idx = s_idx;
-      const Task t = load_task(S.ring[RING_BIG][idx % QCAP]);
+      const int idx = s_idx, bring = s_ring;
+      const Task t = load_task(S.ring[bring][idx % QCAP]);
       const long long t1 = clock64();
       if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
       if (t.kind == TK_EXIT) break;
@@ -682,7 +745,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       flops += fl > 0 ? fl : 0.0;
       gsync(g);
       if (g.t == 0) {
-        publish_done(S, RING_BIG, idx);
+        publish_done(S, bring, idx);
         prof_add(prof, PROF_BIG_CYC, clock64() - t1);
         prof_add(prof, PROF_BIG_N, 1);
       }

@@ -16,7 +16,7 @@ p = db.profile().astype(np.float64)
 names = ["FFT_CYC", "FFT_N", "DIR_CYC", "DIR_N", "OTHER_CYC", "OTHER_N", "BIG_CYC", "BIG_N",
          "STRIP_CYC", "STRIP_ROWS", "WAIT_CYC", "FUSE_CYC", "FUSE_N", "KERNEL_CYC", "IDLE_CYC",
          "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC", "ISS_SCAN", "ISS_STALL", "ISS_SLOT", "F_STAGE", "F_MID",
-         "F_BOT", "STRIP_LOOP", "LEAF_LOAD"]
+         "F_BOT", "STRIP_LOOP", "LEAF_LOAD", "W_RAW_S", "W_RAW_B", "W_WAR_S", "W_WAR_B", "W_N", "W_SUML", "W_SUMH", "W_FFT", "W_MAXL", "MAX_LOUT", "MAX_H", "MAX_YX", "HB64", "HB128", "HB256", "HB512", "HBBIG", "LB64", "LB128", "LB256", "LB512", "LBBIG"]
 P = dict(zip(names, p[:len(names)]))
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
 for nm in names:
@@ -37,4 +37,6 @@ print("fused per node: stage %.0f mid %.0f bottom %.0f" % (d(P["F_STAGE"], P["FU
                                                           d(P["F_BOT"], P["FUSE_N"])))
 print("strip: loop %.1f cyc/row, load %.0f cyc/leaf (leaves/option %.0f)" % (
     d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"] / 28.0), P["STRIP_ROWS"] / 28.0 / nopt))
+print("conflict waits per option: RAW small %.3g big %.3g, WAR small %.3g big %.3g (n=%.0f)" % (
+    P["W_RAW_S"] / nopt, P["W_RAW_B"] / nopt, P["W_WAR_S"] / nopt, P["W_WAR_B"] / nopt, P["W_N"] / nopt))
 print("status nonzero:", int(np.sum(r.status != 0)))
