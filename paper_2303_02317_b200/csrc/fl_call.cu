@@ -44,10 +44,10 @@ __device__ __forceinline__ int64_t first_green_rec(int64_t i, int64_t j) {  // a
 // reference-algorithmic cost model; the reference strip's cell
 // count depends on the boundary path, estimated as 3/4 h^2 for h rows of width h
 __device__ __forceinline__ double call_ref_jump(int64_t L, int64_t M) {
-  int64_t N = 1;
-  int lg = 0;
-  while (N < L + M - 1) { N <<= 1; ++lg; }
-  return 5.0 * (double)N * (double)lg + 6.0 * (double)(N / 2 + 1);
+  const uint64_t need = (uint64_t)(L + M - 1);
+  const int lg = need <= 1 ? 0 : 64 - __clzll((long long)(need - 1));
+  const double N = (double)(1ull << lg);
+  return 5.0 * N * (double)lg + 6.0 * (N * 0.5 + 1.0);
 }
 
 // Leaf strip (binomial_strip_sweep with lo = j-h+1, height h <= 32) on the

@@ -64,10 +64,10 @@ enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD =
 
 // reference-algorithmic cost model
 __device__ __forceinline__ double ref_jump_flops(int64_t L, int64_t M) {
-  int64_t N = 1;
-  int lg = 0;
-  while (N < L + M - 1) { N <<= 1; ++lg; }
-  return 5.0 * (double)N * (double)lg + 6.0 * (double)(N / 2 + 1);
+  const uint64_t need = (uint64_t)(L + M - 1);
+  const int lg = need <= 1 ? 0 : 64 - __clzll((long long)(need - 1));  // N = next_pow2(L+M-1) = 2^lg
+  const double N = (double)(1ull << lg);
+  return 5.0 * N * (double)lg + 6.0 * (N * 0.5 + 1.0);
 }
 // projected cells of a reference strip of width W swept `rows` times (shrinking cone)
 __device__ __forceinline__ double ref_strip_flops(int64_t W, int64_t rows) {

@@ -32,29 +32,34 @@
 namespace fl {
 
 // Warp layout (a warp's SM sub-partition, SMSP, is warp_id % 4):
-//   warps 0-3    big group (SMSP 0-3)
-//   warps 4-9    small workers
-//   warps 10-11  chain warps (SMSP 2, 3)
-//   warps 12-15  helper warps, two per chain: the chain's private
+//   warps 0-3    big FFT group: 8192-point blocks, consumes RING_BIG, then RING_LOW
+//   warps 4-7    medium FFT group: 2048-point blocks, consumes RING_SMALL
+//   warps 8-9    chain warps
+//   warps 10-15  helper warps, three per chain: the chain's private
 //                co-processors for the direct correlations of its shared-memory
 //                subtrees, fed through a request ring (no deps scan)
+// Groups execute one task at a time over 128 threads (named barriers 1, 2).
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
+#ifndef FL_NHELP
+#define FL_NHELP 3
+#endif
 constexpr int NCHAIN = 2;
-constexpr int NHELP = 4;  // helper warps per chain
-constexpr int SMALL_WORKERS = 2;
-constexpr int BIG_WARPS = 4;
-constexpr int SCHED_WARPS = BIG_WARPS + SMALL_WORKERS + NCHAIN * (1 + NHELP);
-constexpr int BIG_THREADS = 32 * BIG_WARPS;
+constexpr int NHELP = FL_NHELP;  // helper warps per chain
+constexpr int GROUP_WARPS = 4;
+constexpr int GROUP_THREADS = 32 * GROUP_WARPS;
+constexpr int BIG_WARPS = GROUP_WARPS;
+constexpr int BIG_THREADS = GROUP_THREADS;
+constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP);
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
-enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_SMALL = 2, ROLE_HELPER = 3 };
+enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3 };
 
 __device__ __forceinline__ int warp_role(int w, int* rank) {
-  constexpr int C0 = BIG_WARPS + SMALL_WORKERS, H0 = C0 + NCHAIN;
+  constexpr int C0 = 2 * GROUP_WARPS, H0 = C0 + NCHAIN;
   if (w >= H0) { *rank = w - H0; return ROLE_HELPER; }  // helper rank: chain = rank / NHELP
   if (w >= C0) { *rank = w - C0; return ROLE_CHAIN; }
-  if (w < BIG_WARPS) { *rank = w; return ROLE_BIG; }
-  *rank = w - BIG_WARPS;
-  return ROLE_SMALL;
+  if (w < GROUP_WARPS) { *rank = w; return ROLE_BIG; }
+  *rank = w - GROUP_WARPS;
+  return ROLE_MED;
 }
 
 // Request ring between chain warp c and its helpers: direct correlations
@@ -84,8 +89,8 @@ constexpr int NRINGS = 3;
 #ifndef FL_DIRECT_H  // kernels with h <= FL_DIRECT_H use direct dot products
 #define FL_DIRECT_H 64
 #endif
-#ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to one warp
-#define FL_SMALL_MW 320
+#ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to the medium group
+#define FL_SMALL_MW 600
 #endif
 #ifndef FL_POST_FENCE  // 1: CTA fences around helper posts (0: in-order shared stores + compiler barrier)
 #define FL_POST_FENCE 1
@@ -98,6 +103,7 @@ constexpr int NRINGS = 3;
 #endif
 constexpr int QCAP = FL_QCAP;  // per ring
 constexpr int BIG_BAR = 1;
+constexpr int MED_BAR = 2;
 constexpr int DIRECT_H = FL_DIRECT_H;  // direct-correlation TASKS for kernels up to this height
 #ifndef FL_KT_H  // composed weights W_1..W_KT_H are tabulated per option (subtree correlations)
 #define FL_KT_H 128
@@ -105,7 +111,7 @@ constexpr int DIRECT_H = FL_DIRECT_H;  // direct-correlation TASKS for kernels u
 constexpr int KT_H = FL_KT_H;
 static_assert(KT_H >= DIRECT_H, "direct tasks read the table");
 constexpr int BIG_LOGN = 13;    // big-group FFT blocks <= 8192 real points
-constexpr int SMALL_LOGN = 10;  // small-worker FFT blocks <= 1024 real points
+constexpr int SMALL_LOGN = 12;  // medium-group FFT blocks <= 4096 real points
 constexpr int BIG_SLOTS = smem_complex_slots(1 << (BIG_LOGN - 1));
 constexpr int SMALL_SLOTS = smem_complex_slots(1 << (SMALL_LOGN - 1));
 constexpr int NDEP = 6;
@@ -595,7 +601,8 @@ __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logN
                                const Grp& g) {
   const Stencil st{t.c0, t.c1, t.c2, t.span};
   if (t.kind == TK_FFT) return conv_fft(t.x, t.L, t.y, t.Lout, t.h, st, sbuf, logNmax, tq, g);
-  // TK_DIRECT: one warp, x and weights staged in shared memory
+  // TK_DIRECT: the group's first warp, x and weights staged in shared memory
+  if (g.t >= 32) return 0.0;
   const int M = t.h * t.span + 1;
   double* sx = (double*)sbuf;
   double* sw = sx + 2 * slots - M - 8;
@@ -626,7 +633,7 @@ constexpr int CHAIN_SMEM = CHAIN_SCRATCH;
 
 __host__ __device__ constexpr int sched_smem_bytes() {
   return (SCHED_SHARED_DOUBLES + NCHAIN * CHAIN_SMEM) * (int)sizeof(double) +
-         (TWQ + BIG_SLOTS + SMALL_WORKERS * SMALL_SLOTS) * (int)sizeof(double2);
+         (TWQ + BIG_SLOTS + SMALL_SLOTS) * (int)sizeof(double2);
 }
 
 template <class Pricer>
@@ -639,8 +646,8 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double* chain_scratch = reinterpret_cast<double*>(sdyn_raw) + SCHED_SHARED_DOUBLES;
   double2* tq = reinterpret_cast<double2*>(chain_scratch + NCHAIN * CHAIN_SMEM);  // quarter-wave twiddles
   double2* bigbuf = tq + TWQ;              // big-group FFT buffer
-  double2* smallbuf = bigbuf + BIG_SLOTS;  // SMALL_WORKERS x SMALL_SLOTS
-  __shared__ int s_idx, s_ring;
+  double2* medbuf = bigbuf + BIG_SLOTS;   // medium-group FFT buffer
+  __shared__ int s_idx[2], s_ring[2];
   for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
   sched_init(S);
   if (threadIdx.x == 0) S.prof = prof;
@@ -698,87 +705,81 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     if (lane_id() == 0) last = (atomicSub(&S.chains_left, 1) == 1);
     last = __shfl_sync(FULL, last, 0);
     if (last) {
-      // last chain out: one EXIT per small worker and one for the big group
+      // last chain out: one EXIT for each group
       Task t;
       t.kind = TK_EXIT;
       t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
       t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
       t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
-      for (int k = 0; k < SMALL_WORKERS; ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
+      issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
       issue(S, c, RING_BIG, t, 0, 0, 0, 0);
     }
     return;
   }
+  // ---- FFT groups: one task at a time over 128 threads; each group is the
+  // only consumer of its rings (the big group: RING_BIG, then RING_LOW; the
+  // medium group: RING_SMALL), so claims need no atomics
   double flops = 0.0;
   const long long t_start = clock64();
-  if (role == ROLE_BIG) {
-    // ---- big group: one task at a time over BIG_THREADS threads
-    const Grp g{rank * 32 + lane_id(), BIG_THREADS, BIG_BAR};
-    for (;;) {
-      const long long t0 = clock64();
-      if (rank == 0) {
-        // the big group is the only consumer of RING_BIG / RING_LOW: claim the
-        // oldest urgent task, else the oldest low-priority one
-        int ring = -1, idx = 0;
-        unsigned ns = 16;
-        for (;;) {
-          int r = -1, i = 0;
-          if (lane_id() == 0) {
-            if (S.claim[RING_BIG] < *(volatile int*)&S.reserve[RING_BIG]) { r = RING_BIG; i = S.claim[RING_BIG]++; }
-            else if (S.claim[RING_LOW] < *(volatile int*)&S.reserve[RING_LOW]) { r = RING_LOW; i = S.claim[RING_LOW]++; }
+  const int gi = (role == ROLE_BIG) ? 0 : 1;
+  const Grp g{rank * 32 + lane_id(), GROUP_THREADS, gi == 0 ? BIG_BAR : MED_BAR};
+  double2* buf = gi == 0 ? bigbuf : medbuf;
+  const int slots = gi == 0 ? BIG_SLOTS : SMALL_SLOTS;
+  const int logN = gi == 0 ? BIG_LOGN : SMALL_LOGN;
+  const int r_hi = gi == 0 ? RING_BIG : RING_SMALL;
+  const int r_lo = gi == 0 ? RING_LOW : -1;
+  for (;;) {
+    const long long t0 = clock64();
+    if (rank == 0) {
+      int ring = -1, idx = 0;
+      unsigned ns = 16;
+      for (;;) {
+        // take the head of RING_hi if it is published and its dependencies are
+        // done, else the head of RING_lo if so: never commit to a task that
+        // waits on a task queued behind it in this group's own rings (the
+        // earliest-issued head always becomes ready, so this cannot deadlock)
+        int r = -1, i = 0;
+        if (lane_id() == 0) {
+          for (int k = 0; k < 2 && r < 0; ++k) {
+            const int rr = k == 0 ? r_hi : r_lo;
+            if (rr < 0 || S.claim[rr] >= *(volatile int*)&S.reserve[rr]) continue;
+            const int ii = S.claim[rr];
+            const Task& sl = S.ring[rr][ii % QCAP];
+            if (sl.seq != ii) continue;  // reserved, not yet published
+            __threadfence_block();
+            bool ready = true;
+            for (int d = 0; d < sl.ndep; ++d) ready = ready && task_done(S, sl.dep[d]);
+            if (ready) { r = rr; i = S.claim[rr]++; }
           }
-          r = __shfl_sync(FULL, r, 0);
-          if (r >= 0) { ring = r; idx = __shfl_sync(FULL, i, 0); break; }
-          __nanosleep(ns);
-          ns = ns < FL_IDLE_NS ? 2 * ns : ns;
         }
-        worker_wait_ready(S, ring, idx);
-        if (lane_id() == 0) { s_idx = idx; s_ring = ring; }
+        r = __shfl_sync(FULL, r, 0);
+        if (r >= 0) { ring = r; idx = __shfl_sync(FULL, i, 0); break; }
+        __nanosleep(ns);
+        ns = ns < FL_IDLE_NS ? 2 * ns : ns;
       }
-      gsync(g);
-      const int idx = s_idx, bring = s_ring;
-      const Task t = load_task(S.ring[bring][idx % QCAP]);
-      const long long t1 = clock64();
-      if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-      if (t.kind == TK_EXIT) break;
-      const double fl = pr.exec(S, t, bigbuf, BIG_SLOTS, BIG_LOGN, tq, g);
-      flops += fl > 0 ? fl : 0.0;
-      gsync(g);
-      if (g.t == 0) {
-        publish_done(S, bring, idx);
-        prof_add(prof, PROF_BIG_CYC, clock64() - t1);
-        prof_add(prof, PROF_BIG_N, 1);
-      }
+      worker_wait_ready(S, ring, idx);
+      if (lane_id() == 0) { s_idx[gi] = idx; s_ring[gi] = ring; }
     }
-  } else {
-    // ---- small workers: one warp per task
-    const int sw = rank;
-    const Grp g{lane_id(), 32, -1};
-    double2* buf = smallbuf + sw * SMALL_SLOTS;
-    for (;;) {
-      const long long t0 = clock64();
-      int idx = 0;
-      if (lane_id() == 0) idx = atomicAdd(&S.claim[RING_SMALL], 1);
-      idx = __shfl_sync(FULL, idx, 0);
-      worker_wait_ready(S, RING_SMALL, idx);
-      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
-      const long long t1 = clock64();
-      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-      if (t.kind == TK_EXIT) break;
-      const double fl = pr.exec(S, t, buf, SMALL_SLOTS, SMALL_LOGN, tq, g);
-      flops += fl > 0 ? fl : 0.0;
-      __syncwarp();
-      if (lane_id() == 0) {
-        publish_done(S, RING_SMALL, idx);
-        if (prof) {
-          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
-          prof_add(prof, ps, clock64() - t1);
-          prof_add(prof, ps + 1, 1);
-        }
+    gsync(g);
+    const int idx = s_idx[gi], tring = s_ring[gi];
+    const Task t = load_task(S.ring[tring][idx % QCAP]);
+    const long long t1 = clock64();
+    if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+    if (t.kind == TK_EXIT) break;
+    const double fl = pr.exec(S, t, buf, slots, logN, tq, g);
+    flops += fl > 0 ? fl : 0.0;
+    gsync(g);
+    if (g.t == 0) {
+      publish_done(S, tring, idx);
+      if (prof) {
+        const int ps = gi == 0 ? PROF_BIG_CYC
+                               : (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
+        prof_add(prof, ps, clock64() - t1);
+        prof_add(prof, ps + 1, 1);
       }
     }
   }
-  if (lane_id() == 0 && (role == ROLE_SMALL || rank == 0)) {
+  if (g.t == 0) {
     if (flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     prof_add(prof, PROF_KERNEL_CYC, clock64() - t_start);
   }
