@@ -145,7 +145,7 @@ struct CallSubFrame {
   const double* in;
   double* out;
   double* asmo;
-  int h, state, tk, tk0;
+  int h, state, tk, tk0, q;
 };
 
 // A recursion subtree of height h0 <= CALL_HS done whole in shared memory
@@ -179,8 +179,9 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
         continue;
       }
       F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : CSUB_ASM1) - lo;
+      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
       // mid (helper): cols lo .. j-h1 of row i-h1
-      F.tk = helper_post(*X.S, X.c, F.in + lo, F.asmo + lo, h2, X.kc + (int64_t)h1 * h1, h1 + 1, &F.tk0);
+      F.tk = helper_post(*X.S, X.c, F.q, F.in + lo, F.asmo + lo, h2, X.kc + (int64_t)h1 * h1, h1 + 1, &F.tk0);
       X.flops += 2.0 * h2 * (h1 + 1);
       F.state = 1;
       CallSubFrame& C = stk[sp++];
@@ -190,13 +191,13 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       if (jm < F.j - h1 || jm > F.j) { *err = FL_E_GEOMETRY | 1; return 0; }
       F.jm = jm;
       const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
       twait += clock64() - tw;
       const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
       call_ref_bottom(X, h, A);
       F.tk = -1;
       if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h
-        F.tk = helper_post(*X.S, X.c, F.asmo + lo, F.out + lo, (int)(A - h2), X.kc + (int64_t)h2 * h2, h2 + 1, &F.tk0);
+        F.tk = helper_post(*X.S, X.c, F.q, F.asmo + lo, F.out + lo, (int)(A - h2), X.kc + (int64_t)h2 * h2, h2 + 1, &F.tk0);
         X.flops += 2.0 * (A - h2) * (h2 + 1);
       }
       F.state = 2;
@@ -207,7 +208,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       if (jp < F.jm - h2 || jp > F.jm) { *err = FL_E_GEOMETRY | 2; return 0; }
       if (F.tk >= 0) {
         const long long tw = clock64();
-        helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+        helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
         twait += clock64() - tw;
       }
       --sp;

@@ -166,7 +166,7 @@ struct SubFrame {
   const double* in;
   double* out;
   double* asmo;
-  int h, state, tk, tk0;
+  int h, state, tk, tk0, q;
 };
 
 // A recursion subtree of height h0 <= PUT_HS done whole in shared memory
@@ -207,10 +207,11 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
         continue;
       }
       F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : sp == 2 ? SUB_ASM1 : SUB_ASM2) - (F.f - h1 + 1);
+      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
       // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
       const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, X.kc + (int64_t)h1 * h1, Mmid,
+      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, X.kc + (int64_t)h1 * h1, Mmid,
                          &F.tk0);
       tpost += clock64() - tp;
       X.flops += 2.0 * Lmid * Mmid;
@@ -222,14 +223,14 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
       F.km = km;
       const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
       twait += clock64() - tw;
       // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;
       ref_node_bottom(X, h, A);
       const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, X.kc + (int64_t)h2 * h2, Mbot,
+      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, X.kc + (int64_t)h2 * h2, Mbot,
                          &F.tk0);
       tpost += clock64() - tp;
       X.flops += 2.0 * Lbot * Mbot;
@@ -240,7 +241,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       const int64_t kp = ret;
       if (kp < F.km - h2 || kp > F.km) { *err = FL_E_GEOMETRY | 3; return 0; }
       const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.tk0, F.tk);
+      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
       twait += clock64() - tw;
       --sp;
     }

@@ -95,6 +95,9 @@ constexpr int NRINGS = 3;
 #ifndef FL_POST_FENCE  // 1: CTA fences around helper posts (0: in-order shared stores + compiler barrier)
 #define FL_POST_FENCE 1
 #endif
+#ifndef FL_CONV_PAIRS  // 1: two consecutive outputs per lane for short correlations
+#define FL_CONV_PAIRS 1
+#endif
 #ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
 #define FL_IDLE_NS 512
 #endif
@@ -160,7 +163,7 @@ struct SchedShared {
   double result[NCHAIN];   // per-chain results of blocking tasks
   double result2[NCHAIN];
   int64_t iresult[NCHAIN];
-  Mailbox mb[NCHAIN];
+  Mailbox mb[NCHAIN][2];  // per chain: [0] urgent requests, [1] background (subtree root)
   unsigned long long* prof;  // profile counters (null unless FL_PROFILE)
   int chains_left;
 };
@@ -182,6 +185,7 @@ enum : int {
   // conflict waits by cause: read-after-write / write-after-read-or-write, small / big ring
   PROF_W_RAW_S, PROF_W_RAW_B, PROF_W_WAR_S, PROF_W_WAR_B, PROF_W_N, PROF_W_SUML, PROF_W_SUMH, PROF_W_FFT,
   PROF_W_MAXL,
+  PROF_HELP_CYC = 48, PROF_HELP_CYC_BG, PROF_HELP_FMA,
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
@@ -201,10 +205,13 @@ __device__ void sched_init(SchedShared& S) {
   if (threadIdx.x == 0) S.chains_left = NCHAIN;
   if (threadIdx.x < NCHAIN) {
     S.npend[threadIdx.x] = 0;
-    S.mb[threadIdx.x].seq = 0;
-    S.mb[threadIdx.x].claim = 0;
-    S.mb[threadIdx.x].quit = 0;
-    for (int k = 0; k < HQ; ++k) S.mb[threadIdx.x].done[k] = (k == 0) ? 0 : k - HQ;  // ticket t's slot predecessor t-HQ is done
+    for (int q = 0; q < 2; ++q) {
+      Mailbox& m = S.mb[threadIdx.x][q];
+      m.seq = 0;
+      m.claim = 0;
+      m.quit = 0;
+      for (int k = 0; k < HQ; ++k) m.done[k] = (k == 0) ? 0 : k - HQ;  // ticket t's slot predecessor t-HQ is done
+    }
   }
 }
 
@@ -217,48 +224,46 @@ __device__ __forceinline__ bool task_done(const SchedShared& S, int id) {
   return S.done[r][idx % QCAP] >= idx;
 }
 
-// Chain side of the request ring (all lanes call): post one correlation,
-// returns its ticket.
-__device__ __forceinline__ int helper_post1(SchedShared& S, int c, const double* x, double* y, int Lout,
-                                            const double* w, int M) {
-  Mailbox& m = S.mb[c];
-  const int t = m.seq + 1;
-  while (__shfl_sync(0xffffffffu, m.done[t % HQ], 0) < t - HQ) __nanosleep(16);  // slot still busy
+constexpr int HCHUNK = 64;  // outputs per helper request (large correlations are split)
+
+// Chain side of request ring q of chain c (all lanes call): post a correlation
+// as chunks of HCHUNK outputs with one publication; returns the last ticket and
+// the first in *first (see helper_wait_range).
+__device__ __forceinline__ int helper_post(SchedShared& S, int c, int q, const double* x, double* y, int Lout,
+                                           const double* w, int M, int* first) {
+  Mailbox& m = S.mb[c][q];
+  const int t0 = m.seq + 1;
+  *first = t0;
+  if (Lout <= 0) return t0 - 1;
+  const int n = (Lout + HCHUNK - 1) / HCHUNK;  // <= HQ by construction (Lout <= 2 * PUT_HS)
+  const int tl = t0 + n - 1;
+  const int lane = lane_id();
+  // the slots' previous occupants (t - HQ) must be finished
+  while (__any_sync(0xffffffffu, lane < n && m.done[(t0 + lane) % HQ] < t0 + lane - HQ)) __nanosleep(16);
 #if FL_POST_FENCE
   __threadfence_block();  // every lane's writes to x (shared) ...
 #endif
-  __syncwarp();           // ... are done before lane 0 publishes
-  if (threadIdx.x % 32 == 0) {
-    HReq& r = m.q[t % HQ];
-    r.x = x; r.y = y; r.w = w; r.Lout = Lout; r.M = M;
+  if (lane < n) {
+    HReq& r = m.q[(t0 + lane) % HQ];
+    const int k0 = lane * HCHUNK;
+    r.x = x + k0; r.y = y + k0; r.w = w; r.Lout = (Lout - k0 < HCHUNK) ? Lout - k0 : HCHUNK; r.M = M;
+  }
+  __syncwarp();           // ... and the requests are written before lane 0 publishes
+  if (lane == 0) {
 #if FL_POST_FENCE
     __threadfence_block();
 #else
-    asm volatile("" ::: "memory");  // shared-memory stores of one warp are performed in order
+    asm volatile("" ::: "memory");
 #endif
-    m.seq = t;
+    m.seq = tl;
   }
   __syncwarp();
-  return t;
+  return tl;
 }
 
-constexpr int HCHUNK = 64;  // outputs per helper request (large correlations are split)
-
-// Post a correlation as chunks of HCHUNK outputs; returns the last ticket
-// (its tickets are last-nchunks+1 .. last; see helper_wait_range).
-__device__ __forceinline__ int helper_post(SchedShared& S, int c, const double* x, double* y, int Lout,
-                                           const double* w, int M, int* first) {
-  int t = 0;
-  *first = S.mb[c].seq + 1;
-  for (int k0 = 0; k0 < Lout; k0 += HCHUNK)
-    t = helper_post1(S, c, x + k0, y + k0, (Lout - k0 < HCHUNK) ? Lout - k0 : HCHUNK, w, M);
-  if (Lout <= 0) t = *first - 1;
-  return t;
-}
-
-__device__ __forceinline__ void helper_wait_range(SchedShared& S, int c, int first, int last) {
+__device__ __forceinline__ void helper_wait_range(SchedShared& S, int c, int q, int first, int last) {
   for (int t = first; t <= last; ++t)
-    while (__shfl_sync(0xffffffffu, S.mb[c].done[t % HQ], 0) < t) __nanosleep(8);
+    while (__shfl_sync(0xffffffffu, S.mb[c][q].done[t % HQ], 0) < t) __nanosleep(8);
   __threadfence_block();
 }
 
@@ -492,8 +497,45 @@ __device__ __forceinline__ void conv_direct_pass(const double* __restrict__ x, d
   }
 }
 
+// Lout <= 64: lane l produces the two consecutive outputs 2l, 2l+1, sliding a
+// 3-value window of x through registers (one new x per tap instead of two).
+// Reads x[0 .. Lout+M-1] (one past the window when Lout is odd: callers keep
+// slack behind x) and w[0 .. M-1].
+__device__ __forceinline__ void conv_direct_pairs(const double* __restrict__ x, double* __restrict__ y, int Lout,
+                                                  const double* __restrict__ w, int M) {
+  const int k = 2 * lane_id();
+  const double* xk = x + (k < Lout ? k : 0);
+  double a0e = 0.0, a0o = 0.0, a1e = 0.0, a1o = 0.0;
+  double xc = xk[0];
+  int r = 0;
+#pragma unroll 4
+  for (; r + 1 < M; r += 2) {
+    const double w0 = w[r], w1 = w[r + 1];
+    const double x1 = xk[r + 1], x2 = xk[r + 2];
+    a0e = fma(w0, xc, a0e);
+    a1e = fma(w0, x1, a1e);
+    a0o = fma(w1, x1, a0o);
+    a1o = fma(w1, x2, a1o);
+    xc = x2;
+  }
+  if (r < M) {
+    const double w0 = w[r];
+    a0e = fma(w0, xc, a0e);
+    a1e = fma(w0, xk[r + 1], a1e);
+  }
+  if (k < Lout) y[k] = a0e + a0o;
+  if (k + 1 < Lout) y[k + 1] = a1e + a1o;
+}
+
 __device__ double warp_conv_direct(const double* __restrict__ x, double* __restrict__ y, int64_t Lout,
                                    const double* __restrict__ w, int M) {
+#if FL_CONV_PAIRS
+  if (Lout <= 64) {
+    conv_direct_pairs(x, y, (int)Lout, w, M);
+    __syncwarp();
+    return 2.0 * (double)Lout * (double)M;
+  }
+#endif
   int64_t k0 = 0;
   for (; Lout - k0 > 64; k0 += 128) conv_direct_pass<4>(x, y, k0, Lout, w, M);
   if (Lout - k0 > 32) conv_direct_pass<2>(x, y, k0, Lout, w, M);
@@ -655,31 +697,46 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   int rank = 0;
   const int role = warp_role(threadIdx.x >> 5, &rank);
   if (role == ROLE_HELPER) {
-    // ---- helper warp of chain rank / NHELP: correlations from its request ring
-    Mailbox& m = S.mb[rank / NHELP];
+    // ---- helper warp of chain rank / NHELP: correlations from the chain's
+    // request rings, urgent ring first (claims by CAS: never commit to an
+    // unposted ticket while the other ring has work)
+    const int cc = rank / NHELP;
     double flops = 0.0;
+    unsigned ns = 8;
     for (;;) {
-      int t = 0;
-      if (lane_id() == 0) t = atomicAdd(&m.claim, 1) + 1;
-      t = __shfl_sync(FULL, t, 0);
-      unsigned ns = 8;
-      bool quit = false;
-      while (__shfl_sync(FULL, m.seq, 0) < t) {
-        if (__shfl_sync(FULL, m.quit, 0)) { quit = true; break; }
+      int q = -1, t = 0;
+      if (lane_id() == 0) {
+        for (int k = 0; k < 2 && q < 0; ++k) {
+          Mailbox& mm = S.mb[cc][k];
+          const int cl = *(volatile int*)&mm.claim;
+          if (cl < mm.seq && atomicCAS(&mm.claim, cl, cl + 1) == cl) { q = k; t = cl + 1; }
+        }
+      }
+      q = __shfl_sync(FULL, q, 0);
+      if (q < 0) {
+        if (__shfl_sync(FULL, S.mb[cc][0].quit, 0)) break;
         __nanosleep(ns);
         ns = ns < FL_HELPER_NS ? 2 * ns : ns;
+        continue;
       }
-      if (quit) break;
+      ns = 8;
+      t = __shfl_sync(FULL, t, 0);
+      Mailbox& m = S.mb[cc][q];
       __threadfence_block();
       const volatile HReq& r = m.q[t % HQ];
       const double* x = r.x;
       double* y = r.y;
       const double* w = r.w;
       const int Lout = r.Lout, M = r.M;
+      const long long th = clock64();
       flops += warp_conv_direct(x, y, Lout, w, M);
       __threadfence_block();
       __syncwarp();
-      if (lane_id() == 0) m.done[t % HQ] = t;
+      if (lane_id() == 0) {
+        m.done[t % HQ] = t;
+        prof_add(prof, PROF_HELP_CYC + q, clock64() - th);
+        prof_add(prof, PROF_HELP_FMA, (unsigned long long)Lout * M);
+      }
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     return;
@@ -698,7 +755,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     }
     if (lane_id() == 0) {  // release this chain's helper (all its requests were waited for)
       __threadfence_block();
-      S.mb[c].quit = 1;
+      S.mb[c][0].quit = 1;
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)chain_flops);
     int last = 0;

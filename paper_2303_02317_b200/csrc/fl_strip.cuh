@@ -17,6 +17,9 @@
 namespace fl {
 
 constexpr int64_t NONE_SEEN = -(((int64_t)1) << 60);  // _accel.py:46
+#ifndef FL_STRIP_ORDER
+#define FL_STRIP_ORDER 1
+#endif
 
 // Put strip over columns [lo, hi], `height` forward rows.  Cells <= f hold the
 // payoff, cells f+1..hi come from in_org[col].  Writes the continuation values
@@ -54,7 +57,13 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
     for (int c = 0; c < CPL; ++c) {
       const double l = (c == 0) ? left : v[c - 1];
       const double r = (c == CPL - 1) ? right : v[c + 1];
+      // the shuffled neighbour enters last: one DFMA between a shuffle and the
+      // next row's shuffle on the warp's critical path
+#if FL_STRIP_ORDER
+      const double lin = (c == CPL - 1) ? fma(cu, r, fma(cd, l, cm * v[c])) : fma(cd, l, fma(cu, r, cm * v[c]));
+#else
       const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+#endif
       const bool red = lin > p[c];
       nv[c] = red ? lin : p[c];
       green |= (red ? 0u : 1u) << c;

@@ -18,6 +18,7 @@ names = ["FFT_CYC", "FFT_N", "DIR_CYC", "DIR_N", "OTHER_CYC", "OTHER_N", "BIG_CY
          "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC", "ISS_SCAN", "ISS_STALL", "ISS_SLOT", "F_STAGE", "F_MID",
          "F_BOT", "STRIP_LOOP", "LEAF_LOAD", "W_RAW_S", "W_RAW_B", "W_WAR_S", "W_WAR_B", "W_N", "W_SUML", "W_SUMH", "W_FFT", "W_MAXL", "MAX_LOUT", "MAX_H", "MAX_YX", "HB64", "HB128", "HB256", "HB512", "HBBIG", "LB64", "LB128", "LB256", "LB512", "LBBIG"]
 P = dict(zip(names, p[:len(names)]))
+P["HELP_CYC"], P["HELP_CYC_BG"], P["HELP_FMA"] = p[48], p[49], p[50]
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
 for nm in names:
     print(f"{nm:12s} {P[nm]:.4g}")
@@ -39,4 +40,7 @@ print("strip: loop %.1f cyc/row, load %.0f cyc/leaf (leaves/option %.0f)" % (
     d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"] / 28.0), P["STRIP_ROWS"] / 28.0 / nopt))
 print("conflict waits per option: RAW small %.3g big %.3g, WAR small %.3g big %.3g (n=%.0f)" % (
     P["W_RAW_S"] / nopt, P["W_RAW_B"] / nopt, P["W_WAR_S"] / nopt, P["W_WAR_B"] / nopt, P["W_N"] / nopt))
+print("helpers: urgent %.3g cyc, background %.3g cyc per option; %.3g FMA per option (%.2f FMA/cycle)" % (
+    P["HELP_CYC"] / nopt, P["HELP_CYC_BG"] / nopt, P["HELP_FMA"] / nopt,
+    P["HELP_FMA"] / max(P["HELP_CYC"] + P["HELP_CYC_BG"], 1)))
 print("status nonzero:", int(np.sum(r.status != 0)))
