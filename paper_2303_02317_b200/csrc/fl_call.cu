@@ -22,12 +22,19 @@
 namespace fl {
 
 constexpr int CALL_LEAF = 32;
-constexpr int CALL_HS = 128;  // recursion subtrees of height <= CALL_HS run whole in shared memory
+#ifndef FL_CALL_LEAF_V2
+#define FL_CALL_LEAF_V2 1
+#endif
+#ifndef FL_CALL_HS
+#define FL_CALL_HS 256
+#endif
+constexpr int CALL_HS = FL_CALL_HS;  // recursion subtrees of height <= CALL_HS run whole in shared memory
 constexpr int CALL_MAX_DEPTH = 28;
 constexpr int CALL_RESID_CPT = 8;  // residual strip: cells per big-group thread (width <= 1024)
-constexpr int CSUB_IN = 0, CSUB_ASM0 = CALL_HS + 8, CSUB_ASM1 = CSUB_ASM0 + CALL_HS + 8;
-static_assert(CSUB_ASM1 + CALL_HS / 2 + 8 <= CHAIN_SCRATCH, "call subtree scratch");
-static_assert(CALL_HS <= 4 * CALL_LEAF, "two asm levels cover a subtree");
+constexpr int CSUB_IN = 0, CSUB_ASM0 = CALL_HS + 8, CSUB_ASM1 = CSUB_ASM0 + CALL_HS + 8,
+              CSUB_ASM2 = CSUB_ASM1 + CALL_HS / 2 + 8;
+static_assert(CSUB_ASM2 + CALL_HS / 4 + 8 <= CHAIN_SCRATCH, "call subtree scratch");
+static_assert(CALL_HS <= 8 * CALL_LEAF, "three asm levels cover a subtree");
 static_assert(CALL_HS / 2 <= KT_H, "subtree correlations use the kernel table");
 
 enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
@@ -95,6 +102,46 @@ __device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict_
   return j;
 }
 
+// call_leaf_warp without the per-row boundary reduction.  The call boundary
+// only moves left as rows descend (american.py:232-251 enforces it), so every
+// column right of the row's boundary is an exercise cell for the rest of the
+// strip: advancing all strip columns with the projected update
+// max(wd v + wu v', green) reproduces the analytic exercise values there
+// (lin < green strictly inside the exercise region), and the boundary is
+// needed only once, on the last row (first green by one warp min).  Cells
+// beyond the lattice edge (col > child) are never read by valid cells.  Same
+// operation order as _accel.py:143-158.
+__device__ int64_t call_leaf_v2(const CallParams& P, const double* __restrict__ in_org, double* __restrict__ out_org,
+                                int64_t lo, int64_t top_row, int64_t j0, int height, double* cells) {
+  const int lane = threadIdx.x & 31;
+  const int W = (int)(j0 - lo + 1);
+  const int64_t col = lo + lane;
+  double v = (lane < W) ? in_org[col] : 0.0;
+  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
+  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
+  bool green = false;
+  for (int s = 0; s < height; ++s) {
+    const double bp = __shfl_sync(FULL, Bl, s);
+    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
+    const double right = __shfl_down_sync(FULL, v, 1);
+    const double vr = (lane + 1 < W) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);  // right of j0: exercise
+    const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
+    const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
+    green = !(lin >= grn);
+    v = green ? grn : lin;
+  }
+  const int64_t child = top_row - height;  // last lattice column of the final row
+  const int64_t top = (j0 < child) ? j0 : child;
+  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
+  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
+  *cells += (double)W * height;
+  if (col <= jp && lane < W) out_org[col] = v;
+  __syncwarp();
+  return jp;
+}
+
 struct CallFrame {
   int64_t i, j, jm;
   double* in_org;
@@ -131,7 +178,11 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
                                              double* out_org, int64_t i, int64_t j, int h) {
   const long long t1 = clock64();
   double cells = 0.0;
+#if FL_CALL_LEAF_V2
+  const int64_t jp = call_leaf_v2(P, in_org, out_org, j - h + 1, i, j, h, &cells);
+#else
   const int64_t jp = call_leaf_warp(P, in_org, out_org, j - h + 1, i, j, h, &cells);
+#endif
   X.flops += 5.0 * cells;
   if (X.prof && lane_id() == 0) {
     prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
@@ -162,7 +213,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   double* s_in = X.scratch + CSUB_IN;
   warp_stage(s_in, in_org + lo0, h0);
   long long twait = 0;
-  CallSubFrame stk[4];
+  CallSubFrame stk[5];
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in = s_in - lo0; stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
@@ -178,7 +229,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
         --sp;
         continue;
       }
-      F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : CSUB_ASM1) - lo;
+      F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : sp == 2 ? CSUB_ASM1 : CSUB_ASM2) - lo;
       F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
       // mid (helper): cols lo .. j-h1 of row i-h1
       F.tk = helper_post(*X.S, X.c, F.q, F.in + lo, F.asmo + lo, h2, X.kc + (int64_t)h1 * h1, h1 + 1, &F.tk0);
