@@ -3,6 +3,7 @@
 // result merging.  The reference's pricing entry points (binomial.py:80/161,
 // american.py:428, bsm.py:273/585) map onto fl_price_batch per option kind.
 #include <algorithm>
+#include <iterator>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -147,6 +148,10 @@ struct fl_batch {
   bool need_put = false, need_call = false, need_euro = false;
   std::vector<double> cost;
   std::vector<int32_t> o_put_fast, o_put_base, o_call_fast, o_call_base, o_euro_fast, o_euro_base;
+  std::vector<int32_t> o_mixed;  // puts and calls together (both kinds present): e >= 0 put, e < 0 call -e-1
+  size_t off_mixed = 0;
+  int grid_mixed = 0;
+  int64_t ws_mixed_stride = 0;
   // device-side
   DevBuf d_put, d_call, d_euro, d_orders, d_price, d_status, d_bt, d_bc, d_bcount, d_counter;
   DevBuf d_ws_put, d_ws_call, d_ws_base;
@@ -245,6 +250,13 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
   }
   sort_by_cost(b->o_put_fast, b->cost);
   sort_by_cost(b->o_call_fast, b->cost);
+  b->o_mixed.clear();
+  if (!b->o_put_fast.empty() && !b->o_call_fast.empty()) {  // one kernel, one cost-ordered queue
+    std::merge(b->o_put_fast.begin(), b->o_put_fast.end(), b->o_call_fast.begin(), b->o_call_fast.end(),
+               std::back_inserter(b->o_mixed), [&](int32_t a, int32_t c) { return b->cost[a] > b->cost[c]; });
+    for (int32_t& e : b->o_mixed)
+      if (b->kind[e] == FL_KIND_CALL) e = -e - 1;
+  }
   b->need_put = !b->o_put_fast.empty() || !b->o_put_base.empty();
   b->need_call = !b->o_call_fast.empty() || !b->o_call_base.empty();
   b->need_euro = !b->o_euro_fast.empty() || !b->o_euro_base.empty();
@@ -270,6 +282,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
   place(b->o_call_base, b->off_call_base);
   place(b->o_euro_fast, b->off_euro_fast);
   place(b->o_euro_base, b->off_euro_base);
+  place(b->o_mixed, b->off_mixed);
   FL_CUDA(b->d_orders.ensure(sizeof(int32_t) * (off + 1)));
   FL_CUDA(b->d_price.ensure(sizeof(double) * n));
   FL_CUDA(b->d_status.ensure(sizeof(int32_t) * n));
@@ -301,6 +314,12 @@ int upload(fl_batch* b, cudaStream_t stream) {
     b->grid_call = std::min<int>(((int)b->o_call_fast.size() + nc - 1) / nc, nsm);
     FL_CUDA(b->d_ws_call.ensure(sizeof(double) * b->ws_call_stride * b->grid_call * nc));
   }
+  if (!b->o_mixed.empty()) {
+    b->ws_mixed_stride = std::max(b->ws_put_stride, b->ws_call_stride);
+    const int nc = fl::put_chains_per_cta();
+    b->grid_mixed = std::min<int>(((int)b->o_mixed.size() + nc - 1) / nc, nsm);
+    FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_mixed_stride * b->grid_mixed * nc));
+  }
   const int64_t nbase = (int64_t)std::max({b->o_put_base.size(), b->o_call_base.size(), b->o_euro_base.size()});
   if (nbase > 0) {
     b->ws_base_stride = 3 * nmax_base + 16;
@@ -317,6 +336,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
   copy_in(b->o_call_base, b->off_call_base);
   copy_in(b->o_euro_fast, b->off_euro_fast);
   copy_in(b->o_euro_base, b->off_euro_base);
+  copy_in(b->o_mixed, b->off_mixed);
   b->h2d_bytes = sizeof(int32_t) * (off + 1);
   if (b->need_put) {
     FL_CUDA(cudaMemcpyAsync(b->d_put.p, b->put.data(), sizeof(fl::PutParams) * n, cudaMemcpyHostToDevice, stream));
@@ -353,12 +373,17 @@ int run(fl_batch* b, cudaStream_t stream) {
   int32_t* counter = b->d_counter.as<int32_t>();
   b->launches = 0;
   FL_CUDA(cudaMemsetAsync(b->d_stats.p, 0, 64 * sizeof(unsigned long long), stream));
-  if (!b->o_put_fast.empty()) {
+  if (!b->o_mixed.empty()) {
+    FL_CUDA(fl::launch_american_fast(b->d_put.as<fl::PutParams>(), b->d_call.as<fl::CallParams>(),
+                                     ord + b->off_mixed, (int)b->o_mixed.size(), counter, b->d_ws_put.as<double>(),
+                                     b->ws_mixed_stride, b->grid_mixed, out, stream));
+    ++b->launches;
+  } else if (!b->o_put_fast.empty()) {
     FL_CUDA(fl::launch_put_fast(b->d_put.as<fl::PutParams>(), ord + b->off_put_fast, (int)b->o_put_fast.size(),
                                 counter, b->d_ws_put.as<double>(), b->ws_put_stride, b->grid_put, out, stream));
     ++b->launches;
   }
-  if (!b->o_call_fast.empty()) {
+  if (b->o_mixed.empty() && !b->o_call_fast.empty()) {
     FL_CUDA(fl::launch_call_fast(b->d_call.as<fl::CallParams>(), ord + b->off_call_fast,
                                  (int)b->o_call_fast.size(), counter + 8, b->d_ws_call.as<double>(),
                                  b->ws_call_stride, b->grid_call, out, stream));

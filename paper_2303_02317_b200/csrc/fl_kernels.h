@@ -58,4 +58,10 @@ cudaError_t launch_call_fast(const CallParams* opts, const int32_t* order, int n
 cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,
                                  int64_t ws_stride, BatchOut out, cudaStream_t stream);
 
+// mixed American put / call batches (fl_american.cu): work item e >= 0 is put
+// option e, e < 0 call option -e-1
+cudaError_t launch_american_fast(const PutParams* put, const CallParams* call, const int32_t* order, int nwork,
+                                 int32_t* counter, double* ws, int64_t ws_stride, int grid, BatchOut out,
+                                 cudaStream_t stream);
+
 }  // namespace fl

@@ -4,5 +4,6 @@
 #include "fl_conv.cu"
 #include "fl_put.cu"
 #include "fl_call.cu"
+#include "fl_american.cu"
 #include "fl_euro.cu"
 #include "fl_abi.cu"
