@@ -131,6 +131,42 @@ int fl_call_trapezoid(double S, double K, double wd, double wu, double lu, int64
                       int64_t j, int64_t first, const double* run, int64_t h, double* out_run, int64_t* jp,
                       int32_t* status, void* stream);
 
+/* binomial.py:94 baseline_american_call(keep_grid=True): the projected
+ * induction with every row retained (binomial.py:133-158): rows packed, row i
+ * (i+1 values) at offset i(i+1)/2; masks the same layout (1 = exercise);
+ * cols[i] = first exercise column of row i or INT64_MIN.  steps <= 32768. */
+int fl_call_grid(double S, double K, double wd, double wu, double lu, int64_t n, double* rows, uint8_t* masks,
+                 int64_t* cols, double* price, void* stream);
+
+/* bsm.py:273 baseline_put_fd(record_rows=times): the O(T^2) march of one put
+ * (grid weights cd, cm, cu, spacing ds, anchor k*, strike K, n steps) with the
+ * valid window of each requested row (increasing times in [1, n]) packed into
+ * snap: row t contributes 2n+1-2t values for columns k*-n+t .. k*+n-t.
+ * last_green[0..n]: the boundary record (window offsets already converted to
+ * columns, INT64_MIN once the window loses the boundary). */
+int fl_put_march_rows(double cd, double cm, double cu, double ds, double K, int64_t ks, int64_t n,
+                      const int64_t* times, int ntimes, double* snap, int64_t snap_cap, int64_t* last_green,
+                      double* price, void* stream);
+
+/* bsm.py:585 fast_put_bsm(record_rows=True): one put (Y = 0) priced by the
+ * fast path with the continuation segment of every stage-handoff row appended
+ * to snap (capacity snap_cap doubles; *snap_len = total length needed): the
+ * row recorded at (times[k], cols[k]), k >= 1, holds columns cols[k]+1 ..
+ * k* + T - times[k].  Price, status and boundary record as fl_price_batch. */
+int fl_put_fast_rows(double S, double K, double R, double V, double E, int64_t T, double lam, int64_t base_cutoff,
+                     double* snap, int64_t snap_cap, int64_t* snap_len, double* price, int32_t* status,
+                     int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
+
+/* fft.py:84 fft_forward / fft.py:114 fft_inverse: unnormalised power-of-two
+ * DFT (inverse with the 1/N factor) of n complex values, interleaved
+ * (re, im) doubles, host buffers. */
+int fl_fft(const double* in, int64_t n, int inverse, double* out, void* stream);
+
+/* fft.py:130 convolve: full linear convolution of two complex sequences
+ * (interleaved re, im; real inputs with zero imaginary parts), zero-padded to
+ * the next power of two >= nx + ny - 1; out receives nx + ny - 1 complex values. */
+int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double* out, void* stream);
+
 /* Measured FP64 (DFMA) throughput of the current device in TFLOP/s: the
  * roofline denominator bench.py reports against. */
 int fl_probe_fp64(double* tflops, void* stream);

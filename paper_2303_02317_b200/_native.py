@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
     "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
+    "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve",
     "fl_probe_fp64",
 )
 
@@ -96,6 +97,16 @@ def lib():
         L.fl_put_trapezoid.restype = c_int
         L.fl_call_trapezoid.argtypes = [d, d, d, d, d, i64, i64, i64, i64, P, i64, P, P, P, P]
         L.fl_call_trapezoid.restype = c_int
+        L.fl_call_grid.argtypes = [d, d, d, d, d, i64, P, P, P, P, P]
+        L.fl_call_grid.restype = c_int
+        L.fl_put_march_rows.argtypes = [d, d, d, d, d, i64, i64, P, c_int, P, i64, P, P, P]
+        L.fl_put_march_rows.restype = c_int
+        L.fl_put_fast_rows.argtypes = [d, d, d, d, d, i64, d, i64, P, i64, P, P, P, P, P, P, i32, P]
+        L.fl_put_fast_rows.restype = c_int
+        L.fl_fft.argtypes = [P, i64, c_int, P, P]
+        L.fl_fft.restype = c_int
+        L.fl_convolve.argtypes = [P, i64, P, i64, P, P]
+        L.fl_convolve.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
         _lib = L
@@ -352,3 +363,76 @@ def inspect(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=1
     _check(lib().fl_inspect(n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), float(lam),
                             int(call_cutoff), int(put_cutoff), _ptr(status), _ptr(mode), _ptr(dp), _ptr(ip)))
     return status, mode, dp, ip
+
+
+def call_grid(S, K, wd, wu, lu, n):
+    """fl_call_grid: (price, rows list, masks list, first-green cols)."""
+    n = int(n)
+    cells = (n + 1) * (n + 2) // 2
+    rows = np.empty(cells)
+    masks = np.empty(cells, dtype=np.uint8)
+    cols = np.empty(n + 1, dtype=np.int64)
+    price = ctypes.c_double(0.0)
+    _check(lib().fl_call_grid(float(S), float(K), float(wd), float(wu), float(lu), n, _ptr(rows), _ptr(masks),
+                              _ptr(cols), ctypes.byref(price), None))
+    rl = [rows[i * (i + 1) // 2: i * (i + 1) // 2 + i + 1].copy() for i in range(n + 1)]
+    ml = [masks[i * (i + 1) // 2: i * (i + 1) // 2 + i + 1].astype(bool) for i in range(n + 1)]
+    return price.value, rl, ml, cols
+
+
+def put_march_rows(cd, cm, cu, ds, K, ks, n, times):
+    """fl_put_march_rows: (price, last_green cols[0..n], {t: window values})."""
+    n = int(n)
+    times = np.ascontiguousarray(sorted(set(int(t) for t in times)), dtype=np.int64)
+    cap = int(sum(2 * n + 1 - 2 * t for t in times))
+    snap = np.empty(max(cap, 1))
+    lg = np.empty(n + 1, dtype=np.int64)
+    price = ctypes.c_double(0.0)
+    _check(lib().fl_put_march_rows(float(cd), float(cm), float(cu), float(ds), float(K), int(ks), n,
+                                   _ptr(times) if len(times) else None, len(times), _ptr(snap), cap, _ptr(lg),
+                                   ctypes.byref(price), None))
+    out, off = {}, 0
+    for t in times.tolist():
+        m = 2 * n + 1 - 2 * t
+        out[t] = snap[off:off + m].copy()
+        off += m
+    return price.value, lg, out
+
+
+def put_fast_rows(S, K, R, V, E, T, lam, base_cutoff):
+    """fl_put_fast_rows: (price, status, times, cols, flat snapshot buffer)."""
+    cap = 1 << 16
+    for _ in range(3):
+        snap = np.empty(cap)
+        used = ctypes.c_int64(0)
+        price = ctypes.c_double(0.0)
+        status = ctypes.c_int32(0)
+        bcap = 128
+        bt = np.empty(bcap, dtype=np.int64)
+        bc = np.empty(bcap, dtype=np.int64)
+        bn = ctypes.c_int32(0)
+        _check(lib().fl_put_fast_rows(float(S), float(K), float(R), float(V), float(E), int(T), float(lam),
+                                      int(base_cutoff), _ptr(snap), cap, ctypes.byref(used), ctypes.byref(price),
+                                      ctypes.byref(status), _ptr(bt), _ptr(bc), ctypes.byref(bn), bcap, None))
+        if used.value <= cap:
+            k = min(bn.value, bcap)
+            return price.value, status.value, bt[:k].copy(), bc[:k].copy(), snap[:used.value].copy()
+        cap = int(used.value) + 16
+    raise NativeLibraryError("fl_put_fast_rows: snapshot buffer did not converge")
+
+
+def fft(vec: np.ndarray, inverse: bool) -> np.ndarray:
+    """fl_fft on a complex128 vector (power-of-two length)."""
+    v = np.ascontiguousarray(vec, dtype=np.complex128)
+    out = np.empty_like(v)
+    _check(lib().fl_fft(_ptr(v), v.shape[0], 1 if inverse else 0, _ptr(out), None))
+    return out
+
+
+def convolve(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """fl_convolve on complex128 vectors: full linear convolution."""
+    a = np.ascontiguousarray(x, dtype=np.complex128)
+    b = np.ascontiguousarray(y, dtype=np.complex128)
+    out = np.empty(a.shape[0] + b.shape[0] - 1, dtype=np.complex128)
+    _check(lib().fl_convolve(_ptr(a), a.shape[0], _ptr(b), b.shape[0], _ptr(out), None))
+    return out

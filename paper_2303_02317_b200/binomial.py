@@ -19,7 +19,6 @@ from .model import (
     BoundarySeries,
     GridRow,
     OptionSpec,
-    UnsupportedCombinationError,
     derive_binomial_params,
 )
 
@@ -35,11 +34,8 @@ __all__ = [
 
 @dataclass(frozen=True, slots=True)
 class AmericanCallResult:
-    """Price plus first-exercise-column record (binomial.py:41-55).
-
-    ``rows`` / ``exercise_masks`` (the reference's keep_grid output) are not
-    produced by the GPU path and stay None.
-    """
+    """Price plus first-exercise-column record (binomial.py:41-55); ``rows`` /
+    ``exercise_masks`` are filled by ``baseline_american_call(keep_grid=True)``."""
 
     price: float
     boundaries: BoundarySeries
@@ -73,9 +69,16 @@ def baseline_american_call(spec: OptionSpec, params: BinomialParams | None = Non
                            keep_grid: bool = False) -> AmericanCallResult:
     """O(T^2) projected induction on the device, first green per row recorded
     (binomial.py:94-130)."""
-    if keep_grid:
-        raise UnsupportedCombinationError("keep_grid=True (full-grid snapshots) is not produced by the GPU path")
     _pricing.check_params(spec, params)
+    if keep_grid:
+        # every row and exercise mask retained (binomial.py:133-158), computed on the device
+        from . import _native
+
+        p = derive_binomial_params(spec)
+        price, rows, masks, cols = _native.call_grid(spec.spot, spec.strike, p.weight_down, p.weight_up,
+                                                     p.log_up, spec.steps)
+        series = BoundarySeries(np.arange(spec.steps + 1, dtype=np.int64), cols)
+        return AmericanCallResult(price=price, boundaries=series, rows=rows, exercise_masks=masks)
     price, series = _pricing.price_one(_pricing.KIND_CALL, spec, method=_pricing.BASELINE)
     return AmericanCallResult(price=price, boundaries=series)
 

@@ -149,10 +149,21 @@ def baseline_put_fd(spec: OptionSpec, lam: float = DEFAULT_LAMBDA, steps: int | 
                     record_rows: tuple[int, ...] | None = None) -> PutResult:
     """O(T^2) projected march over the shrinking window, on the device; the
     last green column of every row is recorded (bsm.py:273-338)."""
-    if record_rows:
-        raise UnsupportedCombinationError("record_rows snapshots are not produced by the GPU path")
     from . import _pricing
 
+    if record_rows is not None:
+        # snapshots of the valid window of the named rows (bsm.py:296-322), on the device
+        from . import _native
+
+        disc = discretize_bsm(spec, lam, steps)
+        n = disc.steps
+        targets = sorted({int(t) for t in record_rows if 0 < t <= n})
+        price, cols, snaps = _native.put_march_rows(disc.coef_down, disc.coef_mid, disc.coef_up, disc.d_s,
+                                                    spec.strike, disc.k_star, n, targets)
+        lo = disc.k_star - n
+        rows = {t: GridRow(time_index=t, col_offset=lo + t, values=v) for t, v in snaps.items()}
+        series = BoundarySeries(times=np.arange(n + 1, dtype=np.int64), columns=cols)
+        return PutResult(price=price, boundaries=series, rows=rows)
     price, series = _pricing.price_one(_pricing.KIND_PUT, spec, method=_pricing.BASELINE, lam=float(lam),
                                        steps=steps)
     return PutResult(price=price, boundaries=series)
@@ -166,9 +177,28 @@ def fast_put_bsm(spec: OptionSpec, lam: float = DEFAULT_LAMBDA, steps: int | Non
     -> the O(T^2) march), same stage schedule, same handoff-row record.
     ``parallel`` is accepted and has no effect on results."""
     del parallel
-    if record_rows:
-        raise UnsupportedCombinationError("record_rows snapshots are not produced by the GPU path")
     from . import _pricing
+
+    if record_rows:
+        disc = discretize_bsm(spec, lam, steps)
+        n = disc.steps
+        if base_cutoff < 1:
+            raise ValidationError("base_cutoff", "base_cutoff must be >= 1")
+        if disc.k_star > -n and n > 2 * base_cutoff:  # the stage loop runs: snapshot every handoff row
+            from . import _native
+
+            price, status, times, cols, flat = _native.put_fast_rows(
+                spec.spot, spec.strike, spec.rate, spec.volatility, spec.days_to_expiry, n, float(lam),
+                int(base_cutoff))
+            err = _native.status_error(status)
+            if err is not None:
+                raise err
+            rows, off = {}, 0
+            for t, f in zip(times[1:].tolist(), cols[1:].tolist()):
+                m = disc.k_star + n - t - f
+                rows[t] = GridRow(time_index=t, col_offset=f + 1, values=flat[off:off + m])
+                off += m
+            return PutResult(price=price, boundaries=BoundarySeries(times, cols), rows=rows)
 
     price, series = _pricing.price_one(_pricing.KIND_PUT, spec, method=_pricing.FAST, lam=float(lam),
                                        steps=steps, put_cutoff=int(base_cutoff))

@@ -152,6 +152,8 @@ struct fl_batch {
   size_t off_mixed = 0;
   int grid_mixed = 0;
   int64_t ws_mixed_stride = 0;
+  int64_t snap_cap = 0;  // fast-put record_rows capture (fl_put_fast_rows only)
+  DevBuf d_snap, d_snaplen;
   // device-side
   DevBuf d_put, d_call, d_euro, d_orders, d_price, d_status, d_bt, d_bc, d_bcount, d_counter;
   DevBuf d_ws_put, d_ws_call, d_ws_base;
@@ -162,7 +164,7 @@ struct fl_batch {
 
   void release() {
     for (DevBuf* b : {&d_put, &d_call, &d_euro, &d_orders, &d_price, &d_status, &d_bt, &d_bc, &d_bcount, &d_counter,
-                      &d_ws_put, &d_ws_call, &d_ws_base, &d_stats})
+                      &d_ws_put, &d_ws_call, &d_ws_base, &d_stats, &d_snap, &d_snaplen})
       b->release();
     put.release();
     call.release();
@@ -364,6 +366,11 @@ fl::BatchOut make_out(fl_batch* b) {
   o.cap = b->cap;
   o.flops = b->d_stats.as<unsigned long long>();
   o.prof = std::getenv("FL_PROFILE") ? b->d_stats.as<unsigned long long>() + 8 : nullptr;
+  if (b->snap_cap > 0) {
+    o.snap = b->d_snap.as<double>();
+    o.snap_cap = b->snap_cap;
+    o.snap_len = b->d_snaplen.as<int64_t>();
+  }
   return o;
 }
 
@@ -645,6 +652,147 @@ int fl_call_trapezoid(double S, double K, double wd, double wu, double lu, int64
     if (len < 0 || len > width) return fail("fl_call_trapezoid: inconsistent output length");
     if (len > 0) FL_CUDA(cudaMemcpy(out_run, B.out.p, sizeof(double) * len, cudaMemcpyDeviceToHost));
   }
+  return 0;
+}
+
+int fl_call_grid(double S, double K, double wd, double wu, double lu, int64_t n, double* rows, uint8_t* masks,
+                 int64_t* cols, double* price, void* stream) {
+  if (!rows || !masks || !cols || !price) return fail("fl_call_grid: null pointer");
+  if (n < 1 || n > (1 << 15)) return fail("fl_call_grid: steps must be in [1, 32768] for a retained grid");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t cells = (n + 1) * (n + 2) / 2;
+  DevBuf d_rows, d_masks, d_cols, d_price, d_ws;
+  FL_CUDA(d_rows.ensure(sizeof(double) * cells));
+  FL_CUDA(d_masks.ensure(cells));
+  FL_CUDA(d_cols.ensure(sizeof(int64_t) * (n + 1)));
+  FL_CUDA(d_price.ensure(sizeof(double)));
+  FL_CUDA(d_ws.ensure(sizeof(double) * 2 * (n + 2)));
+  fl::CallParams P{};
+  P.S = S; P.K = K; P.wd = wd; P.wu = wu; P.lu = lu; P.n = n; P.mode = fl::MODE_BASELINE;
+  cudaError_t e = fl::launch_call_grid(P, d_rows.as<double>(), d_masks.as<uint8_t>(), d_cols.as<int64_t>(),
+                                       d_price.as<double>(), d_ws.as<double>(), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(rows, d_rows.p, sizeof(double) * cells, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(masks, d_masks.p, cells, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cols, d_cols.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(price, d_price.p, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (DevBuf* b : {&d_rows, &d_masks, &d_cols, &d_price, &d_ws}) b->release();
+  if (e != cudaSuccess) return fail(std::string("fl_call_grid: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int fl_put_march_rows(double cd, double cm, double cu, double ds, double K, int64_t ks, int64_t n,
+                      const int64_t* times, int ntimes, double* snap, int64_t snap_cap, int64_t* last_green,
+                      double* price, void* stream) {
+  if (!last_green || !price || (ntimes > 0 && (!times || !snap))) return fail("fl_put_march_rows: null pointer");
+  if (n < 1) return fail("fl_put_march_rows: steps must be >= 1");
+  int64_t need = 0;
+  for (int i = 0; i < ntimes; ++i) {
+    if (times[i] < 1 || times[i] > n || (i > 0 && times[i] <= times[i - 1]))
+      return fail("fl_put_march_rows: times must be increasing in [1, steps]");
+    need += 2 * n + 1 - 2 * times[i];
+  }
+  if (need > snap_cap) return fail("fl_put_march_rows: snapshot buffer too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf d_times, d_snap, d_lg, d_price, d_ws;
+  FL_CUDA(d_times.ensure(sizeof(int64_t) * (ntimes + 1)));
+  FL_CUDA(d_snap.ensure(sizeof(double) * (need + 1)));
+  FL_CUDA(d_lg.ensure(sizeof(int64_t) * (n + 1)));
+  FL_CUDA(d_price.ensure(sizeof(double)));
+  FL_CUDA(d_ws.ensure(sizeof(double) * 3 * (2 * n + 1)));
+  if (ntimes > 0) FL_CUDA(cudaMemcpyAsync(d_times.p, times, sizeof(int64_t) * ntimes, cudaMemcpyHostToDevice, st));
+  fl::PutParams P{};
+  P.K = K; P.cd = cd; P.cm = cm; P.cu = cu; P.ds = ds; P.ks = ks; P.n = n; P.mode = fl::MODE_BASELINE;
+  cudaError_t e = fl::launch_put_march_rows(P, d_times.as<int64_t>(), ntimes, d_snap.as<double>(),
+                                            d_lg.as<int64_t>(), d_price.as<double>(), d_ws.as<double>(), st);
+  if (e == cudaSuccess && need > 0)
+    e = cudaMemcpyAsync(snap, d_snap.p, sizeof(double) * need, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(last_green, d_lg.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(price, d_price.p, sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (DevBuf* b : {&d_times, &d_snap, &d_lg, &d_price, &d_ws}) b->release();
+  if (e != cudaSuccess) return fail(std::string("fl_put_march_rows: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int fl_put_fast_rows(double S, double K, double R, double V, double E, int64_t T, double lam, int64_t base_cutoff,
+                     double* snap, int64_t snap_cap, int64_t* snap_len, double* price, int32_t* status,
+                     int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream) {
+  if (!snap || !snap_len || !price || !status) return fail("fl_put_fast_rows: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  fl_batch b;
+  const int8_t kind = FL_KIND_PUT;
+  const double Y = 0.0;
+  int rc = plan_host(&b, 1, &kind, &S, &K, &R, &Y, &V, &E, &T, lam, 256, base_cutoff, FL_METHOD_FAST, bnd_cap);
+  if (rc) { b.release(); return rc; }
+  b.snap_cap = snap_cap;
+  cudaError_t e = b.d_snap.ensure(sizeof(double) * (snap_cap + 1));
+  if (e == cudaSuccess) e = b.d_snaplen.ensure(sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.d_snaplen.p, 0, sizeof(int64_t), st);
+  if (e != cudaSuccess) { b.release(); return fail(std::string("fl_put_fast_rows: ") + cudaGetErrorString(e)); }
+  rc = upload(&b, st);
+  if (!rc) rc = run(&b, st);
+  if (!rc) rc = fetch(&b, price, status, bnd_times, bnd_cols, bnd_count, st);
+  if (!rc) {
+    e = cudaMemcpy(snap_len, b.d_snaplen.p, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    const int64_t got = std::min<int64_t>(*snap_len, snap_cap);
+    if (e == cudaSuccess && got > 0) e = cudaMemcpy(snap, b.d_snap.p, sizeof(double) * got, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(std::string("fl_put_fast_rows: ") + cudaGetErrorString(e));
+  }
+  b.release();
+  return rc;
+}
+
+int fl_fft(const double* in, int64_t n, int inverse, double* out, void* stream) {
+  if (!in || !out) return fail("fl_fft: null pointer");
+  if (n < 1 || (n & (n - 1)) != 0) return fail("fl_fft: length must be a power of two");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf a, b;
+  FL_CUDA(a.ensure(sizeof(double2) * n));
+  FL_CUDA(b.ensure(sizeof(double2) * n));
+  FL_CUDA(cudaMemcpyAsync(a.p, in, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+  double2* r = nullptr;
+  cudaError_t e = fl::fft_pow2(a.as<double2>(), b.as<double2>(), n, inverse ? 1 : -1, &r, st);
+  if (e == cudaSuccess && inverse) e = fl::launch_cscale(r, n, 1.0 / (double)n, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, r, sizeof(double2) * n, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  a.release();
+  b.release();
+  if (e != cudaSuccess) return fail(std::string("fl_fft: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double* out, void* stream) {
+  if (!x || !y || !out) return fail("fl_convolve: null pointer");
+  if (nx < 1 || ny < 1) return fail("fl_convolve: empty input");
+  const int64_t out_len = nx + ny - 1;
+  int64_t n = 1;
+  while (n < out_len) n <<= 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf a, b, t;
+  FL_CUDA(a.ensure(sizeof(double2) * n));
+  FL_CUDA(b.ensure(sizeof(double2) * n));
+  FL_CUDA(t.ensure(sizeof(double2) * n));
+  FL_CUDA(cudaMemsetAsync(a.p, 0, sizeof(double2) * n, st));
+  FL_CUDA(cudaMemsetAsync(b.p, 0, sizeof(double2) * n, st));
+  FL_CUDA(cudaMemcpyAsync(a.p, x, sizeof(double2) * nx, cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(b.p, y, sizeof(double2) * ny, cudaMemcpyHostToDevice, st));
+  double2 *fa = nullptr, *fb = nullptr, *r = nullptr;
+  cudaError_t e = fl::fft_pow2(a.as<double2>(), t.as<double2>(), n, -1, &fa, st);
+  // fa is a or t; transform b using the other scratch
+  double2* scratch = (fa == a.as<double2>()) ? t.as<double2>() : a.as<double2>();
+  if (e == cudaSuccess) e = fl::fft_pow2(b.as<double2>(), scratch, n, -1, &fb, st);
+  if (e == cudaSuccess) e = fl::launch_cmul(fa, fb, n, 1.0, st);
+  double2* other = (fa == a.as<double2>()) ? ((fb == t.as<double2>()) ? b.as<double2>() : t.as<double2>())
+                                           : ((fb == a.as<double2>()) ? b.as<double2>() : a.as<double2>());
+  if (e == cudaSuccess) e = fl::fft_pow2(fa, other, n, 1, &r, st);
+  if (e == cudaSuccess) e = fl::launch_cscale(r, n, 1.0 / (double)n, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, r, sizeof(double2) * out_len, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  a.release();
+  b.release();
+  t.release();
+  if (e != cudaSuccess) return fail(std::string("fl_convolve: ") + cudaGetErrorString(e));
   return 0;
 }
 

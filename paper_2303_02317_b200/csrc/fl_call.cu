@@ -703,6 +703,61 @@ cudaError_t launch_call_trapezoid(const CallParams& P, int64_t i, int64_t j, int
   return cudaGetLastError();
 }
 
+// baseline_american_call(keep_grid=True) (binomial.py:133-158, numpy form):
+// every row and its exercise mask retained, rows packed (row i at i(i+1)/2).
+// Exercise value S exp((2j - i) lu) - K per cell (the grid variant's formula).
+__global__ void __launch_bounds__(CTA_THREADS)
+call_grid_kernel(CallParams P, double* __restrict__ rows, uint8_t* __restrict__ masks, int64_t* __restrict__ cols,
+                 double* __restrict__ price, double* __restrict__ ws) {
+  __shared__ int s_fg;
+  const int64_t n = P.n;
+  double* a = ws;
+  double* b = a + (n + 2);
+  if (threadIdx.x == 0) s_fg = INT32_MAX;
+  __syncthreads();
+  const int64_t base_n = n * (n + 1) / 2;
+  for (int64_t j = threadIdx.x; j <= n; j += CTA_THREADS) {
+    const double node = __dsub_rn(__dmul_rn(P.S, exp(__dmul_rn(__dsub_rn(2.0 * (double)j, (double)n), P.lu))), P.K);
+    const double v = node > 0.0 ? node : 0.0;  // leaf_row
+    a[j] = v;
+    rows[base_n + j] = v;
+    const bool g = v > 0.0;
+    masks[base_n + j] = g;
+    if (g) atomicMin(&s_fg, (int)j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cols[n] = (s_fg == INT32_MAX) ? INT64_MIN : s_fg;
+  for (int64_t i = n - 1; i >= 0; --i) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_fg = INT32_MAX;
+    __syncthreads();
+    const int64_t base = i * (i + 1) / 2;
+    for (int64_t j = threadIdx.x; j <= i; j += CTA_THREADS) {
+      const double lin = __dadd_rn(__dmul_rn(P.wd, a[j]), __dmul_rn(P.wu, a[j + 1]));
+      const double grn =
+          __dsub_rn(__dmul_rn(P.S, exp(__dmul_rn(__dsub_rn(2.0 * (double)j, (double)i), P.lu))), P.K);
+      const bool g = lin < grn;
+      const double v = g ? grn : lin;
+      b[j] = v;
+      rows[base + j] = v;
+      masks[base + j] = g;
+      if (g) atomicMin(&s_fg, (int)j);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cols[i] = (s_fg == INT32_MAX) ? INT64_MIN : s_fg;
+    double* t = a;
+    a = b;
+    b = t;
+  }
+  if (threadIdx.x == 0) *price = a[0];
+}
+
+cudaError_t launch_call_grid(const CallParams& P, double* rows, uint8_t* masks, int64_t* cols, double* price,
+                             double* ws, cudaStream_t stream) {
+  call_grid_kernel<<<1, CTA_THREADS, 0, stream>>>(P, rows, masks, cols, price, ws);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,
                                  int64_t ws_stride, BatchOut out, cudaStream_t stream) {
   if (nwork <= 0) return cudaSuccess;

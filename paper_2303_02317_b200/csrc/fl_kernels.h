@@ -20,6 +20,11 @@ struct BatchOut {
   int32_t cap;
   unsigned long long* flops;  // [0] executed fp64 flops, [1] reference-algorithmic flops (accumulated), may be null
   unsigned long long* prof;   // optional profile counters (PROF_* in fl_sched.cuh), may be null
+  // optional fast-put row snapshots (record_rows): option o appends its handoff
+  // segments at snap + o * snap_cap, snap_len[o] = total length (may exceed cap)
+  double* snap = nullptr;
+  int64_t snap_cap = 0;
+  int64_t* snap_len = nullptr;
 };
 
 void init_twiddles(cudaStream_t stream);
@@ -63,5 +68,16 @@ cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, i
 cudaError_t launch_american_fast(const PutParams* put, const CallParams* call, const int32_t* order, int nwork,
                                  int32_t* counter, double* ws, int64_t ws_stride, int grid, BatchOut out,
                                  cudaStream_t stream);
+
+// grid / row snapshots for the structural APIs
+cudaError_t launch_put_march_rows(const PutParams& P, const int64_t* times, int ntimes, double* snap,
+                                  int64_t* last_green, double* price, double* ws, cudaStream_t stream);
+cudaError_t launch_call_grid(const CallParams& P, double* rows, uint8_t* masks, int64_t* cols, double* price,
+                             double* ws, cudaStream_t stream);
+
+// generic transform utilities (fl_fft.cu)
+cudaError_t fft_pow2(double2* buf, double2* tmp, int64_t n, int sign, double2** result, cudaStream_t stream);
+cudaError_t launch_cmul(double2* a, const double2* b, int64_t n, double scale, cudaStream_t stream);
+cudaError_t launch_cscale(double2* a, int64_t n, double scale, cudaStream_t stream);
 
 }  // namespace fl

@@ -6,4 +6,5 @@
 #include "fl_call.cu"
 #include "fl_american.cu"
 #include "fl_euro.cu"
+#include "fl_fft.cu"
 #include "fl_abi.cu"

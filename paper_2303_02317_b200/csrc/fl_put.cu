@@ -413,6 +413,18 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       m += hh;
     }
     put_record(out, o, cnt, m, f);
+    if (out.snap) {  // record_rows (bsm.py:667-671): the handoff row's continuation segment
+      wait_all_own(S, c);
+      const int64_t len = ks + (n - m) - f;
+      int64_t* used = out.snap_len + o;
+      if (*used + len <= out.snap_cap) {
+        double* dst = out.snap + (int64_t)o * out.snap_cap + *used;
+        for (int64_t i = lane_id(); i < len; i += 32) dst[i] = nxt_org[f + 1 + i];
+      }
+      __syncwarp();
+      if (lane_id() == 0) *used += len;  // the true length even when truncated
+      __syncwarp();
+    }
     double* t = cur_org;
     cur_org = nxt_org;
     nxt_org = t;
@@ -644,6 +656,69 @@ cudaError_t launch_put_trapezoid(const PutParams& P, int64_t f, int64_t W, int64
   if (e != cudaSuccess) return e;
   const PutTrapPricer pr{P, f, W, h, seg, out, meta, flops};
   put_trap_kernel<<<1, SCHED_THREADS, sched_smem_bytes(), stream>>>(pr, counter, ws, ws_stride);
+  return cudaGetLastError();
+}
+
+// baseline_put_fd with record_rows (bsm.py:296-322): one option, the O(T^2)
+// march with snapshots of the valid window after the given steps.  Row t
+// snapshot = window offsets t .. 2n-t (columns lo+t ..), packed in order.
+__global__ void __launch_bounds__(CTA_THREADS)
+put_march_rows_kernel(PutParams P, const int64_t* __restrict__ times, int ntimes, double* __restrict__ snap,
+                      int64_t* __restrict__ last_green, double* __restrict__ price, double* __restrict__ ws) {
+  __shared__ int s_red[CTA_THREADS / 32];
+  const int64_t n = P.n;
+  const int64_t W = 2 * n + 1;
+  const int64_t lo = P.ks - n;
+  double* a = ws;
+  double* b = a + W;
+  double* pay = b + W;
+  for (int64_t k = threadIdx.x; k < W; k += CTA_THREADS) {
+    const double p = 1.0 - exp((double)(lo + k) * P.ds);
+    pay[k] = p;
+    a[k] = p > 0.0 ? p : 0.0;
+    b[k] = a[k];
+  }
+  __syncthreads();
+  int ti = 0;
+  int64_t soff = 0;
+  for (int64_t s = 1; s <= n; ++s) {
+    int lg = -1;
+    for (int64_t k = s + threadIdx.x; k <= W - 1 - s; k += CTA_THREADS) {
+      const double lin = __dadd_rn(__dadd_rn(__dmul_rn(P.cm, a[k]), __dmul_rn(P.cu, a[k + 1])),
+                                   __dmul_rn(P.cd, a[k - 1]));
+      const double p = pay[k];
+      const bool red = lin > p;
+      b[k] = red ? lin : p;
+      if (!red) lg = (int)k;
+    }
+    lg = warp_max_i32(lg);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = lg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int m = -1;
+      for (int i = 0; i < CTA_THREADS / 32; ++i) m = s_red[i] > m ? s_red[i] : m;
+      last_green[s] = (m < 0) ? INT64_MIN : lo + m;
+    }
+    double* t = a;
+    a = b;
+    b = t;
+    while (ti < ntimes && times[ti] == s) {  // snapshot of the valid window of row s
+      const int64_t len = W - 2 * s;
+      for (int64_t k = threadIdx.x; k < len; k += CTA_THREADS) snap[soff + k] = a[s + k];
+      soff += len;
+      ++ti;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *price = P.K * a[n];
+    last_green[0] = (P.ks + n < 0) ? P.ks + n : 0;
+  }
+}
+
+cudaError_t launch_put_march_rows(const PutParams& P, const int64_t* times, int ntimes, double* snap,
+                                  int64_t* last_green, double* price, double* ws, cudaStream_t stream) {
+  put_march_rows_kernel<<<1, CTA_THREADS, 0, stream>>>(P, times, ntimes, snap, last_green, price, ws);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ from .model import (
     ValidationError,
 )
 
-__all__ = ["Kernel", "kernel_power", "apply_linear_steps"]
+__all__ = ["Kernel", "kernel_power", "apply_linear_steps", "fft_forward", "fft_inverse", "convolve"]
 
 
 @dataclass(frozen=True, slots=True)
@@ -98,3 +98,39 @@ def apply_linear_steps(row: GridRow, kernel: Kernel, h: int, *, direction: int =
     taps, c0, c1, c2 = _device_taps(kernel)
     vals = _native.apply_linear_steps(row.values, taps, c0, c1, c2, h)
     return GridRow(row.time_index + direction * h, row.col_offset - h * kernel.min_offset, vals)
+
+
+def _require_pow2(n: int) -> None:
+    if n < 1 or (n & (n - 1)) != 0:
+        raise ValidationError("length", f"fft length must be a power of two, got {n}")
+
+
+def fft_forward(vec: np.ndarray) -> np.ndarray:
+    """Unnormalised DFT of a power-of-two vector on the device (fft.py:84-111)."""
+    arr = np.asarray(vec)
+    if arr.ndim != 1:
+        raise ValidationError("vec", "fft input must be 1-D")
+    _require_pow2(arr.shape[0])
+    return _native.fft(arr, inverse=False)
+
+
+def fft_inverse(vec: np.ndarray) -> np.ndarray:
+    """Inverse DFT with the 1/N factor on the device (fft.py:114-123)."""
+    arr = np.asarray(vec)
+    if arr.ndim != 1:
+        raise ValidationError("vec", "fft input must be 1-D")
+    _require_pow2(arr.shape[0])
+    return _native.fft(arr, inverse=True)
+
+
+def convolve(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Full linear convolution by the transform pair on the device (fft.py:130-163).
+    Real inputs give a real float64 result, complex inputs the complex one."""
+    ax = np.asarray(x)
+    ay = np.asarray(y)
+    if ax.ndim != 1 or ay.ndim != 1 or ax.shape[0] < 1 or ay.shape[0] < 1:
+        raise ValidationError("x", "convolve inputs must be nonempty 1-D")
+    out = _native.convolve(ax, ay)
+    if not (np.iscomplexobj(x) or np.iscomplexobj(y)):
+        return np.ascontiguousarray(out.real)
+    return out

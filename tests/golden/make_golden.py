@@ -242,6 +242,70 @@ def ops_cases():
     print(f"ops: {int(out['n_kp'])} kernel cases, {int(out['n_pt'])} put stages, {int(out['n_ct'])} trapezoids")
 
 
+def api_cases():
+    """Golden vectors for the structural API options the reference tests use:
+    keep_grid, record_rows (baseline and fast), fft_forward / fft_inverse /
+    convolve.  Saved as api.npz."""
+    out = {}
+    O = fl.OptionSpec
+    rng = np.random.default_rng([98, 20261019])
+    k = 0
+    for spec in [O(100.0, 90.0, 0.03, 0.07, 0.25, 365, 64), O(150.0, 80.0, 0.09, 0.05, 0.15, 365, 200),
+                 O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 33)]:
+        r = fl.baseline_american_call(spec, keep_grid=True)
+        out[f"g{k}_spec"] = np.array([spec.spot, spec.strike, spec.rate, spec.dividend_yield, spec.volatility,
+                                      spec.days_to_expiry, spec.steps])
+        out[f"g{k}_price"] = np.asarray(r.price)
+        out[f"g{k}_cols"] = r.boundaries.columns
+        out[f"g{k}_rows"] = np.concatenate(r.rows)
+        out[f"g{k}_masks"] = np.concatenate(r.exercise_masks).astype(np.uint8)
+        k += 1
+    out["n_g"] = np.asarray(k)
+    k = 0
+    for spec, steps, rec in [(O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024), 512, (100, 300, 500)),
+                             (O(90.0, 110.0, 0.06, 0.0, 0.35, 500, 300), None, (1, 150, 299, 300))]:
+        r = fl.baseline_put_fd(spec, 0.4, steps, record_rows=rec)
+        out[f"b{k}_spec"] = np.array([spec.spot, spec.strike, spec.rate, spec.dividend_yield, spec.volatility,
+                                      spec.days_to_expiry, spec.steps if steps is None else steps])
+        out[f"b{k}_price"] = np.asarray(r.price)
+        out[f"b{k}_cols"] = r.boundaries.columns
+        ts = sorted(r.rows)
+        out[f"b{k}_times"] = np.asarray(ts, dtype=np.int64)
+        out[f"b{k}_offs"] = np.asarray([r.rows[t].col_offset for t in ts], dtype=np.int64)
+        out[f"b{k}_vals"] = np.concatenate([r.rows[t].values for t in ts])
+        k += 1
+    out["n_b"] = np.asarray(k)
+    k = 0
+    for spec, cut in [(O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024), 32), (O(140.0, 100.0, 0.03, 0.0, 0.5, 60, 4096), 128)]:
+        r = fl.fast_put_bsm(spec, 0.4, base_cutoff=cut, record_rows=True)
+        out[f"f{k}_spec"] = np.array([spec.spot, spec.strike, spec.rate, spec.dividend_yield, spec.volatility,
+                                      spec.days_to_expiry, spec.steps])
+        out[f"f{k}_cut"] = np.asarray(cut)
+        out[f"f{k}_price"] = np.asarray(r.price)
+        out[f"f{k}_times"] = r.boundaries.times
+        out[f"f{k}_cols"] = r.boundaries.columns
+        ts = sorted(r.rows)
+        out[f"f{k}_rtimes"] = np.asarray(ts, dtype=np.int64)
+        out[f"f{k}_roffs"] = np.asarray([r.rows[t].col_offset for t in ts], dtype=np.int64)
+        out[f"f{k}_rlens"] = np.asarray([len(r.rows[t]) for t in ts], dtype=np.int64)
+        out[f"f{k}_rvals"] = np.concatenate([r.rows[t].values for t in ts])
+        k += 1
+    out["n_f"] = np.asarray(k)
+    for n in (1, 8, 1024, 4096):
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        out[f"fft{n}_x"] = x
+        out[f"fft{n}_f"] = fl.fft_forward(x)
+        out[f"fft{n}_i"] = fl.fft_inverse(x)
+    for a, b in [(5, 3), (300, 17), (1000, 1000)]:
+        x = rng.standard_normal(a)
+        y = rng.standard_normal(b)
+        out[f"conv{a}_{b}_x"] = x
+        out[f"conv{a}_{b}_y"] = y
+        out[f"conv{a}_{b}_z"] = fl.convolve(x, y)
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
+    print("api: keep_grid, record_rows, fft cases written")
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     want = lambda k: not which or k in which  # noqa: E731
@@ -267,3 +331,5 @@ if __name__ == "__main__":
         save("c5_fast", stratified_c5(), "fast")
     if want("ops"):
         ops_cases()
+    if want("api"):
+        api_cases()

@@ -151,3 +151,77 @@ def test_batch_helpers():
     assert np.all(status == 0)
     for i in range(32):
         assert price_close(price[i], g.price[i], g.K[i])
+
+
+@pytest.fixture(scope="module")
+def api():
+    return np.load(os.path.join(GOLDEN, "api.npz"))
+
+
+def test_keep_grid(api):
+    import paper_2303_02317_b200 as fl
+
+    for k in range(int(api["n_g"])):
+        S, K, R, Y, V, E, T = api[f"g{k}_spec"]
+        spec = fl.OptionSpec(S, K, R, Y, V, E, int(T))
+        r = fl.baseline_american_call(spec, keep_grid=True)
+        assert price_close(r.price, float(api[f"g{k}_price"]), K)
+        assert np.array_equal(r.boundaries.columns, api[f"g{k}_cols"]), k
+        rows = np.concatenate(r.rows)
+        ref = api[f"g{k}_rows"]
+        assert rows.shape == ref.shape
+        assert np.max(np.abs(rows - ref)) <= 1e-9 * max(1.0, K), k
+        assert np.array_equal(np.concatenate(r.exercise_masks).astype(np.uint8), api[f"g{k}_masks"]), k
+        assert len(r.rows) == int(T) + 1 and all(len(x) == i + 1 for i, x in enumerate(r.rows))
+
+
+def test_baseline_record_rows(api):
+    import paper_2303_02317_b200 as fl
+
+    for k in range(int(api["n_b"])):
+        S, K, R, Y, V, E, T = api[f"b{k}_spec"]
+        spec = fl.OptionSpec(S, K, R, Y, V, E, int(T))
+        times = api[f"b{k}_times"].tolist()
+        r = fl.baseline_put_fd(spec, 0.4, int(T), record_rows=tuple(times) + (0, int(T) + 5))
+        assert price_close(r.price, float(api[f"b{k}_price"]), K)
+        assert np.array_equal(r.boundaries.columns, api[f"b{k}_cols"]), k
+        assert sorted(r.rows) == times
+        vals = np.concatenate([r.rows[t].values for t in times])
+        assert [r.rows[t].col_offset for t in times] == api[f"b{k}_offs"].tolist()
+        assert np.max(np.abs(vals - api[f"b{k}_vals"])) <= 1e-12, k
+
+
+def test_fast_record_rows(api):
+    import paper_2303_02317_b200 as fl
+
+    for k in range(int(api["n_f"])):
+        S, K, R, Y, V, E, T = api[f"f{k}_spec"]
+        spec = fl.OptionSpec(S, K, R, Y, V, E, int(T))
+        r = fl.fast_put_bsm(spec, 0.4, base_cutoff=int(api[f"f{k}_cut"]), record_rows=True)
+        assert price_close(r.price, float(api[f"f{k}_price"]), K)
+        assert np.array_equal(r.boundaries.times, api[f"f{k}_times"])
+        assert np.array_equal(r.boundaries.columns, api[f"f{k}_cols"])
+        ts = sorted(r.rows)
+        assert ts == api[f"f{k}_rtimes"].tolist()
+        assert [r.rows[t].col_offset for t in ts] == api[f"f{k}_roffs"].tolist()
+        assert [len(r.rows[t]) for t in ts] == api[f"f{k}_rlens"].tolist()
+        vals = np.concatenate([r.rows[t].values for t in ts])
+        assert np.max(np.abs(vals - api[f"f{k}_rvals"])) <= 1e-9, k
+
+
+def test_fft_and_convolve(api):
+    import paper_2303_02317_b200 as fl
+
+    for n in (1, 8, 1024, 4096):
+        x = api[f"fft{n}_x"]
+        f = fl.fft_forward(x)
+        assert np.max(np.abs(f - api[f"fft{n}_f"])) <= 1e-12 * max(1.0, np.max(np.abs(api[f"fft{n}_f"])))
+        i = fl.fft_inverse(x)
+        assert np.max(np.abs(i - api[f"fft{n}_i"])) <= 1e-12 * max(1.0, np.max(np.abs(api[f"fft{n}_i"])))
+        assert np.max(np.abs(fl.fft_inverse(fl.fft_forward(x)) - x)) <= 1e-12  # round trip (test_fft.py)
+    for a, b in [(5, 3), (300, 17), (1000, 1000)]:
+        z = fl.convolve(api[f"conv{a}_{b}_x"], api[f"conv{a}_{b}_y"])
+        ref = api[f"conv{a}_{b}_z"]
+        assert z.dtype == np.float64 and z.shape == ref.shape
+        assert np.max(np.abs(z - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+    assert np.allclose(fl.convolve(np.array([1.0, 1.0]), np.array([1.0, 1.0])), [1.0, 2.0, 1.0], atol=1e-15)

@@ -183,10 +183,12 @@ def test_api_argument_checks_before_device():
     with pytest.raises(fl.ValidationError):
         fl.Kernel(np.array([]), 0)
     spec = fl.OptionSpec(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024)
-    with pytest.raises(fl.UnsupportedCombinationError):
-        fl.fast_put_bsm(spec, record_rows=True)
-    with pytest.raises(fl.UnsupportedCombinationError):
-        fl.baseline_american_call(spec, keep_grid=True)
+    with pytest.raises(fl.ValidationError):
+        fl.fft_forward(np.ones(3))
+    with pytest.raises(fl.ValidationError):
+        fl.fft_inverse(np.ones((2, 2)))
+    with pytest.raises(fl.ValidationError):
+        fl.convolve(np.ones(0), np.ones(2))
     disc = fl.discretize_bsm(spec)
     st = fl.initial_row(disc)
     assert st.boundary == 0 and st.segment.first_col == 1 and len(st.segment) == disc.k_star + 1024
