@@ -34,6 +34,8 @@ extern "C" {
 
 #define FL_METHOD_FAST 0     /* fast_european / fast_american_call / fast_put_bsm        */
 #define FL_METHOD_BASELINE 1 /* baseline_european / baseline_american_call / baseline_put_fd */
+#define FL_METHOD_GAUSS 2    /* gaussian_approx_european (fl_euro_approx only)                */
+#define FL_METHOD_CLOSED 3   /* closed_form_european (fl_euro_approx only)                    */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int fl_version(void);
@@ -156,6 +158,13 @@ int fl_put_march_rows(double cd, double cm, double cu, double ds, double K, int6
 int fl_put_fast_rows(double S, double K, double R, double V, double E, int64_t T, double lam, int64_t base_cutoff,
                      double* snap, int64_t snap_cap, int64_t* snap_len, double* price, int32_t* status,
                      int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
+
+/* binomial.py:218 gaussian_approx_european (method FL_METHOD_GAUSS) and
+ * binomial.py:243 closed_form_european (FL_METHOD_CLOSED) for a batch of
+ * European calls; per-option status as fl_price_batch (DomainError for a
+ * degenerate window / non-positive strike). */
+int fl_euro_approx(int64_t n, const double* S, const double* K, const double* R, const double* Y, const double* V,
+                   const double* E, const int64_t* T, int method, double* price, int32_t* status, void* stream);
 
 /* fft.py:84 fft_forward / fft.py:114 fft_inverse: unnormalised power-of-two
  * DFT (inverse with the 1/N factor) of n complex values, interleaved

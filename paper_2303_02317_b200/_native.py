@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 KIND_EURO, KIND_CALL, KIND_PUT = 0, 1, 2
-METHOD_FAST, METHOD_BASELINE = 0, 1
+METHOD_FAST, METHOD_BASELINE, METHOD_GAUSS, METHOD_CLOSED = 0, 1, 2, 3
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_NAME = "libfftlattice_b200.so"
@@ -41,7 +41,7 @@ EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
     "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
-    "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve",
+    "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
     "fl_probe_fp64",
 )
 
@@ -107,6 +107,8 @@ def lib():
         L.fl_fft.restype = c_int
         L.fl_convolve.argtypes = [P, i64, P, i64, P, P]
         L.fl_convolve.restype = c_int
+        L.fl_euro_approx.argtypes = [i64, P, P, P, P, P, P, P, c_int, P, P, P]
+        L.fl_euro_approx.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
         _lib = L
@@ -165,6 +167,10 @@ def status_error(code: int) -> Exception | None:
     if cls == 0x300:
         if det == 1:
             return DomainError("spot lies too many grid nodes from the strike")
+        if det == 3:
+            return DomainError("degenerate Gaussian weight window")
+        if det == 4:
+            return DomainError("strike must be positive for the closed form")
         return DomainError("put grid requires a positive strike")
     if cls == 0x400:
         return GeometryError(f"decomposition failed to tile its region (site {det})")
@@ -436,3 +442,13 @@ def convolve(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     out = np.empty(a.shape[0] + b.shape[0] - 1, dtype=np.complex128)
     _check(lib().fl_convolve(_ptr(a), a.shape[0], _ptr(b), b.shape[0], _ptr(out), None))
     return out
+
+
+def euro_approx(S, K, R, Y, V, E, T, method):
+    """fl_euro_approx: (price, status) for METHOD_GAUSS / METHOD_CLOSED."""
+    n, _, S, K, R, Y, V, E, T = _inputs(0, S, K, R, Y, V, E, T)
+    price = np.empty(n)
+    status = np.empty(n, dtype=np.int32)
+    _check(lib().fl_euro_approx(n, _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), int(method),
+                                _ptr(price), _ptr(status), None))
+    return price, status

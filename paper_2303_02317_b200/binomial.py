@@ -28,6 +28,8 @@ __all__ = [
     "baseline_european",
     "baseline_american_call",
     "fast_european",
+    "gaussian_approx_european",
+    "closed_form_european",
     "price_european_batch",
 ]
 
@@ -87,3 +89,30 @@ def price_european_batch(S, K, R, Y, V, E, T, *, method: str = "fast"):
     """Batched European calls (one device call).  Returns (price, status)."""
     m = _pricing.FAST if method == "fast" else _pricing.BASELINE
     return _pricing.price_many(np.int8(_pricing.KIND_EURO), S, K, R, Y, V, E, T, method=m)
+
+
+def _euro_approx(spec: OptionSpec, params: BinomialParams | None, method: int) -> float:
+    from . import _native
+
+    _pricing.check_params(spec, params)
+    S, K, R, Y, V, E, T = _pricing.spec_arrays([spec])
+    price, status = _native.euro_approx(S, K, R, Y, V, E, T, method)
+    err = _native.status_error(int(status[0]))
+    if err is not None:
+        raise err
+    return float(price[0])
+
+
+def gaussian_approx_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
+    """European call with the composed weights replaced by their normal limit,
+    summed over a six-sigma window on the device (binomial.py:197-240)."""
+    from . import _native
+
+    return _euro_approx(spec, params, _native.METHOD_GAUSS)
+
+
+def closed_form_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
+    """Closed form of the normal-limit price, on the device (binomial.py:243-296)."""
+    from . import _native
+
+    return _euro_approx(spec, params, _native.METHOD_CLOSED)

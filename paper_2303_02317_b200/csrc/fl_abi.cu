@@ -743,6 +743,40 @@ int fl_put_fast_rows(double S, double K, double R, double V, double E, int64_t T
   return rc;
 }
 
+int fl_euro_approx(int64_t n, const double* S, const double* K, const double* R, const double* Y, const double* V,
+                   const double* E, const int64_t* T, int method, double* price, int32_t* status, void* stream) {
+  if (n < 0 || !S || !K || !R || !Y || !V || !E || !T || !price || !status) return fail("fl_euro_approx: null pointer");
+  if (method != FL_METHOD_GAUSS && method != FL_METHOD_CLOSED) return fail("fl_euro_approx: unknown method");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  FL_CUDA(ensure_device_init(dev, st));
+  std::vector<fl::EuroApprox> ok;
+  std::vector<int64_t> idx;
+  for (int64_t i = 0; i < n; ++i) {
+    fl::EuroApprox a{};
+    const fl::SpecIn s{S[i], K[i], R[i], Y[i], V[i], E[i], T[i]};
+    status[i] = fl::prep_euro_approx(s, method, a);
+    price[i] = 0.0;
+    if (!status[i]) { ok.push_back(a); idx.push_back(i); }
+  }
+  if (ok.empty()) return 0;
+  const int m = (int)ok.size();
+  DevBuf d_opts, d_price;
+  FL_CUDA(d_opts.ensure(sizeof(fl::EuroApprox) * m));
+  FL_CUDA(d_price.ensure(sizeof(double) * m));
+  std::vector<double> out(m);
+  cudaError_t e = cudaMemcpyAsync(d_opts.p, ok.data(), sizeof(fl::EuroApprox) * m, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = fl::launch_euro_approx(d_opts.as<fl::EuroApprox>(), m, method, d_price.as<double>(), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out.data(), d_price.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  d_opts.release();
+  d_price.release();
+  if (e != cudaSuccess) return fail(std::string("fl_euro_approx: ") + cudaGetErrorString(e));
+  for (int k = 0; k < m; ++k) price[idx[k]] = out[k];
+  return 0;
+}
+
 int fl_fft(const double* in, int64_t n, int inverse, double* out, void* stream) {
   if (!in || !out) return fail("fl_fft: null pointer");
   if (n < 1 || (n & (n - 1)) != 0) return fail("fl_fft: length must be a power of two");

@@ -184,4 +184,54 @@ cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, i
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Normal-limit approximations (binomial.py:197-296).  One CTA per option for
+// the Gaussian window sum (fixed-order tree reduction), one thread per option
+// for the closed form.
+
+__global__ void __launch_bounds__(CTA_THREADS)
+euro_gauss_kernel(const EuroApprox* __restrict__ opts, int n_opts, double* __restrict__ price) {
+  __shared__ double red[CTA_THREADS];
+  const int o = blockIdx.x;
+  if (o >= n_opts) return;
+  const EuroApprox A = opts[o];
+  double acc = 0.0;
+  const double norm = sqrt(2.0 * 3.141592653589793 * A.sigma);
+  for (int64_t x = A.lo + threadIdx.x; x <= A.hi; x += CTA_THREADS) {
+    const double xd = (double)x;
+    const double dens = exp(-((xd + A.mu) * (xd + A.mu)) / (2.0 * A.sigma)) / norm;
+    double leaf = A.S * exp((2.0 * xd - (double)A.n) * A.lu) - A.K;
+    leaf = leaf > 0.0 ? leaf : 0.0;
+    acc = fma(dens, leaf, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = CTA_THREADS / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) price[o] = A.disc * red[0];
+}
+
+__global__ void euro_closed_kernel(const EuroApprox* __restrict__ opts, int n_opts, double* __restrict__ price) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n_opts) return;
+  const EuroApprox A = opts[o];
+  if (A.x0 > A.n) { price[o] = 0.0; return; }
+  const double root = sqrt(2.0 * A.sigma);
+  const double n = (double)A.n, x0 = (double)A.x0;
+  const double bn = (n + A.mu) / root, bx = (x0 + A.mu) / root;
+  const double an = bn - A.lu * root, ax = bx - A.lu * root;
+  const double spot_leg = A.S * exp(A.lu * (2.0 * A.sigma * A.lu - 2.0 * A.mu - n)) * (erf(an) - erf(ax));
+  const double strike_leg = A.K * (erf(bn) - erf(bx));
+  price[o] = 0.5 * A.disc * (spot_leg - strike_leg);
+}
+
+cudaError_t launch_euro_approx(const EuroApprox* opts, int n_opts, int method, double* price, cudaStream_t stream) {
+  if (n_opts <= 0) return cudaSuccess;
+  if (method == 2) euro_gauss_kernel<<<n_opts, CTA_THREADS, 0, stream>>>(opts, n_opts, price);
+  else euro_closed_kernel<<<(n_opts + 127) / 128, 128, 0, stream>>>(opts, n_opts, price);
+  return cudaGetLastError();
+}
+
 }  // namespace fl

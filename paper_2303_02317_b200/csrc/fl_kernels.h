@@ -75,6 +75,9 @@ cudaError_t launch_put_march_rows(const PutParams& P, const int64_t* times, int 
 cudaError_t launch_call_grid(const CallParams& P, double* rows, uint8_t* masks, int64_t* cols, double* price,
                              double* ws, cudaStream_t stream);
 
+// European normal-limit approximations (fl_euro.cu); method 2 Gaussian, 3 closed form
+cudaError_t launch_euro_approx(const EuroApprox* opts, int n_opts, int method, double* price, cudaStream_t stream);
+
 // generic transform utilities (fl_fft.cu)
 cudaError_t fft_pow2(double2* buf, double2* tmp, int64_t n, int sign, double2** result, cudaStream_t stream);
 cudaError_t launch_cmul(double2* a, const double2* b, int64_t n, double scale, cudaStream_t stream);

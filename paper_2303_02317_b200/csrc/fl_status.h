@@ -37,5 +37,7 @@
 /* DomainError details */
 #define FL_D_GRID_NODES 1 /* bsm.py:185-189 */
 #define FL_D_STRIKE 2     /* bsm.py:165-166 */
+#define FL_D_WINDOW 3     /* binomial.py:212-215 degenerate Gaussian window */
+#define FL_D_CF_STRIKE 4  /* binomial.py:265-269 closed form needs a positive strike */
 
 #endif

@@ -182,6 +182,40 @@ inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroPar
   return FL_OK;
 }
 
+// European normal-limit approximations (binomial.py:197-296)
+struct EuroApprox {
+  double S, K, lu, mu, sigma, disc;  // disc = exp(-R * years)
+  int64_t n, lo, hi, x0;             // Gaussian window [lo, hi]; closed-form threshold x0
+  int32_t method, pad;               // 2: Gaussian window sum, 3: closed form
+};
+
+inline int32_t prep_euro_approx(const SpecIn& s, int method, EuroApprox& a) {
+  Binom b;
+  int32_t st = derive_binomial(s, b);
+  a.S = s.S; a.K = s.K; a.n = s.T; a.method = method; a.pad = 0;
+  a.lo = a.hi = a.x0 = 0;
+  if (st) return st;
+  const int64_t n = s.T;
+  a.lu = b.lu;
+  a.mu = -b.p * (double)n;
+  a.sigma = b.p * (1.0 - b.p) * (double)n;
+  a.disc = std::exp(-s.R * (s.E / DAYS_PER_YEAR));
+  if (method == 2) {  // _gaussian_window (binomial.py:197-215)
+    const double center = -a.mu;
+    const double lo = std::ceil(center - 6.0 * std::sqrt(a.sigma));
+    const double hi = std::floor(center + 6.0 * std::sqrt(a.sigma));
+    a.lo = lo > 0.0 ? (int64_t)lo : 0;
+    a.hi = hi < (double)(n - 1) ? (int64_t)hi : n - 1;
+    if (a.lo > a.hi) return FL_E_DOMAIN | FL_D_WINDOW;
+  } else {  // closed_form_european (binomial.py:243-296)
+    if (s.K <= 0.0) return FL_E_DOMAIN | FL_D_CF_STRIKE;
+    const double threshold = 0.5 * (double)n + std::log(s.K / s.S) / (2.0 * b.lu);
+    const double x0 = std::ceil(threshold);
+    a.x0 = x0 > (double)n ? n + 1 : (x0 < 0.0 ? 0 : (int64_t)x0);
+  }
+  return FL_OK;
+}
+
 struct PutDisc {
   int64_t n, ks;
   double omega, tau_max, d_tau, d_s, cd, cm, cu;

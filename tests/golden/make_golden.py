@@ -302,6 +302,22 @@ def api_cases():
         out[f"conv{a}_{b}_x"] = x
         out[f"conv{a}_{b}_y"] = y
         out[f"conv{a}_{b}_z"] = fl.convolve(x, y)
+    # European normal-limit approximations (binomial.py:197-296), incl. their DomainErrors
+    specs = [O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024), O(100.0, 95.0, 0.03, 0.05, 0.25, 180, 16384),
+             O(120.0, 100.0, 0.04, 0.02, 0.35, 300, 4096), O(80.0, 110.0, 0.02, 0.04, 0.45, 90, 65536),
+             O(100.0, 0.0, 0.05, 0.0, 0.2, 365, 64), O(100.0, 300.0, 0.05, 0.0, 0.1, 10, 64),
+             O(100.0, 100.0, 0.05, 0.0, 0.2, 365, 2)]
+    vals = []
+    for spec in specs:
+        row = [spec.spot, spec.strike, spec.rate, spec.dividend_yield, spec.volatility, spec.days_to_expiry,
+               spec.steps]
+        for fn in (fl.gaussian_approx_european, fl.closed_form_european):
+            try:
+                row.append(fn(spec))
+            except fl.DomainError:
+                row.append(np.nan)
+        vals.append(row)
+    out["approx"] = np.asarray(vals)
     np.savez_compressed(os.path.join(HERE, "api.npz"), **out)
     print("api: keep_grid, record_rows, fft cases written")
 

@@ -225,3 +225,17 @@ def test_fft_and_convolve(api):
         assert z.dtype == np.float64 and z.shape == ref.shape
         assert np.max(np.abs(z - ref)) <= 1e-12 * max(1.0, np.max(np.abs(ref)))
     assert np.allclose(fl.convolve(np.array([1.0, 1.0]), np.array([1.0, 1.0])), [1.0, 2.0, 1.0], atol=1e-15)
+
+
+def test_european_approximations(api):
+    import paper_2303_02317_b200 as fl
+
+    for row in api["approx"]:
+        S, K, R, Y, V, E, T, g_ref, c_ref = row
+        spec = fl.OptionSpec(S, K, R, Y, V, E, int(T))
+        for fn, ref in ((fl.gaussian_approx_european, g_ref), (fl.closed_form_european, c_ref)):
+            if np.isnan(ref):
+                with pytest.raises(fl.DomainError):
+                    fn(spec)
+            else:
+                assert price_close(fn(spec), ref, K), (fn.__name__, row)
