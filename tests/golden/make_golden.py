@@ -322,6 +322,52 @@ def api_cases():
     print("api: keep_grid, record_rows, fft cases written")
 
 
+def batch_case():
+    """A portfolio CSV exercising every combination and error column, with the
+    reference's own cmd_batch output (cli.py:797-842)."""
+    import argparse
+    import contextlib
+    import io
+
+    from fftlattice import cli
+
+    rows = [
+        "european,call,binomial,fast,100,100,0.05,0,0.2,365,1024,",
+        "european,call,binomial,baseline,100,95,0.03,0.05,0.25,180,512,",
+        "european,call,binomial,gaussian,120,100,0.04,0.02,0.35,300,4096,",
+        "european,call,binomial,closed-form,80,110,0.02,0.04,0.45,90,16384,",
+        "american,call,binomial,fast,100,90,0.03,0.07,0.25,365,512,",
+        "american,call,binomial,baseline,150,80,0.09,0.05,0.15,365,300,",
+        "american,put,bsm,fast,100,100,0.05,0,0.2,365,1024,0.4",
+        "american,put,bsm,baseline,90,110,0.06,0,0.35,500,400,",
+        "american,put,bsm,fast,140,100,0.03,0,0.5,60,4096,0.3",
+        "american,put,bsm,fast,100,100,0.05,0,0.2,365,1024,0.9",   # StabilityError -> lambda
+        "american,put,bsm,fast,100,100,0.05,0,0.2,365,1024,abc",   # unparsable lambda
+        "american,put,bsm,fast,100,100,0.05,0,0.2,365,1024,0",     # lam must be positive
+        "american,put,bsm,fast,100,0,0.05,0,0.2,365,64,",          # DomainError -> S
+        "american,put,bsm,fast,100,100,0.05,-1,0.2,365,64,",       # ValidationError dividend -> Y
+        "american,call,bsm,fast,100,100,0.05,0,0.2,365,64,",       # unsupported combination
+        "european,call,binomial,fast,100,100,0.05,0,0.2,365.5,64,",  # E not an int
+        "european,call,binomial,fast,-1,100,0.05,0,0.2,365,64,",   # spot
+        "european,call,binomial,fast,100,100,0.9,0,0.01,365,4,",   # prob_up -> T? (field prob_up)
+        "european,call,binomial,gaussian,100,100,0.05,0,0.2,365,2,",
+        "european,call,binomial,closed-form,100,0,0.05,0,0.2,365,64,",
+        "american,call,binomial,fast,100,95,0.04,0.06,0.3,365,200,",
+        "european,call,binomial,fast,100,100,0.05,0,0.2,365",      # short row
+        "european,call,binomial,fast,100,100,0.05,0,0.2,365,64,,x",  # long row
+    ]
+    text = "style,right,model,method,S,K,R,Y,V,E,T,lambda\n" + "\n".join(rows) + "\n"
+    path = os.path.join(HERE, "portfolio.csv")
+    with open(path, "w") as fh:
+        fh.write(text)
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = cli.cmd_batch(argparse.Namespace(csv=path, parallel=False))
+    with open(os.path.join(HERE, "portfolio_ref.csv"), "w") as fh:
+        fh.write(buf.getvalue())
+    print(f"batch: {len(rows)} rows, reference exit code {rc}")
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     want = lambda k: not which or k in which  # noqa: E731
@@ -349,3 +395,5 @@ if __name__ == "__main__":
         ops_cases()
     if want("api"):
         api_cases()
+    if want("batch"):
+        batch_case()
