@@ -53,7 +53,25 @@ constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP);
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
 enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3 };
 
+#ifndef FL_LAYOUT
+#define FL_LAYOUT 0
+#endif
 __device__ __forceinline__ int warp_role(int w, int* rank) {
+#if FL_LAYOUT == 1
+  // SMSP-aware: SMSP 0 / 1 hold one chain each plus the OTHER chain's helpers
+  // (a chain and its own helpers never compete for one issue port), the FFT
+  // groups (steady issuers) live on SMSP 2 / 3
+  static_assert(NCHAIN == 2 && NHELP == 3 && SCHED_WARPS == 16, "layout 1 shape");
+  const int smsp = w & 3, slot = w >> 2;
+  if (smsp < 2) {
+    if (slot == 0) { *rank = smsp; return ROLE_CHAIN; }
+    *rank = (1 - smsp) * NHELP + (slot - 1);
+    return ROLE_HELPER;
+  }
+  if (slot < 2) { *rank = slot * 2 + (smsp - 2); return ROLE_BIG; }
+  *rank = (slot - 2) * 2 + (smsp - 2);
+  return ROLE_MED;
+#endif
   constexpr int C0 = 2 * GROUP_WARPS, H0 = C0 + NCHAIN;
   if (w >= H0) { *rank = w - H0; return ROLE_HELPER; }  // helper rank: chain = rank / NHELP
   if (w >= C0) { *rank = w - C0; return ROLE_CHAIN; }
