@@ -33,57 +33,37 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
   const int lane = threadIdx.x & 31;
   double v[CPL], p[CPL];
   const int64_t c0 = lo + (int64_t)lane * CPL;
-  // unconditional loads at clamped (always valid) columns, all in flight at
-  // once; the selects below discard what is outside the strip
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     const int64_t col = c0 + c;
-    const int64_t cc = col < hi ? col : hi;
-    p[c] = pay_org[cc];
-    v[c] = in_org[cc > f ? cc : f + 1];
-  }
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    const int64_t col = c0 + c;
-    v[c] = (col > hi) ? 0.0 : (col <= f) ? p[c] : v[c];
-    p[c] = (col > hi) ? 0.0 : p[c];
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
   }
   unsigned green = 0;
   long long ta = 0;
   __syncwarp();
   if (tm) { ta = clock64() + (long long)(v[0] + p[0] == 12345.678 ? 1 : 0); }
-  // the shuffled neighbour enters last: one DFMA between a shuffle and the
-  // next row's shuffle on the warp's critical path; the green mask is formed
-  // on the final row only
+  for (int s = 1; s <= height; ++s) {
+    const double left = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double right = __shfl_down_sync(FULL, v[0], 1);
+    double nv[CPL];
+    green = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double l = (c == 0) ? left : v[c - 1];
+      const double r = (c == CPL - 1) ? right : v[c + 1];
+      // the shuffled neighbour enters last: one DFMA between a shuffle and the
+      // next row's shuffle on the warp's critical path
 #if FL_STRIP_ORDER
-#define FL_STRIP_LIN(c, l, r) \
-  ((c) == CPL - 1 ? fma(cu, (r), fma(cd, (l), cm * v[c])) : fma(cd, (l), fma(cu, (r), cm * v[c])))
+      const double lin = (c == CPL - 1) ? fma(cu, r, fma(cd, l, cm * v[c])) : fma(cd, l, fma(cu, r, cm * v[c]));
 #else
-#define FL_STRIP_LIN(c, l, r) fma(cd, (l), fma(cu, (r), cm * v[c]))
+      const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
 #endif
-  for (int s = 1; s < height; ++s) {
-    const double left = __shfl_up_sync(FULL, v[CPL - 1], 1);
-    const double right = __shfl_down_sync(FULL, v[0], 1);
-    double nv[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const double l = (c == 0) ? left : v[c - 1];
-      const double r = (c == CPL - 1) ? right : v[c + 1];
-      const double lin = FL_STRIP_LIN(c, l, r);
-      nv[c] = lin > p[c] ? lin : p[c];
-    }
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
-  }
-  if (height >= 1) {  // final row
-    const double left = __shfl_up_sync(FULL, v[CPL - 1], 1);
-    const double right = __shfl_down_sync(FULL, v[0], 1);
-    double nv[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const double l = (c == 0) ? left : v[c - 1];
-      const double r = (c == CPL - 1) ? right : v[c + 1];
-      const double lin = FL_STRIP_LIN(c, l, r);
       const bool red = lin > p[c];
       nv[c] = red ? lin : p[c];
       green |= (red ? 0u : 1u) << c;
@@ -91,7 +71,6 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
 #pragma unroll
     for (int c = 0; c < CPL; ++c) v[c] = nv[c];
   }
-#undef FL_STRIP_LIN
   if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
   // last green inside the final valid range [lo+height, hi-height]
   const int64_t vlo = lo + height, vhi = hi - height;
