@@ -434,7 +434,10 @@ def call_fast(S, K, R, Y, V, E, T, base_cutoff=256):
     times.append(i)
     bounds.append(_first_green(i, j))
     if j < 0:
-        return S - K, np.asarray(times, dtype=np.int64), np.asarray(bounds, dtype=np.int64)
+        # american.py:478-486 returns BoundarySeries(times=[n, n-1], ...) here,
+        # whose constructor rejects non-increasing times (model.py:318-328): the
+        # reference raises ValidationError('times') for an all-exercise row T-1
+        raise OracleError("ValidationError", "times")
     resid = math.isqrt(n - 1) + 1
     ctx = _CallCtx(S, K, p, base_cutoff)
     while i > resid and j >= 0:

@@ -133,7 +133,7 @@ def _ptr(a: np.ndarray):
 # status codes (csrc/fl_status.h)
 
 _FIELDS = {1: "spot", 2: "strike", 3: "rate", 4: "dividend_yield", 5: "volatility",
-           6: "days_to_expiry", 7: "steps", 8: "prob_up", 9: "lam", 10: "base_cutoff"}
+           6: "days_to_expiry", 7: "steps", 8: "prob_up", 9: "lam", 10: "base_cutoff", 11: "times"}
 _FIELD_MSG = {
     "spot": "spot must be positive and finite",
     "strike": "strike must be nonnegative and finite",
@@ -146,6 +146,7 @@ _FIELD_MSG = {
                "increase steps or volatility",
     "lam": "lambda must be positive",
     "base_cutoff": "base_cutoff must be >= 1",
+    "times": "times must be strictly increasing",
 }
 _WEIGHTS = {1: ("coef_mid", "centre weight is negative; choose a smaller lambda"),
             2: ("coef_up", "upper weight is negative; increase steps or adjust lambda"),

@@ -28,6 +28,7 @@
 #define FL_F_PROB_UP 8
 #define FL_F_LAM 9
 #define FL_F_CUTOFF 10
+#define FL_F_TIMES 11  /* model.py:318-328 via american.py:478-486 (all-exercise row T-1) */
 
 /* StabilityError weights (bsm.py:204-222) */
 #define FL_W_MID 1

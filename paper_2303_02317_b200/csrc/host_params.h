@@ -177,7 +177,10 @@ inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroPar
   st = call_junction_boundary(s, b, c.top_b, j);
   if (st) { c.mode = MODE_ERROR; return st; }
   c.junc_j = j;
-  if (j < 0) { c.mode = MODE_INTRINSIC; c.price = s.S - s.K; return FL_OK; }
+  // all-exercise row T-1: the reference builds BoundarySeries(times=[T, T-1])
+  // here (american.py:478-486), which its constructor rejects -> it raises
+  // ValidationError('times'); mirrored (the price would be S - K)
+  if (j < 0) { c.mode = MODE_ERROR; c.price = s.S - s.K; return FL_E_VALIDATION | FL_F_TIMES; }
   c.mode = MODE_FAST;
   return FL_OK;
 }
