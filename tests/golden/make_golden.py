@@ -368,6 +368,22 @@ def batch_case():
     print(f"batch: {len(rows)} rows, reference exit code {rc}")
 
 
+def verify_case():
+    """The reference's own verify output (cli.py:598-616) for a fixed seed."""
+    import argparse
+    import contextlib
+    import io
+
+    from fftlattice import cli
+
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = cli.cmd_verify(argparse.Namespace(reps=6, steps=1024, seed=3))
+    with open(os.path.join(HERE, "verify_ref.txt"), "w") as fh:
+        fh.write(buf.getvalue())
+    print(f"verify: reference exit code {rc}")
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     want = lambda k: not which or k in which  # noqa: E731
@@ -397,3 +413,5 @@ if __name__ == "__main__":
         api_cases()
     if want("batch"):
         batch_case()
+    if want("verify"):
+        verify_case()
