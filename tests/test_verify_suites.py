@@ -41,3 +41,35 @@ def test_verify_argument_errors():
     with pytest.raises(fl.ValidationError):
         verify.run_suites(reps=2, steps=10)
     assert verify.run_suites(reps=0) == 0
+
+
+def test_benchcsv_argument_errors():
+    import paper_2303_02317_b200 as fl
+    from paper_2303_02317_b200 import benchcsv
+
+    spec = fl.OptionSpec(100.0, 100.0, 0.05, 0.03, 0.2, 365, 1)
+    with pytest.raises(fl.UnsupportedCombinationError):
+        benchcsv.bench_records(["nope"], "64", 1, spec)
+    with pytest.raises(fl.ValidationError):
+        benchcsv.bench_records(["fast_put"], "x", 1, spec)
+    with pytest.raises(fl.ValidationError):
+        benchcsv.bench_records(["fast_put"], "64", 0, spec)
+
+
+@pytest.mark.gpu
+def test_benchcsv_schema_and_prices():
+    import csv as _csv
+
+    from paper_2303_02317_b200 import benchcsv
+
+    out = io.StringIO()
+    import contextlib
+
+    with contextlib.redirect_stdout(out):
+        rc = benchcsv.main(["--method", ",".join(benchcsv.BENCH_METHODS), "--steps", "300,1024", "--reps", "2"])
+    assert rc == 0
+    rows = list(_csv.reader(io.StringIO(out.getvalue())))
+    assert rows[0] == ["method", "T", "seconds", "price", "reps"]
+    assert len(rows) == 1 + 2 * len(benchcsv.BENCH_METHODS)
+    for r in rows[1:]:
+        assert float(r[2]) > 0.0 and float(r[3]) == float(r[3]) and r[4] == "2"
