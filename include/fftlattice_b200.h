@@ -104,6 +104,9 @@ void fl_batch_free(fl_batch* b);
  * environment at run time; zeros otherwise): 56 uint64 slots, see PROF_* in
  * csrc/fl_sched.cuh. */
 int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream);
+/* Per-work-item timeline of the last fast run (FL_PROFILE set): 3 uint64 per
+ * work item in scheduling (decreasing-cost) order: start ns, end ns, SM << 1 | chain. */
+int fl_batch_timeline(fl_batch* b, uint64_t* out3n, void* stream);
 
 /* Batched valid-mode composed-stencil correlation (fft.py:263 apply_linear_steps,
  * american.py:180 / bsm.py:384 _valid_corr), on host buffers:

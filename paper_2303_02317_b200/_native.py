@@ -39,7 +39,7 @@ _lib = None
 #: Every symbol include/fftlattice_b200.h declares.
 EXPORTED_SYMBOLS = (
     "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
-    "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_free",
+    "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_timeline", "fl_batch_free",
     "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
     "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
     "fl_probe_fp64",
@@ -89,6 +89,8 @@ def lib():
         L.fl_batch_stats.restype = c_int
         L.fl_batch_profile.argtypes = [P, P, P]
         L.fl_batch_profile.restype = c_int
+        L.fl_batch_timeline.argtypes = [P, P, P]
+        L.fl_batch_timeline.restype = c_int
         L.fl_inspect.argtypes = [i64, P, P, P, P, P, P, P, P, d, i64, i64, P, P, P, P]
         L.fl_inspect.restype = c_int
         L.fl_batch_ref_flops.argtypes = [P, P, P]
@@ -246,6 +248,12 @@ class DeviceBatch:
         """Scheduler profile counters of the last run (FL_PROFILE=1 at run time)."""
         out = np.zeros(56, dtype=np.uint64)
         _check(lib().fl_batch_profile(self._h, _ptr(out), ctypes.c_void_p(stream) if stream else None))
+        return out
+
+    def timeline(self, stream=None) -> np.ndarray:
+        """(n, 3) per work item of the last run: start ns, end ns, SM << 1 | chain (FL_PROFILE=1)."""
+        out = np.zeros((self.n, 3), dtype=np.uint64)
+        _check(lib().fl_batch_timeline(self._h, _ptr(out), ctypes.c_void_p(stream) if stream else None))
         return out
 
     def launches(self) -> int:

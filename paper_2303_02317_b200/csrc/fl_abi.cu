@@ -274,7 +274,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
   if (b->need_put) FL_CUDA(b->d_put.ensure(sizeof(fl::PutParams) * n));
   if (b->need_call) FL_CUDA(b->d_call.ensure(sizeof(fl::CallParams) * n));
   if (b->need_euro) FL_CUDA(b->d_euro.ensure(sizeof(fl::EuroParams) * n));
-  FL_CUDA(b->d_stats.ensure(64 * sizeof(unsigned long long)));
+  FL_CUDA(b->d_stats.ensure((64 + 3 * n) * sizeof(unsigned long long)));  // counters | timeline
   // orders packed into one buffer
   size_t off = 0;
   auto place = [&](const std::vector<int32_t>& v, size_t& o) { o = off; off += v.size(); };
@@ -837,6 +837,25 @@ int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
   FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return 0;
 }
+
+int fl_batch_timeline(fl_batch* b, uint64_t* out3n, void* stream) {
+  if (!b || !out3n) return fail("fl_batch_timeline: null argument");
+  FL_CUDA(cudaMemcpyAsync(out3n, b->d_stats.as<unsigned long long>() + 64, 3 * b->n * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+#if FL_TRACE
+// Tool-only (FL_TRACE builds): copy the chain event trace of the last run and reset it.
+int fl_trace_read(uint64_t* out, int64_t cap) {
+  FL_CUDA(cudaDeviceSynchronize());
+  FL_CUDA(cudaMemcpyFromSymbol(out, fl::g_trace, (size_t)cap * sizeof(uint64_t)));
+  static const unsigned long long zero = 0;
+  FL_CUDA(cudaMemcpyToSymbol(fl::g_trace, &zero, sizeof(zero)));
+  return 0;
+}
+#endif
 
 int fl_probe_fp64(double* tflops, void* stream) {
   if (!tflops) return fail("fl_probe_fp64: null output");

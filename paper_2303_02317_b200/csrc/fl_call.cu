@@ -213,7 +213,8 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   double* s_in = X.scratch + CSUB_IN;
   warp_stage(s_in, in_org + lo0, h0);
   long long twait = 0;
-  CallSubFrame stk[5];
+  static_assert(sizeof(CallSubFrame) * 5 <= FRAME_SOLVE_OFF - FRAME_SUB_OFF, "subtree frames");
+  CallSubFrame* stk = chain_frames<CallSubFrame>(X.scratch, FRAME_SUB_OFF);
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in = s_in - lo0; stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
@@ -283,7 +284,9 @@ __device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int6
 // vals = in_org[j-h+1 .. j]; writes out_org[j-h+1 .. jp]; returns jp.
 __device__ int64_t call_solve(CallChainCtx& X, const CallParams& P, int64_t i0, int64_t j0, int h0, double* in_org,
                               double* out_org, int32_t* err) {
-  CallFrame stk[CALL_MAX_DEPTH];
+  static_assert(FRAME_SOLVE_OFF + sizeof(CallFrame) * CALL_MAX_DEPTH <= CHAIN_FRAME_DOUBLES * sizeof(double),
+                "recursion frames");
+  CallFrame* stk = chain_frames<CallFrame>(X.scratch, FRAME_SOLVE_OFF);
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
   stk[0].arena = 0; stk[0].state = 0;
   int sp = 1;

@@ -38,6 +38,9 @@ namespace fl {
 #define FL_PUT_LEAF 32
 #endif
 constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
+#ifndef FL_STRIP_PIPE  // 1: leaf strips with the software-pipelined neighbour exchange
+#define FL_STRIP_PIPE 1
+#endif
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
@@ -126,6 +129,7 @@ struct PutChainCtx {
                       // share assembled-row memory (no false WAR dependencies between them)
   const double* pay_org;
   double* scratch;   // chain's shared scratch (CHAIN_SCRATCH doubles)
+  double* wst;       // chain's weight stash (shared)
   int64_t ref_cut;   // the reference's base_cutoff (work accounting only)
   double flops;      // executed chain-side flops (lane-uniform)
   double ref_flops;  // reference-algorithmic flops (lane-uniform)
@@ -149,8 +153,15 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
                                             int64_t f, int height) {
   const long long t1 = clock64();
   long long tm[2] = {0, 0};
+  FL_TR(*X.S, X.c, EV_LEAF_B, height);
+#if FL_STRIP_PIPE
+  const int64_t kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
+                                             X.prof ? tm : nullptr);
+#else
   const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
                                              X.prof ? tm : nullptr);
+#endif
+  FL_TR(*X.S, X.c, EV_LEAF_E, height);
   if (X.prof && lane_id() == 0) {
     prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
     prof_add(X.prof, PROF_STRIP_N, height);
@@ -159,6 +170,29 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   }
   X.flops += ref_strip_flops(hi - lo + 1, height);
   return kb;
+}
+
+
+// Make the weights of every correlation of a subtree rooted at height h0
+// resident in the stash (bsm.py:484-496 use W_{h1}, W_{h2} of each node's children).
+__device__ void put_stash_weights(PutChainCtx& X, int h0) {
+  for (int d = 1; d <= 3; ++d) {
+    const int pmax = (h0 + (1 << (d - 1)) - 1) >> (d - 1);  // tallest node at depth d-1
+    if (pmax <= PUT_LEAF) break;                            // depth d-1 is all leaves
+    const int lo = h0 >> d, hi = (h0 + (1 << d) - 1) >> d;
+    const int key = X.S->wkey[X.c][d];
+    if (key >= 0 && lo >= key && hi <= key + 1) continue;
+    for (int j = 0; j < 2; ++j) {
+      const int m = lo + j;
+      if (m > KT_H) break;
+      warp_stage_nb<9>(X.wst + wst_off(d) + j * wst_sz(d), X.kc + (int64_t)m * m, 2 * m + 1, 2 * m + 1);
+    }
+    if (lane_id() == 0) X.S->wkey[X.c][d] = lo;
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ const double* put_wslot(const PutChainCtx& X, int d, int m) {
+  return X.wst + wst_off(d) + (m - X.S->wkey[X.c][d]) * wst_sz(d);
 }
 
 struct SubFrame {
@@ -173,23 +207,31 @@ struct SubFrame {
 // (bsm.py:443-501 below this node): input cols f0+1..f0+2h0 of in_org, output
 // cols kp+1..f0+h0 of out_org.  The input row and the payoff of cols
 // f0-2h0-1..f0+2h0 are staged once; the chain walks the subtree running the
-// leaf strips, while its helper warp runs every mid / bottom correlation from
+// leaf strips, while its helper warps run every mid / bottom correlation from
 // shared memory (a node's mid overlaps its first child, its bottom its second).
+// The explicit frame stack lives in shared memory (one copy per warp): frames
+// in registers (a compile-time recursion) measured slower -- the live frames
+// push the leaf strip into register spills.
 __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
                                double* out_org, int h0, int ph0, int32_t* err) {
   const long long t0 = clock64();
+  FL_TR(*X.S, X.c, EV_SUB_B, h0);
   wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
                  U(out_org + f0 + h0 + 1));
   const long long t1 = clock64();
+  FL_TR(*X.S, X.c, EV_STG_B, 0);
   double* s_pay = X.scratch + SUB_PAY;
   double* s_in = X.scratch + SUB_IN;
   const int64_t plo = f0 - 2 * (int64_t)h0 - 1;
   warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
   warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
   const double* pay_s = s_pay - plo;
+  if (h0 > PUT_LEAF) put_stash_weights(X, h0);
   const long long t2 = clock64();
+  FL_TR(*X.S, X.c, EV_STG_E, 0);
   long long twait = 0, tpost = 0;
-  SubFrame stk[SUB_DEPTH];
+  static_assert(sizeof(SubFrame) * SUB_DEPTH <= FRAME_SOLVE_OFF - FRAME_SUB_OFF, "subtree frames");
+  SubFrame* stk = chain_frames<SubFrame>(X.scratch, FRAME_SUB_OFF);
   stk[0].f = f0; stk[0].h = h0; stk[0].in = s_in - (f0 + 1); stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
@@ -211,7 +253,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
       const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, X.kc + (int64_t)h1 * h1, Mmid,
+      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, put_wslot(X, sp, h1), Mmid,
                          &F.tk0);
       tpost += clock64() - tp;
       X.flops += 2.0 * Lmid * Mmid;
@@ -230,7 +272,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       ref_node_bottom(X, h, A);
       const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, X.kc + (int64_t)h2 * h2, Mbot,
+      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, put_wslot(X, sp, h2), Mbot,
                          &F.tk0);
       tpost += clock64() - tp;
       X.flops += 2.0 * Lbot * Mbot;
@@ -254,6 +296,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
     prof_add(X.prof, PROF_FUSE_N, 1);
   }
+  FL_TR(*X.S, X.c, EV_SUB_E, h0);
   return ret;
 }
 
@@ -265,7 +308,9 @@ __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
 __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, double* in_org, double* out_org,
                                int h0, int32_t* err) {
-  PutFrame stk[PUT_MAX_DEPTH];
+  static_assert(FRAME_SOLVE_OFF + sizeof(PutFrame) * PUT_MAX_DEPTH <= CHAIN_FRAME_DOUBLES * sizeof(double),
+                "recursion frames");
+  PutFrame* stk = chain_frames<PutFrame>(X.scratch, FRAME_SOLVE_OFF);
   stk[0].f = f0; stk[0].h = h0; stk[0].in_org = in_org; stk[0].out_org = out_org;
   stk[0].arena = 0; stk[0].state = 0;
   int sp = 1;
@@ -274,6 +319,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     PutFrame& F = stk[sp - 1];
     const int h = F.h;
     const int ph = (sp >= 2) ? stk[sp - 2].h : 0x7fffffff;
+    FL_TR(*X.S, X.c, EV_NODE, h * 4 + F.state);
     if (F.state == 0) {
       if (h <= PUT_HS) {
         ret = put_subtree(X, P, F.f, F.in_org, F.out_org, h, ph, err);
@@ -348,7 +394,10 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   double* kc = frames + 2 * fstride;
   const Stencil st{P.cd, P.cm, P.cu, 2};
   build_kernel_table(kc, st, scratch);
-  PutChainCtx X{&S, c, st, kc, frames, fstride, 0u, pay - Lo.colbase, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+  PutChainCtx X{&S,   c,       st,  kc, frames, fstride, 0u, pay - Lo.colbase, scratch, chain_wstash(scratch),
+                (int64_t)P.cutoff, 0.0, 0.0, prof};
+  if (lane_id() < 4) S.wkey[c][lane_id()] = -1;  // new option: new weights
+  __syncwarp();
   // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
   // loaded with an initial segment (cols init_col0 .. +init_len)
   Task t;
@@ -390,7 +439,9 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       t.c0 = P.cd; t.c1 = P.cm; t.c2 = P.cu; t.h = 0; t.span = 2; t.L = 0; t.Lout = 0; t.d0 = 0.0;
       const int ring = (2 * rem + 2 <= SMALL_SLOTS) ? RING_SMALL : RING_BIG;
       const int id = issue(S, c, ring, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
+      FL_TR(S, c, EV_TW_B, 0);
       warp_wait_done(S, id);
+      FL_TR(S, c, EV_TW_E, 0);
       price = P.K * S.result[c];
       const int64_t lo = (f < ks - rem ? f : ks - rem) - 1;
       X.ref_flops += ref_strip_flops(ks + rem - lo + 1, rem);

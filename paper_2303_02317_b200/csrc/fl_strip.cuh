@@ -91,6 +91,86 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
   return kb;
 }
 
+// put_strip_warp with the neighbour exchange software-pipelined.  The per-row
+// loop-carried cycle is shuffle -> DFMA -> DSETP/FSEL -> shuffle (~48 cycles on
+// B200: shuffle 24, DFMA 8, select 14); the warp issues in order, so the two
+// edge cells of each row are finished FIRST and their shuffles for the next row
+// issued before the interior cells, whose ~30 FP64 issue cycles then overlap
+// the shuffle latency instead of preceding it.  Same per-cell arithmetic as
+// put_strip_warp (bit-identical rows, boundary and outputs).
+template <int CPL>
+__device__ int64_t put_strip_pipe(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                  const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
+                                  int height, double cd, double cm, double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 3, "edge / interior split");
+  const int lane = threadIdx.x & 31;
+  double v[CPL], p[CPL];
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
+  }
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(v[0] + p[0] == 12345.678 ? 1 : 0); }
+  double L = __shfl_up_sync(FULL, v[CPL - 1], 1);
+  double R = __shfl_down_sync(FULL, v[0], 1);
+  unsigned green = 0;
+  for (int s = 1; s <= height; ++s) {
+    // off-path partial sums of every cell (previous row only)
+    double a[CPL];
+    a[0] = fma(cu, v[1], cm * v[0]);
+#pragma unroll
+    for (int c = 1; c < CPL - 1; ++c) a[c] = fma(cu, v[c + 1], cm * v[c]);
+    a[CPL - 1] = fma(cd, v[CPL - 2], cm * v[CPL - 1]);
+    // edges (the shuffled neighbour enters last), then next row's exchange
+    const double lin0 = fma(cd, L, a[0]);
+    const double linE = fma(cu, R, a[CPL - 1]);
+    const bool red0 = lin0 > p[0], redE = linE > p[CPL - 1];
+    const double n0 = red0 ? lin0 : p[0];
+    const double nE = redE ? linE : p[CPL - 1];
+    L = __shfl_up_sync(FULL, nE, 1);
+    R = __shfl_down_sync(FULL, n0, 1);
+    green = (red0 ? 0u : 1u) | ((redE ? 0u : 1u) << (CPL - 1));
+    double nv[CPL];
+#pragma unroll
+    for (int c = 1; c < CPL - 1; ++c) {
+      const double lin = fma(cd, v[c - 1], a[c]);
+      const bool red = lin > p[c];
+      nv[c] = red ? lin : p[c];
+      green |= (red ? 0u : 1u) << c;
+    }
+    nv[0] = n0;
+    nv[CPL - 1] = nE;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
+  const int64_t vlo = lo + height, vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col >= vlo && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = v[c];
+  }
+  return kb;
+}
+
 // put_strip_warp restricted to the columns that can still change.  The put
 // boundary drops by 0 or 1 column per row (bsm.py:420-427 enforces it: the
 // reference raises GeometryError otherwise), so at row s every column below

@@ -18,7 +18,7 @@ names = ["FFT_CYC", "FFT_N", "DIR_CYC", "DIR_N", "OTHER_CYC", "OTHER_N", "BIG_CY
          "ISS_CYC", "CHAIN_CYC", "DEPWAIT_CYC", "ISS_SCAN", "ISS_STALL", "ISS_SLOT", "F_STAGE", "F_MID",
          "F_BOT", "STRIP_LOOP", "LEAF_LOAD", "W_RAW_S", "W_RAW_B", "W_WAR_S", "W_WAR_B", "W_N", "W_SUML", "W_SUMH", "W_FFT", "W_MAXL", "MAX_LOUT", "MAX_H", "MAX_YX", "HB64", "HB128", "HB256", "HB512", "HBBIG", "LB64", "LB128", "LB256", "LB512", "LBBIG"]
 P = dict(zip(names, p[:len(names)]))
-P["HELP_CYC"], P["HELP_CYC_BG"], P["HELP_FMA"] = p[48], p[49], p[50]
+P["HELP_CYC"], P["HELP_CYC_BG"], P["HELP_FMA"], P["S_LEAF"] = p[48], p[49], p[50], p[51]
 print(f"wall {1e3*(t1-t0):.2f} ms  n={n} cfg={cfg}")
 for nm in names:
     print(f"{nm:12s} {P[nm]:.4g}")
@@ -34,8 +34,9 @@ print("big tasks: n=%.0f avg %.0f cyc" % (P["BIG_N"], d(P["BIG_CYC"], P["BIG_N"]
 ntask = P["FFT_N"] + P["DIR_N"] + P["OTHER_N"] + P["BIG_N"]
 print("issue per task: scan %.0f stall %.0f slot %.0f (tasks/option %.0f)" % (
     d(P["ISS_SCAN"], ntask), d(P["ISS_STALL"], ntask), d(P["ISS_SLOT"], ntask), ntask / nopt))
-print("fused per node: stage %.0f mid %.0f bottom %.0f" % (d(P["F_STAGE"], P["FUSE_N"]), d(P["F_MID"], P["FUSE_N"]),
-                                                          d(P["F_BOT"], P["FUSE_N"])))
+print("fused per node: stage %.0f wait %.0f post %.0f leaf %.0f rest %.0f (of %.0f)" % (
+    d(P["F_STAGE"], P["FUSE_N"]), d(P["F_MID"], P["FUSE_N"]), d(P["F_BOT"], P["FUSE_N"]), d(P["STRIP_CYC"], P["FUSE_N"]),
+    d(P["FUSE_CYC"] - P["F_STAGE"] - P["F_MID"] - P["F_BOT"] - P["STRIP_CYC"], P["FUSE_N"]), d(P["FUSE_CYC"], P["FUSE_N"])))
 print("strip: loop %.1f cyc/row, load %.0f cyc/leaf (leaves/option %.0f)" % (
     d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"] / 28.0), P["STRIP_ROWS"] / 28.0 / nopt))
 print("conflict waits per option: RAW small %.3g big %.3g, WAR small %.3g big %.3g (n=%.0f)" % (

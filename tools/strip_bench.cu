@@ -14,6 +14,8 @@ __global__ void k(double* in, double* out, double* pay, long long* cyc, int reps
     if (MODE == 2) acc += put_strip_tiled<5, 2>(in, out, pay, lo, hi, f, height, 0.4, 0.2, 0.39);
     if (MODE == 3) acc += put_strip_tiled<5, 3>(in, out, pay, lo, hi, f, height, 0.4, 0.2, 0.39);
     if (MODE == 4) acc += put_strip_tiled<5, 4>(in, out, pay, lo, hi, f, height, 0.4, 0.2, 0.39);
+    if (MODE == 5) acc += put_strip_v2<4>(in, out, pay, hi, f, height, 0.4, 0.2, 0.39);
+    if (MODE == 6) acc += put_strip_pipe<5>(in, out, pay, lo, hi, f, height, 0.4, 0.2, 0.39);
   }
   long long t1 = clock64();
   if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = acc; }
@@ -27,13 +29,15 @@ int main() {
   double ref[256];
   long long h[2];
   for (int height : {32, 31, 17}) {
-    for (int mode : {0, 2, 3, 4}) {
+    for (int mode : {0, 6, 5}) {
       cudaMemset(out, 0, 2048);
       auto run = [&](int reps) {
         if (mode == 0) k<0><<<1, 32>>>(in, out, pay, c, reps, height);
         if (mode == 2) k<2><<<1, 32>>>(in, out, pay, c, reps, height);
         if (mode == 3) k<3><<<1, 32>>>(in, out, pay, c, reps, height);
         if (mode == 4) k<4><<<1, 32>>>(in, out, pay, c, reps, height);
+        if (mode == 5) k<5><<<1, 32>>>(in, out, pay, c, reps, height);
+        if (mode == 6) k<6><<<1, 32>>>(in, out, pay, c, reps, height);
       };
       run(1);
       double o[256]; cudaMemcpy(o, out, 2048, cudaMemcpyDeviceToHost);
