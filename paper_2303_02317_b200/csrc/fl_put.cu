@@ -169,6 +169,7 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
     prof_add(X.prof, PROF_LEAF_LOAD, tm[0] - t1);
   }
   X.flops += ref_strip_flops(hi - lo + 1, height);
+  FL_TR(*X.S, X.c, EV_MARK, 1);
   return kb;
 }
 
@@ -239,13 +240,16 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     SubFrame& F = stk[sp - 1];
     const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
     const int ph = (sp >= 2) ? stk[sp - 2].h : ph0;
+    FL_TR(*X.S, X.c, EV_MARK, 3);
     if (F.state == 0) {
       ref_node_enter(X, h, ph);
+      FL_TR(*X.S, X.c, EV_MARK, 4);
       if (h <= PUT_LEAF) {
         const int64_t kb = put_leaf(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
         --sp;
+        FL_TR(*X.S, X.c, EV_MARK, 2);
         continue;
       }
       F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : sp == 2 ? SUB_ASM1 : SUB_ASM2) - (F.f - h1 + 1);
@@ -264,6 +268,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       const int64_t km = ret;
       if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
       F.km = km;
+      FL_TR(*X.S, X.c, EV_MARK, 5);
       const long long tw = clock64();
       helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
       twait += clock64() - tw;

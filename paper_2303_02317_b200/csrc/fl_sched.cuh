@@ -140,6 +140,9 @@ constexpr int NRINGS = 3;
 #ifndef FL_CONV_PAIRS  // helper correlation: 1 two outputs / lane, 2 register-blocked 8 x 4, 3 blocked + weights in registers
 #define FL_CONV_PAIRS 2
 #endif
+#ifndef FL_STEAL  // 1: the big FFT group also takes small-ring tasks after its own rings (2: before RING_LOW)
+#define FL_STEAL 1
+#endif
 #ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
 #define FL_IDLE_NS 2048
 #endif
@@ -1050,8 +1053,18 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double2* buf = gi == 0 ? bigbuf : medbuf;
   const int slots = gi == 0 ? BIG_SLOTS : SMALL_SLOTS;
   const int logN = gi == 0 ? BIG_LOGN : SMALL_LOGN;
+  // claim order: the big group RING_BIG, RING_LOW (and with FL_STEAL the
+  // medium group's RING_SMALL: idle big-group time absorbs small-ring queueing);
+  // the medium group RING_SMALL only
   const int r_hi = gi == 0 ? RING_BIG : RING_SMALL;
-  const int r_lo = gi == 0 ? RING_LOW : -1;
+#if FL_STEAL == 2
+  const int r_2 = gi == 0 ? RING_SMALL : -1;
+  const int r_3 = gi == 0 ? RING_LOW : -1;
+#else
+  const int r_2 = gi == 0 ? RING_LOW : -1;
+  const int r_3 = (gi == 0 && FL_STEAL) ? RING_SMALL : -1;
+#endif
+  constexpr int NCLAIM = 3;
   for (;;) {
     const long long t0 = clock64();
     if (rank == 0) {
@@ -1064,16 +1077,25 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
         // earliest-issued head always becomes ready, so this cannot deadlock)
         int r = -1, i = 0;
         if (lane_id() == 0) {
-          for (int k = 0; k < 2 && r < 0; ++k) {
-            const int rr = k == 0 ? r_hi : r_lo;
-            if (rr < 0 || S.claim[rr] >= *(volatile int*)&S.reserve[rr]) continue;
-            const int ii = S.claim[rr];
+          for (int k = 0; k < NCLAIM && r < 0; ++k) {
+            const int rr = k == 0 ? r_hi : k == 1 ? r_2 : r_3;
+            if (rr < 0) continue;
+            const int ii = *(volatile int*)&S.claim[rr];
+            if (ii >= *(volatile int*)&S.reserve[rr]) continue;
             const Task& sl = S.ring[rr][ii % QCAP];
             if (sl.seq != ii) continue;  // reserved, not yet published
             __threadfence_block();
+            if (rr == RING_SMALL && gi == 0 && sl.kind == TK_EXIT) continue;  // the medium group's own exit
             bool ready = true;
             for (int d = 0; d < sl.ndep; ++d) ready = ready && task_done(S, sl.dep[d]);
-            if (ready) { r = rr; i = S.claim[rr]++; }
+            if (!ready) continue;
+            if (rr == RING_SMALL && FL_STEAL) {  // two consumers: claim by CAS
+              if (atomicCAS(&S.claim[rr], ii, ii + 1) == ii) { r = rr; i = ii; }
+            } else {
+              r = rr;
+              i = ii;
+              S.claim[rr] = ii + 1;
+            }
           }
         }
         r = __shfl_sync(FULL, r, 0);
@@ -1090,7 +1112,10 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     const long long t1 = clock64();
     if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
     if (t.kind == TK_EXIT) break;
-    const double fl = pr.exec(S, t, buf, slots, logN, tq, g);
+    // a stolen small-ring task runs with the medium group's block plan (same
+    // arithmetic whichever group executes it)
+    const bool stolen = (gi == 0 && tring == RING_SMALL);
+    const double fl = pr.exec(S, t, buf, stolen ? SMALL_SLOTS : slots, stolen ? SMALL_LOGN : logN, tq, g);
     flops += fl > 0 ? fl : 0.0;
     gsync(g);
     if (g.t == 0) {

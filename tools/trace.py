@@ -28,6 +28,7 @@ typ = (ev[:, 0] >> np.uint64(32)).astype(np.int64)
 arg = (ev[:, 0] & np.uint64(0xffffffff)).astype(np.int64)
 clk = ev[:, 1].astype(np.int64)
 names = {1: "SUB", 3: "LEAF", 5: "HWAIT", 7: "POST", 9: "CWAIT", 11: "ISSUE", 13: "STAGE", 16: "OPT", 18: "TWAIT"}
+MARK = 20
 print(f"events {len(typ)}  span {clk[-1] - clk[0]:.4g} cycles")
 # innermost-open attribution
 stack = []
@@ -41,9 +42,11 @@ for t, a, c in zip(typ, arg, clk):
     dt = c - prev_t
     cat = stack[-1] if stack else "top"
     acc[cat] += dt
+    def lab(e, a):
+        if e == MARK: return f"M{a}"
+        return names.get(e, names.get(e - 1, str(e))) + ("_B" if e in names else "_E")
     if cat in ("SUB", "top", "OPT"):
-        gap[(cat, names.get(prev_e[0], names.get(prev_e[0] - 1, str(prev_e[0]))) + ("_B" if prev_e[0] in names else "_E"),
-             names.get(t, names.get(t - 1, str(t))) + ("_B" if t in names else "_E"))] += dt
+        gap[(cat, lab(*prev_e), lab(t, a))] += dt
     if cat == "HWAIT":
         hw_by_q[prev_e[1]] += dt
     if cat == "POST":
