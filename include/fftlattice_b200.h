@@ -96,8 +96,12 @@ int fl_batch_stats(fl_batch* b, double* fp64_flops, int64_t* h2d_bytes, int64_t*
 /* After a run: the REFERENCE-ALGORITHMIC fp64 flops of the batch -- the work
  * the reference decomposition at its base_cutoff performs (5 flops per
  * projected cell of each reference strip; 5 N log2 N + 6 (N/2+1) per
- * reference FFT jump of size N = next_pow2(L + M - 1)), counted live by the
- * fast kernels as they walk the same recursion.  The roofline numerator. */
+ * reference FFT jump of size N = next_pow2(L + M - 1)), counted by the fast
+ * kernels as they walk the same recursion.  The roofline numerator.  Production
+ * runs skip the per-node counting (it costs ~5 % on the chains' critical
+ * path): the first stats / ref-flops query of a prepared batch makes one extra,
+ * untimed accounting run of the same kernel on the same inputs (results are
+ * deterministic, so the counts are exact for every run of the batch). */
 int fl_batch_ref_flops(fl_batch* b, double* ref_flops, void* stream);
 void fl_batch_free(fl_batch* b);
 /* Scheduler profile counters of the last run (requires FL_PROFILE set in the

@@ -22,8 +22,8 @@
 namespace fl {
 
 constexpr int CALL_LEAF = 32;
-#ifndef FL_CALL_LEAF_V2
-#define FL_CALL_LEAF_V2 1
+#ifndef FL_CALL_LEAF_V2  // 2: call_leaf_v3 (shared e2 table, carried bases)
+#define FL_CALL_LEAF_V2 2
 #endif
 #ifndef FL_CALL_HS
 #define FL_CALL_HS 256
@@ -50,11 +50,12 @@ __device__ __forceinline__ int64_t first_green_rec(int64_t i, int64_t j) {  // a
 
 // reference-algorithmic cost model; the reference strip's cell
 // count depends on the boundary path, estimated as 3/4 h^2 for h rows of width h
-__device__ __forceinline__ double call_ref_jump(int64_t L, int64_t M) {
+// (integer arithmetic on the chain: see fl_put.cu ref_jump_flops)
+__device__ __forceinline__ uint64_t call_ref_jump(int64_t L, int64_t M) {
   const uint64_t need = (uint64_t)(L + M - 1);
   const int lg = need <= 1 ? 0 : 64 - __clzll((long long)(need - 1));
-  const double N = (double)(1ull << lg);
-  return 5.0 * N * (double)lg + 6.0 * (N * 0.5 + 1.0);
+  const uint64_t N = 1ull << lg;
+  return 5ull * N * (uint64_t)lg + 3ull * N + 6ull;
 }
 
 // Leaf strip (binomial_strip_sweep with lo = j-h+1, height h <= 32) on the
@@ -142,6 +143,50 @@ __device__ int64_t call_leaf_v2(const CallParams& P, const double* __restrict__ 
   return jp;
 }
 
+// call_leaf_v2 restructured for the warp's in-order issue: the e2 factors
+// come from a per-option shared table (same exp expressions as v2, computed
+// once per option instead of once per leaf), the parent base of row s+1 is
+// carried from row s (one broadcast shuffle per row), and every value that
+// does not depend on the row's neighbour exchange (the green value, the
+// out-of-strip right neighbour, wd v) is formed before the exchange lands.
+// Bit-identical to call_leaf_v2.
+constexpr int CALL_E2 = CHAIN_SCRATCH - 40;  // e2[k] = exp(2 k lu), k = 0..32, in the chain scratch
+static_assert(CALL_E2 >= CSUB_ASM2 + CALL_HS / 4 + 8, "e2 table above the call subtree scratch");
+__device__ int64_t call_leaf_v3(const CallParams& P, const double* __restrict__ in_org, double* __restrict__ out_org,
+                                int64_t lo, int64_t top_row, int64_t j0, int height, double* cells,
+                                const double* __restrict__ e2) {
+  const int lane = threadIdx.x & 31;
+  const int W = (int)(j0 - lo + 1);
+  const int64_t col = lo + lane;
+  double v = (lane < W) ? in_org[col] : 0.0;
+  const double e2_me = e2[lane], e2_nx = e2[lane + 1];
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
+  const bool edge = (lane + 1 >= W);  // right neighbour outside the strip: exercise value
+  double bp = __shfl_sync(FULL, Bl, 0);
+  bool green = false;
+  for (int s = 0; s < height; ++s) {
+    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
+    const double right = __shfl_down_sync(FULL, v, 1);
+    const double ex_r = __dsub_rn(__dmul_rn(bp, e2_nx), P.K);
+    const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
+    const double a = __dmul_rn(P.wd, v);
+    const double vr = edge ? ex_r : right;
+    const double lin = __dadd_rn(a, __dmul_rn(P.wu, vr));
+    green = !(lin >= grn);
+    v = green ? grn : lin;
+    bp = bc;
+  }
+  const int64_t child = top_row - height;
+  const int64_t top = (j0 < child) ? j0 : child;
+  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
+  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
+  *cells += (double)W * height;
+  if (col <= jp && lane < W) out_org[col] = v;
+  __syncwarp();
+  return jp;
+}
+
 struct CallFrame {
   int64_t i, j, jm;
   double* in_org;
@@ -160,30 +205,37 @@ struct CallChainCtx {
   int64_t fstride;
   uint32_t tog;
   double* scratch;
+  double* wst;  // weight stash (shared)
   int64_t ref_cut;
-  double flops, ref_flops;
+  bool acct;        // count flops (accounting runs only)
+  uint64_t flops;   // executed chain-side flops
+  uint64_t ref_q;   // reference-algorithmic flops x 4 (the 3/4 h^2 strip estimate stays exact)
   unsigned long long* prof;
 };
 
 __device__ __forceinline__ void call_ref_enter(CallChainCtx& X, int h, int ph) {
-  if (h > X.ref_cut) X.ref_flops += call_ref_jump(h, (h + 1) / 2 + 1);
-  else if (ph > X.ref_cut) X.ref_flops += 5.0 * 0.75 * (double)h * (double)h;
+  if (!X.acct) return;
+  if (h > X.ref_cut) X.ref_q += 4ull * call_ref_jump(h, (h + 1) / 2 + 1);
+  else if (ph > X.ref_cut) X.ref_q += 15ull * (uint64_t)h * (uint64_t)h;  // 4 x 5 x 3/4 h^2
 }
 __device__ __forceinline__ void call_ref_bottom(CallChainCtx& X, int h, int64_t A) {
+  if (!X.acct) return;
   const int h2 = h - (h + 1) / 2;
-  if (h > X.ref_cut && A > h2) X.ref_flops += call_ref_jump(A, h2 + 1);
+  if (h > X.ref_cut && A > h2) X.ref_q += 4ull * call_ref_jump(A, h2 + 1);
 }
 
 __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& P, const double* in_org,
                                              double* out_org, int64_t i, int64_t j, int h) {
   const long long t1 = clock64();
   double cells = 0.0;
-#if FL_CALL_LEAF_V2
+#if FL_CALL_LEAF_V2 == 2
+  const int64_t jp = call_leaf_v3(P, in_org, out_org, j - h + 1, i, j, h, &cells, X.scratch + CALL_E2);
+#elif FL_CALL_LEAF_V2
   const int64_t jp = call_leaf_v2(P, in_org, out_org, j - h + 1, i, j, h, &cells);
 #else
   const int64_t jp = call_leaf_warp(P, in_org, out_org, j - h + 1, i, j, h, &cells);
 #endif
-  X.flops += 5.0 * cells;
+  if (X.acct) X.flops += 5ull * (uint64_t)cells;
   if (X.prof && lane_id() == 0) {
     prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
     prof_add(X.prof, PROF_STRIP_N, h);
@@ -212,6 +264,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   const long long t1 = clock64();
   double* s_in = X.scratch + CSUB_IN;
   warp_stage(s_in, in_org + lo0, h0);
+  if (h0 > CALL_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, CALL_LEAF, 1);
   long long twait = 0;
   static_assert(sizeof(CallSubFrame) * 5 <= FRAME_SOLVE_OFF - FRAME_SUB_OFF, "subtree frames");
   CallSubFrame* stk = chain_frames<CallSubFrame>(X.scratch, FRAME_SUB_OFF);
@@ -233,8 +286,8 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : sp == 2 ? CSUB_ASM1 : CSUB_ASM2) - lo;
       F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
       // mid (helper): cols lo .. j-h1 of row i-h1
-      F.tk = helper_post(*X.S, X.c, F.q, F.in + lo, F.asmo + lo, h2, X.kc + (int64_t)h1 * h1, h1 + 1, &F.tk0);
-      X.flops += 2.0 * h2 * (h1 + 1);
+      F.tk = helper_post(*X.S, X.c, F.q, F.in + lo, F.asmo + lo, h2, wslot(*X.S, X.c, X.wst, sp, h1), h1 + 1, &F.tk0);
+      if (X.acct) X.flops += 2ull * (uint64_t)(h2 * (h1 + 1));
       F.state = 1;
       CallSubFrame& C = stk[sp++];
       C.i = F.i; C.j = F.j; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
@@ -249,8 +302,9 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       call_ref_bottom(X, h, A);
       F.tk = -1;
       if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h
-        F.tk = helper_post(*X.S, X.c, F.q, F.asmo + lo, F.out + lo, (int)(A - h2), X.kc + (int64_t)h2 * h2, h2 + 1, &F.tk0);
-        X.flops += 2.0 * (A - h2) * (h2 + 1);
+        F.tk = helper_post(*X.S, X.c, F.q, F.asmo + lo, F.out + lo, (int)(A - h2), wslot(*X.S, X.c, X.wst, sp, h2),
+                           h2 + 1, &F.tk0);
+        if (X.acct) X.flops += 2ull * (uint64_t)((A - h2) * (h2 + 1));
       }
       F.state = 2;
       CallSubFrame& C = stk[sp++];
@@ -347,13 +401,19 @@ __device__ void call_record(const BatchOut& out, int o, int32_t& cnt, int64_t t,
 }
 
 __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams& P, int64_t row_len, int64_t h_max,
-                                         double* arena, double* scratch, unsigned long long* prof) {
+                                         double* arena, double* scratch, unsigned long long* prof, bool acct = true) {
   double* frames = arena + 2 * (row_len + 8);
   const int64_t fstride = 2 * h_max + 16 * CALL_MAX_DEPTH;
   double* kc = frames + 2 * fstride;
   const Stencil st{P.wd, P.wu, 0.0, 1};
   build_kernel_table(kc, st, scratch);
-  return CallChainCtx{&S, c, st, kc, frames, fstride, 0u, scratch, (int64_t)P.cutoff, 0.0, 0.0, prof};
+  __syncwarp();
+  for (int k = lane_id(); k <= 32; k += 32) scratch[CALL_E2 + k] = exp(2.0 * (double)k * P.lu);  // call_leaf_v3
+  __syncwarp();
+  if (lane_id() < 4) S.wkey[c][lane_id()] = -1;  // new option: new weights
+  __syncwarp();
+  return CallChainCtx{&S, c, st, kc, frames, fstride, 0u, scratch, chain_wstash(scratch), (int64_t)P.cutoff,
+                      acct, 0ull, 0ull, prof};
 }
 
 // The trapezoid loop from row i / boundary j down to the residual (american.py:486-498).
@@ -366,7 +426,7 @@ __device__ void call_trapezoids(CallChainCtx& X, const CallParams& P, int64_t& i
     // left: cols first .. j-h of row i-h (american.py:341-344)
     const int64_t L = j - first + 1;
     if (L > hh) {
-      X.ref_flops += call_ref_jump(L, hh + 1);
+      X.ref_q += 4ull * call_ref_jump(L, hh + 1);
       chain_conv(*X.S, X.c, X.st, cur_org + first, L, nxt_org + first, L - hh, h, X.kc, X.prof, true);
     }
     const int64_t jp = call_solve(X, P, i, j, h, cur_org, nxt_org, err);
@@ -385,7 +445,7 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
                                   double* scratch, const BatchOut& out, double* chain_flops) {
   const long long t_opt = clock64();
   const int64_t n = P.n;
-  CallChainCtx X = call_chain_setup(S, c, P, n, n, arena, scratch, out.prof);
+  CallChainCtx X = call_chain_setup(S, c, P, n, n, arena, scratch, out.prof, out.acct != 0);
   double* cur_org = arena;
   double* nxt_org = arena + (n + 8);
   int32_t err = 0, cnt = 0;
@@ -423,8 +483,8 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
       warp_wait_done(S, id);
       const int64_t j0 = S.iresult[c];
       price = (j0 >= 0) ? S.result[c] : P.S - P.K;
-      X.flops += 5.0 * S.result2[c];
-      X.ref_flops += 5.0 * S.result2[c];
+      X.flops += 5ull * (uint64_t)S.result2[c];
+      X.ref_q += 20ull * (uint64_t)S.result2[c];
       if (i > 0) call_record(out, o, cnt, 0, first_green_rec(0, j0));
     }
   }
@@ -433,10 +493,10 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
     out.price[o] = err ? 0.0 : price;
     out.status[o] = err;
     if (out.bcount) out.bcount[o] = err ? 0 : cnt;
-    if (out.flops) atomicAdd(out.flops + 1, (unsigned long long)X.ref_flops);
+    if (out.flops) atomicAdd(out.flops + 1, (unsigned long long)(X.ref_q / 4));
     prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
-  *chain_flops += X.flops;
+  *chain_flops += (double)X.flops;
 }
 
 // Worker side of the call-specific tasks.
@@ -571,7 +631,7 @@ struct CallTrapPricer {
     const int64_t hh = h;
     const int64_t L = width;
     if (L > hh) {
-      X.ref_flops += call_ref_jump(L, hh + 1);
+      X.ref_q += 4ull * call_ref_jump(L, hh + 1);
       call_conv(X, cur_org + first, L, nxt_org + first, L - hh, (int)hh);
     }
     const int64_t jp = call_solve(X, P, ii, jj, (int)hh, cur_org, nxt_org, &err);
@@ -581,9 +641,9 @@ struct CallTrapPricer {
     if (lane_id() == 0) {
       meta[0] = err ? 0 : jp;
       meta[1] = err;
-      if (flops) atomicAdd(flops + 1, (unsigned long long)X.ref_flops);
+      if (flops) atomicAdd(flops + 1, (unsigned long long)(X.ref_q / 4));
     }
-    *fl += X.flops;
+    *fl += (double)X.flops;
   }
   __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
                          const Grp& g) const {

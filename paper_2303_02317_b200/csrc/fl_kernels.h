@@ -20,6 +20,10 @@ struct BatchOut {
   int32_t cap;
   unsigned long long* flops;  // [0] executed fp64 flops, [1] reference-algorithmic flops (accumulated), may be null
   unsigned long long* prof;   // optional profile counters (PROF_* in fl_sched.cuh), may be null
+  // 1: the chains count executed / reference-algorithmic flops into flops[0..1];
+  // 0: production runs skip the per-node accounting (an untimed accounting run
+  // of the same batch supplies the counts, fl_abi.cu)
+  int acct = 1;
   // optional fast-put row snapshots (record_rows): option o appends its handoff
   // segments at snap + o * snap_cap, snap_len[o] = total length (may exceed cap)
   double* snap = nullptr;

@@ -65,16 +65,18 @@ static_assert(2 * (2 * KT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
 enum : int { TK_PUT_INIT = TK_USER + 0, TK_PUT_APEX = TK_USER + 1, TK_PUT_LOAD = TK_USER + 2 };
 
-// reference-algorithmic cost model
-__device__ __forceinline__ double ref_jump_flops(int64_t L, int64_t M) {
+// reference-algorithmic cost model.  Exact integers, kept in
+// 64-bit integer registers on the chain (fp64 conversions and dependent adds on
+// the chain's critical path measured ~6 % of the headline run).
+__device__ __forceinline__ uint64_t ref_jump_flops(int64_t L, int64_t M) {
   const uint64_t need = (uint64_t)(L + M - 1);
   const int lg = need <= 1 ? 0 : 64 - __clzll((long long)(need - 1));  // N = next_pow2(L+M-1) = 2^lg
-  const double N = (double)(1ull << lg);
-  return 5.0 * N * (double)lg + 6.0 * (N * 0.5 + 1.0);
+  const uint64_t N = 1ull << lg;
+  return 5ull * N * (uint64_t)lg + 3ull * N + 6ull;  // 5 N lg N + 6 (N/2 + 1)
 }
 // projected cells of a reference strip of width W swept `rows` times (shrinking cone)
-__device__ __forceinline__ double ref_strip_flops(int64_t W, int64_t rows) {
-  return 5.0 * ((double)rows * (double)W - (double)rows * (double)(rows + 1));
+__device__ __forceinline__ uint64_t ref_strip_flops(int64_t W, int64_t rows) {
+  return 5ull * (uint64_t)(rows * W - rows * (rows + 1));
 }
 
 struct PutFrame {
@@ -131,23 +133,32 @@ struct PutChainCtx {
   double* scratch;   // chain's shared scratch (CHAIN_SCRATCH doubles)
   double* wst;       // chain's weight stash (shared)
   int64_t ref_cut;   // the reference's base_cutoff (work accounting only)
-  double flops;      // executed chain-side flops (lane-uniform)
-  double ref_flops;  // reference-algorithmic flops (lane-uniform)
+  bool acct;           // count flops (accounting runs only)
+  uint64_t flops;      // executed chain-side flops (lane-uniform)
+  uint64_t ref_flops;  // reference-algorithmic flops (lane-uniform)
   unsigned long long* prof;
 };
 
 // Reference cost of a recursion node of height h whose parent has height ph:
 // the reference strips it whole if h <= cutoff (and its parent did not), else
 // it issues the mid jump here and the bottom jump once km is known.
+#ifndef FL_ABL
+#define FL_ABL 0
+#endif
+template <bool ACCT = true>
 __device__ __forceinline__ void ref_node_enter(PutChainCtx& X, int h, int ph) {
+  if (FL_ABL || !ACCT || !X.acct) return;
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(2 * (int64_t)h, 2 * (int64_t)((h + 1) / 2) + 1);
   else if (ph > X.ref_cut) X.ref_flops += ref_strip_flops(4 * (int64_t)h + 2, h);
 }
+template <bool ACCT = true>
 __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A) {
+  if (FL_ABL || !ACCT || !X.acct) return;
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
 }
 
 // Leaf strip on the chain warp.  in_org / out_org / pay_org may address shared memory.
+template <bool ACCT = true>
 __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
                                             double* out_org, const double* pay_org, int64_t lo, int64_t hi,
                                             int64_t f, int height) {
@@ -168,33 +179,11 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
     prof_add(X.prof, PROF_STRIP_LOOP, tm[1]);
     prof_add(X.prof, PROF_LEAF_LOAD, tm[0] - t1);
   }
-  X.flops += ref_strip_flops(hi - lo + 1, height);
+  if (!FL_ABL && ACCT && X.acct) X.flops += ref_strip_flops(hi - lo + 1, height);
   FL_TR(*X.S, X.c, EV_MARK, 1);
   return kb;
 }
 
-
-// Make the weights of every correlation of a subtree rooted at height h0
-// resident in the stash (bsm.py:484-496 use W_{h1}, W_{h2} of each node's children).
-__device__ void put_stash_weights(PutChainCtx& X, int h0) {
-  for (int d = 1; d <= 3; ++d) {
-    const int pmax = (h0 + (1 << (d - 1)) - 1) >> (d - 1);  // tallest node at depth d-1
-    if (pmax <= PUT_LEAF) break;                            // depth d-1 is all leaves
-    const int lo = h0 >> d, hi = (h0 + (1 << d) - 1) >> d;
-    const int key = X.S->wkey[X.c][d];
-    if (key >= 0 && lo >= key && hi <= key + 1) continue;
-    for (int j = 0; j < 2; ++j) {
-      const int m = lo + j;
-      if (m > KT_H) break;
-      warp_stage_nb<9>(X.wst + wst_off(d) + j * wst_sz(d), X.kc + (int64_t)m * m, 2 * m + 1, 2 * m + 1);
-    }
-    if (lane_id() == 0) X.S->wkey[X.c][d] = lo;
-    __syncwarp();
-  }
-}
-__device__ __forceinline__ const double* put_wslot(const PutChainCtx& X, int d, int m) {
-  return X.wst + wst_off(d) + (m - X.S->wkey[X.c][d]) * wst_sz(d);
-}
 
 struct SubFrame {
   int64_t f, km;
@@ -213,6 +202,10 @@ struct SubFrame {
 // The explicit frame stack lives in shared memory (one copy per warp): frames
 // in registers (a compile-time recursion) measured slower -- the live frames
 // push the leaf strip into register spills.
+// (instantiated with and without the flop accounting: the counting code in the
+// walk costs ~5 % even when switched off at run time, so production runs use
+// the ACCT = false instance and accounting runs the other)
+template <bool ACCT>
 __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
                                double* out_org, int h0, int ph0, int32_t* err) {
   const long long t0 = clock64();
@@ -227,7 +220,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
   warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
   const double* pay_s = s_pay - plo;
-  if (h0 > PUT_LEAF) put_stash_weights(X, h0);
+  if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
   const long long t2 = clock64();
   FL_TR(*X.S, X.c, EV_STG_E, 0);
   long long twait = 0, tpost = 0;
@@ -257,10 +250,10 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
       const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, put_wslot(X, sp, h1), Mmid,
+      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, wslot(*X.S, X.c, X.wst, sp, h1), Mmid,
                          &F.tk0);
       tpost += clock64() - tp;
-      X.flops += 2.0 * Lmid * Mmid;
+      if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lmid * Mmid);
       F.state = 1;
       SubFrame& C = stk[sp++];
       C.f = F.f; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
@@ -274,13 +267,13 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       twait += clock64() - tw;
       // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;
-      ref_node_bottom(X, h, A);
+      ref_node_bottom<ACCT>(X, h, A);
       const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
       const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, put_wslot(X, sp, h2), Mbot,
+      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, wslot(*X.S, X.c, X.wst, sp, h2), Mbot,
                          &F.tk0);
       tpost += clock64() - tp;
-      X.flops += 2.0 * Lbot * Mbot;
+      if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lbot * Mbot);
       F.state = 2;
       SubFrame& C = stk[sp++];
       C.f = km; C.h = h2; C.in = F.asmo; C.out = F.out; C.state = 0;
@@ -311,6 +304,7 @@ __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_
 }
 
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
+template <bool ACCT>
 __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, double* in_org, double* out_org,
                                int h0, int32_t* err) {
   static_assert(FRAME_SOLVE_OFF + sizeof(PutFrame) * PUT_MAX_DEPTH <= CHAIN_FRAME_DOUBLES * sizeof(double),
@@ -327,12 +321,12 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     FL_TR(*X.S, X.c, EV_NODE, h * 4 + F.state);
     if (F.state == 0) {
       if (h <= PUT_HS) {
-        ret = put_subtree(X, P, F.f, F.in_org, F.out_org, h, ph, err);
+        ret = put_subtree<ACCT>(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
         --sp;
         continue;
       }
-      ref_node_enter(X, h, ph);
+      ref_node_enter<ACCT>(X, h, ph);
       const int h1 = (h + 1) / 2;
       const int d = sp - 1;
       X.tog ^= 1u << d;
@@ -350,7 +344,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
       if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
       F.km = km;
       const int64_t A = F.f + 2 * (int64_t)h - h1 - km;  // assembled cols km+1 .. f+2h-h1
-      ref_node_bottom(X, h, A);
+      ref_node_bottom<ACCT>(X, h, A);
       // bottom: cols km+h2+1 .. f+h of row t+h
       put_conv(X, F.asm_org + km + 1, A, F.out_org + km + h2 + 1, A - 2 * (int64_t)h2, h2);
       F.state = 2;
@@ -370,6 +364,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
 
 // One stage (_advance_stage, bsm.py:557-582): far jump + boundary recursion,
 // cur -> nxt over hh rows.  Returns the new boundary.
+template <bool ACCT = true>
 __device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int64_t red, int64_t hh,
                              double* cur_org, double* nxt_org, int32_t* err) {
   const int h = (int)hh;
@@ -377,7 +372,7 @@ __device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int6
     X.ref_flops += ref_jump_flops(red, 2 * hh + 1);
     chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc, X.prof, true);
   }
-  return put_solve_q(X, P, f, cur_org, nxt_org, h, err);
+  return put_solve_q<ACCT>(X, P, f, cur_org, nxt_org, h, err);
 }
 
 __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, int64_t c) {
@@ -391,7 +386,7 @@ __device__ void put_record(const BatchOut& out, int o, int32_t& cnt, int64_t t, 
 // Arena: stage rows A | B | payoff table | recursion frames | kernel table.
 __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P, const PutLayout& Lo,
                                        int64_t n_rows, double* arena, double* scratch, unsigned long long* prof,
-                                       const double* init_src, int64_t init_col0, int64_t init_len) {
+                                       const double* init_src, int64_t init_col0, int64_t init_len, bool acct = true) {
   double* bufA = arena;
   double* pay = arena + 2 * Lo.span;
   double* frames = arena + 3 * Lo.span;
@@ -400,7 +395,7 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   const Stencil st{P.cd, P.cm, P.cu, 2};
   build_kernel_table(kc, st, scratch);
   PutChainCtx X{&S,   c,       st,  kc, frames, fstride, 0u, pay - Lo.colbase, scratch, chain_wstash(scratch),
-                (int64_t)P.cutoff, 0.0, 0.0, prof};
+                (int64_t)P.cutoff, acct, 0ull, 0ull, prof};
   if (lane_id() < 4) S.wkey[c][lane_id()] = -1;  // new option: new weights
   __syncwarp();
   // payoff table 1 - e^{col ds} (bsm.py:232-244), row A zeroed, optionally
@@ -418,12 +413,13 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
 }
 
 // fast_put_bsm's stage loop (bsm.py:626-676) for option o on chain warp c.
+template <bool ACCT>
 __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
                                  double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
   const long long t_opt = clock64();
   const int64_t n = P.n, ks = P.ks;
   const PutLayout Lo = put_layout(n, ks);
-  PutChainCtx X = put_chain_setup(S, c, P, Lo, n, arena, scratch, out.prof, nullptr, 0, 0);
+  PutChainCtx X = put_chain_setup(S, c, P, Lo, n, arena, scratch, out.prof, nullptr, 0, 0, out.acct != 0);
   double* cur_org = arena - Lo.colbase;
   double* nxt_org = arena + Lo.span - Lo.colbase;
   int32_t err = 0, cnt = 0;
@@ -450,7 +446,7 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       price = P.K * S.result[c];
       const int64_t lo = (f < ks - rem ? f : ks - rem) - 1;
       X.ref_flops += ref_strip_flops(ks + rem - lo + 1, rem);
-      X.flops += 5.0 * ((double)rem * rem + rem);
+      X.flops += 5ull * (uint64_t)(rem * rem + rem);
       break;
     }
     const int64_t hh = (rem / 2 < red / 2) ? rem / 2 : red / 2;
@@ -463,7 +459,7 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       f = kb;
       m += 1;
     } else {
-      const int64_t kp = put_stage(X, P, f, red, hh, cur_org, nxt_org, &err);
+      const int64_t kp = put_stage<ACCT>(X, P, f, red, hh, cur_org, nxt_org, &err);
       if (err) break;
       f = kp;
       m += hh;
@@ -492,8 +488,8 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     if (out.bcount) out.bcount[o] = err ? 0 : cnt;
     prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
-  *chain_flops += X.flops;
-  *ref_flops += X.ref_flops;
+  *chain_flops += (double)X.flops;
+  *ref_flops += (double)X.ref_flops;
 }
 
 // Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
@@ -542,6 +538,11 @@ __device__ double put_exec_task(SchedShared& S, const Task& t, double2* sbuf, in
   return exec_generic(t, sbuf, slots, logN, tq, g);
 }
 
+// ACCT selects the kernel instance: production launches run the walk without
+// the per-node flop counting, accounting launches (fl_abi.cu) with it.  Two
+// kernels rather than a run-time branch: one kernel holding both walks
+// allocates registers for both and spills.
+template <bool ACCT>
 struct PutPricer {
   const PutParams* opts;
   const int32_t* order;
@@ -549,7 +550,7 @@ struct PutPricer {
   __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* flops) const {
     double ref = 0.0;
     const int o = order[w];
-    put_chain_option(S, c, opts[o], o, arena, scratch, out, flops, &ref);
+    put_chain_option<ACCT>(S, c, opts[o], o, arena, scratch, out, flops, &ref);
     if (lane_id() == 0 && out.flops) atomicAdd(out.flops + 1, (unsigned long long)ref);
   }
   __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
@@ -558,10 +559,11 @@ struct PutPricer {
   }
 };
 
+template <bool ACCT>
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
-  const PutPricer pr{opts, order, out};
+  const PutPricer<ACCT> pr{opts, order, out};
   sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
 
@@ -593,7 +595,7 @@ struct PutTrapPricer {
       meta[1] = err;
       if (flops) atomicAdd(flops + 1, (unsigned long long)X.ref_flops);
     }
-    *fl += X.flops;
+    *fl += (double)X.flops;
   }
   __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
                          const Grp& g) const {
@@ -680,7 +682,9 @@ static cudaError_t put_configure() {
   static bool configured = false;
   if (configured) return cudaSuccess;
   const int smem = sched_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(put_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(put_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(put_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(put_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) configured = true;
@@ -694,8 +698,12 @@ cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwo
   if (nwork <= 0) return cudaSuccess;
   e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
   if (e != cudaSuccess) return e;
-  put_fast_kernel<<<grid, SCHED_THREADS, sched_smem_bytes(), stream>>>(opts, order, nwork, counter, ws, ws_stride,
-                                                                         out);
+  if (out.acct)
+    put_fast_kernel<true><<<grid, SCHED_THREADS, sched_smem_bytes(), stream>>>(opts, order, nwork, counter, ws,
+                                                                               ws_stride, out);
+  else
+    put_fast_kernel<false><<<grid, SCHED_THREADS, sched_smem_bytes(), stream>>>(opts, order, nwork, counter, ws,
+                                                                                ws_stride, out);
   return cudaGetLastError();
 }
 

@@ -513,6 +513,16 @@ __device__ __forceinline__ int fft_ring(const Stencil& st, int h) {
 // the one-step stencil -- all terms nonnegative, ~m ulp relative accuracy
 // (tighter than the reference's FFT power).
 
+// Weight stash: the composed weights a shared-memory subtree's correlations
+// use, copied from the per-option kernel table (HBM) into shared memory so the
+// helpers' taps are shared-memory loads.  Subtree roots are <= 256 high, so
+// the node heights at depth d (1..3) are two consecutive values <= 128 / 64 / 32;
+// depth d holds W_key, W_key+1 (slots of WST_SZ[d] doubles at WST_OFF[d]).
+constexpr int WST_SZ1 = 257, WST_SZ2 = 129, WST_SZ3 = 65;
+constexpr int CHAIN_WSTASH = 2 * (WST_SZ1 + WST_SZ2 + WST_SZ3) + 2;
+__device__ __forceinline__ int wst_off(int d) { return d == 1 ? 0 : d == 2 ? 2 * WST_SZ1 : 2 * (WST_SZ1 + WST_SZ2); }
+__device__ __forceinline__ int wst_sz(int d) { return d == 1 ? WST_SZ1 : d == 2 ? WST_SZ2 : WST_SZ3; }
+
 constexpr int64_t KTABLE_DOUBLES = (int64_t)(KT_H + 2) * (KT_H + 2) * 2;
 
 // scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
@@ -872,6 +882,31 @@ __device__ __forceinline__ void publish_done(SchedShared& S, int ring, int idx) 
   S.done[ring][idx % QCAP] = idx;
 }
 
+// Make the composed weights of every correlation of a shared-memory subtree
+// rooted at height h0 resident in the chain's stash: each internal node at
+// depth d-1 correlates with W_m of its children's heights m (depth d), two
+// consecutive values per depth.  Slots are reused while they cover the
+// subtree (consecutive subtrees mostly share heights).
+__device__ void stash_weights(SchedShared& S, int c, double* wst, const double* kc, int h0, int leaf, int span) {
+  for (int d = 1; d <= 3; ++d) {
+    const int pmax = (h0 + (1 << (d - 1)) - 1) >> (d - 1);  // tallest node at depth d-1
+    if (pmax <= leaf) break;                                // depth d-1 is all leaves
+    const int lo = h0 >> d, hi = (h0 + (1 << d) - 1) >> d;
+    const int key = S.wkey[c][d];
+    if (key >= 0 && lo >= key && hi <= key + 1) continue;
+    for (int j = 0; j < 2; ++j) {
+      const int m = lo + j;
+      if (m > KT_H) break;
+      warp_stage_nb<9>(wst + wst_off(d) + j * wst_sz(d), kc + (int64_t)m * m, m * span + 1, m * span + 1);
+    }
+    if (lane_id() == 0) S.wkey[c][d] = lo;
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ const double* wslot(const SchedShared& S, int c, const double* wst, int d, int m) {
+  return wst + wst_off(d) + (m - S.wkey[c][d]) * wst_sz(d);
+}
+
 // Execute a generic task on a worker group; returns executed flops (or < 0 on error).
 // sbuf: the group's shared buffer (slots double2).
 __device__ double exec_generic(const Task& t, double2* sbuf, int slots, int logNmax, const double2* tq,
@@ -912,15 +947,6 @@ constexpr int CHAIN_SCRATCH = 2480;  // doubles of shared-memory scratch per cha
 constexpr int CHAIN_FRAME_DOUBLES = 288;
 constexpr int FRAME_SUB_OFF = 0;      // bytes: subtree walk (put_subtree / call_subtree)
 constexpr int FRAME_SOLVE_OFF = 384;  // bytes: the halving recursion above the subtrees
-// Weight stash: the composed weights a shared-memory subtree's correlations
-// use, copied from the per-option kernel table (HBM) into shared memory so the
-// helpers' taps are shared-memory loads.  Subtree roots are <= 256 high, so
-// the node heights at depth d (1..3) are two consecutive values <= 128 / 64 / 32;
-// depth d holds W_key, W_key+1 (slots of WST_SZ[d] doubles at WST_OFF[d]).
-constexpr int WST_SZ1 = 257, WST_SZ2 = 129, WST_SZ3 = 65;
-constexpr int CHAIN_WSTASH = 2 * (WST_SZ1 + WST_SZ2 + WST_SZ3) + 2;
-__device__ __forceinline__ int wst_off(int d) { return d == 1 ? 0 : d == 2 ? 2 * WST_SZ1 : 2 * (WST_SZ1 + WST_SZ2); }
-__device__ __forceinline__ int wst_sz(int d) { return d == 1 ? WST_SZ1 : d == 2 ? WST_SZ2 : WST_SZ3; }
 constexpr int CHAIN_SMEM = CHAIN_SCRATCH + CHAIN_FRAME_DOUBLES + CHAIN_WSTASH;
 __device__ __forceinline__ double* chain_wstash(double* scratch) { return scratch + CHAIN_SCRATCH + CHAIN_FRAME_DOUBLES; }
 template <class F>

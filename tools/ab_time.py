@@ -6,7 +6,7 @@ import numpy as np
 import torch
 from paper_2303_02317_b200.workloads import draw_config
 
-b = draw_config(6, n=256)
+b = draw_config(int(os.environ.get('AB_CFG', 6)), n=int(os.environ.get('AB_N', 256)))
 P, i64, i32, d, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int
 ptr = lambda a: a.ctypes.data_as(P)
 kind = np.ascontiguousarray(b.kind, dtype=np.int8)

@@ -33,7 +33,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&x, 8 << 20); cudaMalloc(&y, 8 << 20); cudaMalloc(&c, 64); cudaMemset(x, 0, 8 << 20);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   struct Case { int nthr, logN; int64_t Lout; int hh; };
-  Case cs[] = {{32, 10, 64, 64}, {32, 10, 256, 128}, {32, 10, 512, 200}, {128, 11, 1024, 512}, {128, 13, 4096, 2048},
+  Case cs[] = {{128, 12, 2048, 300}, {128, 12, 1024, 1000}, {128, 11, 1024, 512}, {128, 13, 4096, 2048},
                {128, 13, 16384, 8192}, {256, 13, 4096, 2048}, {256, 13, 16384, 8192}};
   int ci = -1;
   for (auto& k : cs) {
