@@ -9,6 +9,7 @@
 
 namespace fl {
 
+template <bool ACCT>  // see PutPricer: production and accounting kernel instances
 struct AmericanPricer {
   const PutParams* put;
   const CallParams* call;
@@ -18,7 +19,7 @@ struct AmericanPricer {
     const int e = order[w];
     if (e >= 0) {
       double ref = 0.0;
-      put_chain_option<true>(S, c, put[e], e, arena, scratch, out, flops, &ref);  // (run-time acct flag)
+      put_chain_option<ACCT>(S, c, put[e], e, arena, scratch, out, flops, &ref);
       if (lane_id() == 0 && out.flops) atomicAdd(out.flops + 1, (unsigned long long)ref);
     } else {
       const int o = -e - 1;
@@ -32,11 +33,12 @@ struct AmericanPricer {
   }
 };
 
+template <bool ACCT>
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 american_fast_kernel(const PutParams* __restrict__ put, const CallParams* __restrict__ call,
                      const int32_t* __restrict__ order, int nwork, int32_t* counter, double* __restrict__ ws,
                      int64_t ws_stride, BatchOut out) {
-  const AmericanPricer pr{put, call, order, out};
+  const AmericanPricer<ACCT> pr{put, call, order, out};
   sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
 
@@ -46,14 +48,21 @@ cudaError_t launch_american_fast(const PutParams* put, const CallParams* call, c
   static bool configured = false;
   const int smem = sched_smem_bytes();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(american_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(american_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(american_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   if (nwork <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);
   if (e != cudaSuccess) return e;
-  american_fast_kernel<<<grid, SCHED_THREADS, smem, stream>>>(put, call, order, nwork, counter, ws, ws_stride, out);
+  if (out.acct)
+    american_fast_kernel<true><<<grid, SCHED_THREADS, smem, stream>>>(put, call, order, nwork, counter, ws, ws_stride,
+                                                                      out);
+  else
+    american_fast_kernel<false><<<grid, SCHED_THREADS, smem, stream>>>(put, call, order, nwork, counter, ws,
+                                                                       ws_stride, out);
   return cudaGetLastError();
 }
 
