@@ -270,6 +270,10 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
   return 0;
 }
 
+// CTAs for a fast batch of n items: one per item while they fit on the SMs
+// (each runs alone, sched_body's solo mode), else NCHAIN items per CTA.
+static int grid_for(int n, int nc, int nsm) { return n <= nsm ? n : std::min((n + nc - 1) / nc, nsm); }
+
 int upload(fl_batch* b, cudaStream_t stream) {
   const int64_t n = b->n;
   FL_CUDA(cudaGetDevice(&b->dev));
@@ -312,19 +316,19 @@ int upload(fl_batch* b, cudaStream_t stream) {
   if (!b->o_put_fast.empty()) {
     b->ws_put_stride = fl::put_ws_doubles(nmax_put, ksmax);
     const int nc = fl::put_chains_per_cta();
-    b->grid_put = std::min<int>(((int)b->o_put_fast.size() + nc - 1) / nc, nsm);
+    b->grid_put = grid_for((int)b->o_put_fast.size(), nc, nsm);
     FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_put_stride * b->grid_put * nc));
   }
   if (!b->o_call_fast.empty()) {
     b->ws_call_stride = fl::call_ws_doubles(nmax_call);
     const int nc = fl::call_chains_per_cta();
-    b->grid_call = std::min<int>(((int)b->o_call_fast.size() + nc - 1) / nc, nsm);
+    b->grid_call = grid_for((int)b->o_call_fast.size(), nc, nsm);
     FL_CUDA(b->d_ws_call.ensure(sizeof(double) * b->ws_call_stride * b->grid_call * nc));
   }
   if (!b->o_mixed.empty()) {
     b->ws_mixed_stride = std::max(b->ws_put_stride, b->ws_call_stride);
     const int nc = fl::put_chains_per_cta();
-    b->grid_mixed = std::min<int>(((int)b->o_mixed.size() + nc - 1) / nc, nsm);
+    b->grid_mixed = grid_for((int)b->o_mixed.size(), nc, nsm);
     FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_mixed_stride * b->grid_mixed * nc));
   }
   const int64_t nbase = (int64_t)std::max({b->o_put_base.size(), b->o_call_base.size(), b->o_euro_base.size()});

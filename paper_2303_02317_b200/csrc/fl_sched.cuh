@@ -1027,10 +1027,21 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     const int c = rank;
     double* arena = ws + ((int64_t)blockIdx.x * NCHAIN + c) * ws_stride;
     double chain_flops = 0.0;
+    // A batch with no more items than CTAs runs one item per CTA on chain 0
+    // (an option alone on an SM runs ~1.5x faster than a co-resident pair);
+    // otherwise chains claim items dynamically in decreasing-cost order.
+    const bool solo = nwork <= (int)gridDim.x;
+    bool taken = false;
     for (;;) {
       int w = 0;
-      if (lane_id() == 0) w = atomicAdd(counter, 1);
-      w = __shfl_sync(FULL, w, 0);
+      if (solo) {
+        if (taken || c != 0) break;
+        w = (int)blockIdx.x;
+        taken = true;
+      } else {
+        if (lane_id() == 0) w = atomicAdd(counter, 1);
+        w = __shfl_sync(FULL, w, 0);
+      }
       if (w >= nwork) break;
       unsigned long long ts = 0;
       if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
