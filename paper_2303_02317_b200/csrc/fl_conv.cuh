@@ -38,6 +38,10 @@ namespace fl {
 
 constexpr int CTA_THREADS = 256;
 
+#ifndef FL_SPEC_SKIP  // 1: bin pairs whose spectrum values are both cut skip the split / multiply / re-pack
+#define FL_SPEC_SKIP 1
+#endif
+
 // A cooperating thread group: index t in [0, n); bar >= 0 -> named barrier,
 // bar < 0 -> the group is one warp (n == 32).
 struct Grp {
@@ -329,6 +333,21 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
     for (int k = g.t; k <= C / 2; k += g.n) {
       const int kc = (C - k) & (C - 1);
       const int pk = slot_of(k, logC), pc = slot_of(kc, logC);
+#if FL_SPEC_SKIP
+      {  // both spectrum values below the 1e-24 cut: the bin pair is zero, skip its loads and math
+        const double2 omk = cconj(Wk), omc = make_double2(-Wk.x, -Wk.y);
+        const double2 omk2 = cmul(omk, omk), omc2 = cmul(omc, omc);
+        const double2 bk = make_double2(st.c0 + st.c1 * omk.x + st.c2 * omk2.x, st.c1 * omk.y + st.c2 * omk2.y);
+        const double2 bc = make_double2(st.c0 + st.c1 * omc.x + st.c2 * omc2.x, st.c1 * omc.y + st.c2 * omc2.y);
+        if (cnorm2(bk) < pl.tau && cnorm2(bc) < pl.tau) {
+          buf[pidx(pk)] = make_double2(0.0, 0.0);
+          if (k != 0 && k != C / 2) buf[pidx(pc)] = make_double2(0.0, 0.0);
+          Wk = cmul(Wk, Wstep);
+          ph = cmul(ph, phstep);
+          continue;
+        }
+      }
+#endif
       const double2 Zk = buf[pidx(pk)];
       const double2 Zc = buf[pidx(pc)];
       const double2 E = make_double2(0.5 * (Zk.x + Zc.x), 0.5 * (Zk.y - Zc.y));
