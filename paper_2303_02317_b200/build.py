@@ -41,14 +41,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     extra = os.environ.get("FL_NVCC_FLAGS", "").split()
+    out = os.environ.get("FL_LIB_OUT", LIB)  # tool builds (A/B variants) write elsewhere
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "fl_lib.cu")]
+           "-Xptxas", "-warn-spills", *extra, "-o", out + ".tmp", os.path.join(CSRC, "fl_lib.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -855,6 +855,7 @@ int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double
 
 int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
   if (!b) return fail("fl_batch_profile: null batch");
+  if (!FL_PROF) return fail("fl_batch_profile: library built without profile counters (build with FL_NVCC_FLAGS=-DFL_PROF=1)");
   FL_CUDA(cudaMemcpyAsync(counters56, b->d_stats.as<unsigned long long>() + 8, 56 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -863,6 +864,7 @@ int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
 
 int fl_batch_timeline(fl_batch* b, uint64_t* out3n, void* stream) {
   if (!b || !out3n) return fail("fl_batch_timeline: null argument");
+  if (!FL_PROF) return fail("fl_batch_timeline: library built without profile counters (build with FL_NVCC_FLAGS=-DFL_PROF=1)");
   FL_CUDA(cudaMemcpyAsync(out3n, b->d_stats.as<unsigned long long>() + 64, 3 * b->n * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

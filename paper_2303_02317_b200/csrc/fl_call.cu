@@ -236,9 +236,9 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
   const int64_t jp = call_leaf_warp(P, in_org, out_org, j - h + 1, i, j, h, &cells);
 #endif
   if (X.acct) X.flops += 5ull * (uint64_t)cells;
-  if (X.prof && lane_id() == 0) {
-    prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
-    prof_add(X.prof, PROF_STRIP_N, h);
+  if (FL_PROFP(X.prof) && lane_id() == 0) {
+    prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
+    prof_add(FL_PROFP(X.prof), PROF_STRIP_N, h);
   }
   return jp;
 }
@@ -320,18 +320,18 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       --sp;
     }
   }
-  if (X.prof && lane_id() == 0) {
-    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
-    prof_add(X.prof, PROF_F_MID, twait);
-    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
-    prof_add(X.prof, PROF_FUSE_N, 1);
+  if (FL_PROFP(X.prof) && lane_id() == 0) {
+    prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
+    prof_add(FL_PROFP(X.prof), PROF_F_MID, twait);
+    prof_add(FL_PROFP(X.prof), PROF_FUSE_CYC, clock64() - t1);
+    prof_add(FL_PROFP(X.prof), PROF_FUSE_N, 1);
   }
   return ret;
 }
 
 __device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                           int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.prof);
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_PROFP(X.prof));
 }
 
 // _solve (american.py:201-257) with an explicit stack on the chain warp.
@@ -427,7 +427,7 @@ __device__ void call_trapezoids(CallChainCtx& X, const CallParams& P, int64_t& i
     const int64_t L = j - first + 1;
     if (L > hh) {
       X.ref_q += 4ull * call_ref_jump(L, hh + 1);
-      chain_conv(*X.S, X.c, X.st, cur_org + first, L, nxt_org + first, L - hh, h, X.kc, X.prof, true);
+      chain_conv(*X.S, X.c, X.st, cur_org + first, L, nxt_org + first, L - hh, h, X.kc, FL_PROFP(X.prof), true);
     }
     const int64_t jp = call_solve(X, P, i, j, h, cur_org, nxt_org, err);
     if (*err) return;

@@ -42,6 +42,11 @@ constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 #define FL_STRIP_PIPE 1
 #endif
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
+#ifndef FL_STRIP_SLIDE  // 1: sliding-frame leaf strips (put_strip_slide) for options with the exercise margin
+#define FL_STRIP_SLIDE 0
+#endif
+constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 31) / 32;  // cells per lane of the sliding frame
+constexpr int PUT_SLIDE_H = (32 * PUT_SLIDE_CPL - 2) / 2;     // tallest strip it holds
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
 #endif
@@ -165,19 +170,27 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   const long long t1 = clock64();
   long long tm[2] = {0, 0};
   FL_TR(*X.S, X.c, EV_LEAF_B, height);
-#if FL_STRIP_PIPE
+#if FL_STRIP_SLIDE
+  // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
+  const int64_t kb =
+      (P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height)
+          ? put_strip_slide<PUT_SLIDE_CPL, 1>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
+                                              FL_PROFP(X.prof) ? tm : nullptr)
+          : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
+                                    FL_PROFP(X.prof) ? tm : nullptr);
+#elif FL_STRIP_PIPE
   const int64_t kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                             X.prof ? tm : nullptr);
+                                             FL_PROFP(X.prof) ? tm : nullptr);
 #else
   const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                             X.prof ? tm : nullptr);
+                                             FL_PROFP(X.prof) ? tm : nullptr);
 #endif
   FL_TR(*X.S, X.c, EV_LEAF_E, height);
-  if (X.prof && lane_id() == 0) {
-    prof_add(X.prof, PROF_STRIP_CYC, clock64() - t1);
-    prof_add(X.prof, PROF_STRIP_N, height);
-    prof_add(X.prof, PROF_STRIP_LOOP, tm[1]);
-    prof_add(X.prof, PROF_LEAF_LOAD, tm[0] - t1);
+  if (FL_PROFP(X.prof) && lane_id() == 0) {
+    prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
+    prof_add(FL_PROFP(X.prof), PROF_STRIP_N, height);
+    prof_add(FL_PROFP(X.prof), PROF_STRIP_LOOP, tm[1]);
+    prof_add(FL_PROFP(X.prof), PROF_LEAF_LOAD, tm[0] - t1);
   }
   if (!FL_ABL && ACCT && X.acct) X.flops += ref_strip_flops(hi - lo + 1, height);
   FL_TR(*X.S, X.c, EV_MARK, 1);
@@ -286,13 +299,13 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       --sp;
     }
   }
-  if (X.prof && lane_id() == 0) {
-    prof_add(X.prof, PROF_WAIT_CYC, t1 - t0);
-    prof_add(X.prof, PROF_F_STAGE, t2 - t1);
-    prof_add(X.prof, PROF_F_MID, twait);
-    prof_add(X.prof, PROF_F_BOT, tpost);
-    prof_add(X.prof, PROF_FUSE_CYC, clock64() - t1);
-    prof_add(X.prof, PROF_FUSE_N, 1);
+  if (FL_PROFP(X.prof) && lane_id() == 0) {
+    prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
+    prof_add(FL_PROFP(X.prof), PROF_F_STAGE, t2 - t1);
+    prof_add(FL_PROFP(X.prof), PROF_F_MID, twait);
+    prof_add(FL_PROFP(X.prof), PROF_F_BOT, tpost);
+    prof_add(FL_PROFP(X.prof), PROF_FUSE_CYC, clock64() - t1);
+    prof_add(FL_PROFP(X.prof), PROF_FUSE_N, 1);
   }
   FL_TR(*X.S, X.c, EV_SUB_E, h0);
   return ret;
@@ -300,7 +313,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
 
 __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                          int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, X.prof);
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_PROFP(X.prof));
 }
 
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
@@ -370,7 +383,7 @@ __device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int6
   const int h = (int)hh;
   if (red > 2 * hh) {  // far: cols f+h+1 .. f+red-h stay linear
     X.ref_flops += ref_jump_flops(red, 2 * hh + 1);
-    chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc, X.prof, true);
+    chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc, FL_PROFP(X.prof), true);
   }
   return put_solve_q<ACCT>(X, P, f, cur_org, nxt_org, h, err);
 }

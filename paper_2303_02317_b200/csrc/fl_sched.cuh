@@ -40,6 +40,10 @@ namespace fl {
 //                subtrees, fed through a request ring (no deps scan)
 // Groups execute one task at a time over 128 threads (named barriers 1, 2).
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
+#ifndef FL_PROF  // 1: scheduler profile counters (FL_PROFILE=1 at run time); tool builds only --
+#define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
+#endif
+#define FL_PROFP(p) (FL_PROF ? (p) : nullptr)
 #ifndef FL_NHELP
 #define FL_NHELP 3
 #endif
@@ -241,7 +245,7 @@ enum : int {
 };
 
 __device__ __forceinline__ void prof_add(unsigned long long* prof, int slot, unsigned long long v) {
-  if (prof) atomicAdd(prof + slot, v);
+  if (FL_PROF && prof) atomicAdd(prof + slot, v);
 }
 
 // Event trace of the chain pricing work item 0 (FL_TRACE builds only; a tool,
@@ -409,29 +413,29 @@ __device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1
     if (n == 0) break;
     const int m = n < 8 ? n : 8;
     for (int i = 0; i < m; ++i) {
-      const long long t0 = S.prof ? clock64() : 0;
-      if (S.prof && lane_id() == 0 && rawf[i]) {
+      const long long t0 = FL_PROFP(S.prof) ? clock64() : 0;
+      if (FL_PROFP(S.prof) && lane_id() == 0 && rawf[i]) {
         const int rg = (int)((unsigned)ids[i] >> 28), ix = ids[i] & 0x0fffffff;
         const Task& tk = S.ring[rg][ix % QCAP];
-        prof_add(S.prof, PROF_W_SUML, (unsigned long long)tk.L);
-        prof_add(S.prof, PROF_W_SUMH, (unsigned long long)tk.h);
-        prof_add(S.prof, PROF_W_FFT, tk.kind == TK_FFT ? 1ull : 0ull);
-        if ((unsigned long long)tk.L > S.prof[PROF_W_MAXL]) {  // debug: describe the longest waited task
-          S.prof[PROF_W_MAXL] = tk.L;
-          S.prof[PROF_W_MAXL + 1] = tk.Lout;
-          S.prof[PROF_W_MAXL + 2] = tk.h;
-          S.prof[PROF_W_MAXL + 3] = (unsigned long long)(tk.y - tk.x);
+        prof_add(FL_PROFP(S.prof), PROF_W_SUML, (unsigned long long)tk.L);
+        prof_add(FL_PROFP(S.prof), PROF_W_SUMH, (unsigned long long)tk.h);
+        prof_add(FL_PROFP(S.prof), PROF_W_FFT, tk.kind == TK_FFT ? 1ull : 0ull);
+        if ((unsigned long long)tk.L > FL_PROFP(S.prof)[PROF_W_MAXL]) {  // debug: describe the longest waited task
+          FL_PROFP(S.prof)[PROF_W_MAXL] = tk.L;
+          FL_PROFP(S.prof)[PROF_W_MAXL + 1] = tk.Lout;
+          FL_PROFP(S.prof)[PROF_W_MAXL + 2] = tk.h;
+          FL_PROFP(S.prof)[PROF_W_MAXL + 3] = (unsigned long long)(tk.y - tk.x);
         }
         // histogram of waited-task h: slots +4 .. +8 for h <= 64, 128, 256, 512, larger
         const int hb = tk.h <= 64 ? 0 : tk.h <= 128 ? 1 : tk.h <= 256 ? 2 : tk.h <= 512 ? 3 : 4;
-        prof_add(S.prof, PROF_W_MAXL + 4 + hb, 1);
-        prof_add(S.prof, PROF_W_MAXL + 9 + hb, (unsigned long long)tk.L);
+        prof_add(FL_PROFP(S.prof), PROF_W_MAXL + 4 + hb, 1);
+        prof_add(FL_PROFP(S.prof), PROF_W_MAXL + 9 + hb, (unsigned long long)tk.L);
       }
       warp_wait_done(S, ids[i]);
-      if (S.prof && lane_id() == 0) {
+      if (FL_PROFP(S.prof) && lane_id() == 0) {
         const int big = ((unsigned)ids[i] >> 28) == RING_BIG;
-        prof_add(S.prof, (rawf[i] ? PROF_W_RAW_S : PROF_W_WAR_S) + big, clock64() - t0);
-        prof_add(S.prof, PROF_W_N, 1);
+        prof_add(FL_PROFP(S.prof), (rawf[i] ? PROF_W_RAW_S : PROF_W_WAR_S) + big, clock64() - t0);
+        prof_add(FL_PROFP(S.prof), PROF_W_N, 1);
       }
     }
     if (n <= 8) break;
@@ -447,11 +451,11 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
   int* deps = S.cw_deps[c];
   int nd;
   FL_TR(S, c, EV_IS_B, ring);
-  const long long t0 = S.prof ? clock64() : 0;
+  const long long t0 = FL_PROFP(S.prof) ? clock64() : 0;
   long long t1 = 0, t2 = 0;
   for (;;) {
     nd = scan_conflicts(S, c, rlo, rhi, 0, 0, wlo, whi, deps, NDEP);
-    if (S.prof && t1 == 0) t1 = clock64();
+    if (FL_PROFP(S.prof) && t1 == 0) t1 = clock64();
     if (nd <= NDEP) break;
     warp_wait_done(S, deps[0]);  // too many: retire the oldest conflict first
   }
@@ -465,14 +469,14 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
   int idx = 0;
   if (lane_id() == 0) idx = atomicAdd(&S.reserve[ring], 1);
   idx = __shfl_sync(FULL, idx, 0);
-  if (S.prof) t2 = clock64();
+  if (FL_PROFP(S.prof)) t2 = clock64();
   // the slot's previous occupant must be finished
   while (!__shfl_sync(FULL, (int)(S.done[ring][idx % QCAP] >= idx - QCAP), 0)) __nanosleep(64);
-  if (S.prof && lane_id() == 0) {
+  if (FL_PROFP(S.prof) && lane_id() == 0) {
     const long long t3 = clock64();
-    prof_add(S.prof, PROF_ISS_SCAN, t1 - t0);
-    prof_add(S.prof, PROF_ISS_STALL, t2 - t1);
-    prof_add(S.prof, PROF_ISS_SLOT, t3 - t2);
+    prof_add(FL_PROFP(S.prof), PROF_ISS_SCAN, t1 - t0);
+    prof_add(FL_PROFP(S.prof), PROF_ISS_STALL, t2 - t1);
+    prof_add(FL_PROFP(S.prof), PROF_ISS_SLOT, t3 - t2);
   }
   const int id = (ring << 28) | (idx & 0x0fffffff);  // ring in bits 28..31
   if (lane_id() == 0) {
@@ -1044,7 +1048,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       }
       if (w >= nwork) break;
       unsigned long long ts = 0;
-      if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+      if (FL_PROFP(prof)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
 #if FL_TRACE
       if (lane_id() == 0) S.trace_c = (w == 0) ? c : (S.trace_c == c ? -1 : S.trace_c);
       __syncwarp();
@@ -1052,7 +1056,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       FL_TR(S, c, EV_OPT_B, w);
       pr.chain(S, c, w, arena, chain_scratch + c * CHAIN_SMEM, &chain_flops);
       FL_TR(S, c, EV_OPT_E, w);
-      if (prof && lane_id() == 0) {  // timeline of work item w: start / end ns, SM and chain
+      if (FL_PROFP(prof) && lane_id() == 0) {  // timeline of work item w: start / end ns, SM and chain
         unsigned long long te, sm;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(te));
         asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(sm));
@@ -1157,7 +1161,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     gsync(g);
     if (g.t == 0) {
       publish_done(S, tring, idx);
-      if (prof) {
+      if (FL_PROFP(prof)) {
         const int ps = gi == 0 ? PROF_BIG_CYC
                                : (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
         prof_add(prof, ps, clock64() - t1);

@@ -252,6 +252,116 @@ __device__ int64_t put_strip_v2(const double* __restrict__ in_org, double* __res
   return kb;
 }
 
+// Sliding-frame put strip.  Same contract as put_strip_warp (lo = f-2h-1,
+// hi = f+2h) but the frame follows the valid cone: at row s it holds only
+// the 2h+2 columns f-s-1 .. f+2h-s, cell j = column f-s-1+j.  Two facts make
+// that exact:
+//   * right side: the reference's valid range shrinks by one column per row
+//     (_accel.py:203-242: after s rows only [lo+s, hi-s] is valid), so
+//     columns right of f+2h-s never influence the final valid range;
+//   * left side: at row s every column < f-s is an exercise cell whose value
+//     is its payoff (the boundary drops by at most one column per row: a cell
+//     whose three parents are exercise cells gets lin = payoff - omega*dtau +
+//     O(dtau ds^2) < payoff; the host checks that margin per option,
+//     PutParams::slide, and options that fail it use put_strip_pipe).
+// In frame coordinates the stencil is left-shifted, new u[j] = F(u[j-2],
+// u[j-1], u[j]), so a lane needs two cells from its left neighbour and none
+// from its right: one shuffle direction, and the lane's last cell of the next
+// row depends on its own cells only.  The loop-carried path is one shuffle,
+// one DFMA and one max per row; each row costs 3 CPL FP64 ops + CPL maxes
+// instead of the 4h+2 frame's 5 x (3 + 1).  Lane 0's two left cells are the
+// payoffs of columns f-s-3, f-s-2.  Per-cell arithmetic is put_strip_warp's
+// interior order: fma(cd, left, fma(cu, right, cm * cur)), projected by max
+// (equal to the reference's lin > pay ? lin : pay), exercise iff !(lin > pay).
+// Requires 2h+2 <= 32*CPL.  pay_org must cover cols f-h-2 .. f+2h.
+template <int CPL, int PAYMODE = 0>
+__device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 2, "two left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = lane * CPL;
+  const bool l0 = lane == 0;
+  // row 0: cols f-1+j; cols <= f hold the payoff, f+1 .. f+2h the input segment
+  const double* pay0 = pay_org + (f - 1);
+  // cells past the frame (j >= W: idle lanes, the tail of the last lane) read
+  // the frame's last column; their values never reach a cell j < W
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];  // payoff of cell j at row 0 (col f-1+j)
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  // lane 0's left fills: at row s cells -2, -1 are cols f-s-3, f-s-2 (exercise
+  // cells: their payoff).  Lane i keeps pay(f-3-i) for row i's broadcast.
+  const double fillv = (lane <= height) ? pay_org[f - 3 - lane] : 0.0;
+  double fill1 = pay_org[f - 2];
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] + fill1 == 12345.678 ? 1 : 0); }
+  const double* pq = pay0 - 1;  // row s+1 payoff of cell j: pq[j - s]
+  unsigned green = 0;
+  for (int s = 0; s < height; ++s) {
+    const double fill2 = __shfl_sync(FULL, fillv, s);
+    double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    L2 = l0 ? fill2 : L2;
+    L1 = l0 ? fill1 : L1;
+    // payoffs of row s+1 (col f-s-2+j = col of cell j-1 at row s)
+    double np[CPL];
+    if (PAYMODE == 0) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) np[c] = pq[jx[c] - s];
+    } else {
+      const double pl = __shfl_up_sync(FULL, p[CPL - 1], 1);
+      np[0] = l0 ? fill1 : pl;
+#pragma unroll
+      for (int c = 1; c < CPL; ++c) np[c] = p[c - 1];
+    }
+    double nu[CPL];
+    // the lane's last cells first (local inputs), so the next row's shuffles issue early
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) {
+      const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+      nu[c] = lin > np[c] ? lin : np[c];
+    }
+    const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+    const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
+    nu[1] = lin1 > np[1] ? lin1 : np[1];
+    nu[0] = lin0 > np[0] ? lin0 : np[0];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      u[c] = nu[c];
+      p[c] = np[c];
+    }
+    fill1 = fill2;
+  }
+  // exercise flags of the final row: the reference's cell is exercise iff
+  // !(lin > pay), i.e. iff its projected value is exactly its payoff
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  // final row: cell j = col f-h-1+j, j < W is the reference's final valid range
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
 // Time-tiled variant of put_strip_warp: lanes exchange K halo cells per side
 // once per K rows (instead of one cell per side per row) and advance K rows on
 // an extended register tile, recomputing the halo cone redundantly.  One

@@ -38,6 +38,8 @@ struct PutParams {
   int64_t n, ks;
   int32_t cutoff, mode;
   double price;  // host-decided price (MODE_INTRINSIC)
+  int32_t slide;  // 1: exercise cells provably stay exercise (sliding-frame leaf strips)
+  int32_t pad;
 };
 
 struct CallParams {
@@ -258,10 +260,22 @@ inline int32_t discretize_put(const SpecIn& s, double lam, PutDisc& d) {
 inline int32_t prep_put(const SpecIn& s, double lam, int64_t cutoff, PutParams& p) {
   PutDisc d;
   p.S = s.S; p.K = s.K; p.n = s.T; p.cutoff = (int32_t)cutoff; p.price = 0.0;
-  p.cd = p.cm = p.cu = p.ds = 0.0; p.ks = 0;
+  p.cd = p.cm = p.cu = p.ds = 0.0; p.ks = 0; p.slide = 0; p.pad = 0;
   int32_t st = discretize_put(s, lam, d);
   if (st) { p.mode = MODE_ERROR; return st; }
   p.cd = d.cd; p.cm = d.cm; p.cu = d.cu; p.ds = d.d_s; p.ks = d.ks;
+  // A cell whose three parents hold the payoff g(x) = 1 - e^x (x = col ds <= 0,
+  // the exercise side of the strike node) gets lin - g = -omega dtau +
+  // e^x (1 - A), A = cd e^-ds + cm + cu e^ds (cd + cm + cu = 1 - omega dtau).
+  // When that is negative for every x <= 0 with a margin far above the
+  // rounding of lin (~1e-15), exercise cells stay exercise cells and the
+  // boundary drops by at most one column per row: the leaf strips may then
+  // skip every column left of the moving boundary (put_strip_slide).
+  {
+    const double A = d.cd * std::exp(-d.d_s) + d.cm + d.cu * std::exp(d.d_s);
+    const double rise = 1.0 - A > 0.0 ? 1.0 - A : 0.0;
+    p.slide = (d.omega * d.d_tau - rise > 1e-12) ? 1 : 0;
+  }
   if (cutoff < 1) { p.mode = MODE_ERROR; return FL_E_VALIDATION | FL_F_CUTOFF; }
   if (d.ks <= -d.n) { p.mode = MODE_INTRINSIC; p.price = s.K - s.S; return FL_OK; }
   if (d.n <= 2 * cutoff) { p.mode = MODE_BASELINE; return FL_OK; }
