@@ -69,7 +69,8 @@ int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double*
  *   EURO: dparams = {wd, wu, gauged wu e^{2 lu}, lu}     (binomial.py:161-194)
  *   CALL: dparams = {wd, wu, lu, closed price}, iparams = {terminal boundary,
  *         row T-1 boundary}                             (american.py:260-470)
- *   PUT:  dparams = {cd, cm, cu, ds}, iparams = {k*}    (bsm.py:150-229, 585-625)
+ *   PUT:  dparams = {cd, cm, cu, ds}, iparams = {k*, sliding-strip flag}
+ *                                                       (bsm.py:150-229, 585-625)
  * dparams: n x 4 doubles, iparams: n x 2 int64. */
 int fl_inspect(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R, const double* Y,
                const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,

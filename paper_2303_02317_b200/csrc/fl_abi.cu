@@ -196,6 +196,10 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
   b->cost.assign(n, 0.0);
   for (auto* v : {&b->o_put_fast, &b->o_put_base, &b->o_call_fast, &b->o_call_base, &b->o_euro_fast, &b->o_euro_base})
     v->clear();
+  // FL_FULL_STRIPS=1 (tests only): disable the sliding-frame put leaf strips, so
+  // the full-frame fallback is exercised on well-conditioned options too
+  const char* fs = std::getenv("FL_FULL_STRIPS");
+  const bool full_strips = fs && fs[0] == '1';
   for (int64_t i = 0; i < n; ++i) {
     const fl::SpecIn s{S[i], K[i], R[i], Y[i], V[i], E[i], T[i]};
     const int32_t o = (int32_t)i;
@@ -234,6 +238,7 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
       }
       case FL_KIND_PUT: {
         st = fl::prep_put(s, lam, put_cutoff, b->put[i]);
+        if (full_strips) b->put[i].slide = 0;  // test knob: every leaf on the full 4h+2 frame
         if (method == FL_METHOD_BASELINE) {
           // baseline_put_fd: discretization errors only, no cutoff / intrinsic dispatch
           if (!st || (st == (FL_E_VALIDATION | FL_F_CUTOFF))) {
@@ -579,7 +584,7 @@ int fl_inspect(int64_t n, const int8_t* kind, const double* S, const double* K, 
     } else if (kind[i] == FL_KIND_PUT) {
       fl::PutParams p;
       st = fl::prep_put(s, lam, put_cutoff, p);
-      if (!st) { md = p.mode; d[0] = p.cd; d[1] = p.cm; d[2] = p.cu; d[3] = p.ds; q[0] = p.ks; }
+      if (!st) { md = p.mode; d[0] = p.cd; d[1] = p.cm; d[2] = p.cu; d[3] = p.ds; q[0] = p.ks; q[1] = p.slide; }
     } else {
       st = FL_E_VALIDATION;
     }

@@ -35,7 +35,7 @@
 namespace fl {
 
 #ifndef FL_PUT_LEAF
-#define FL_PUT_LEAF 32
+#define FL_PUT_LEAF 64
 #endif
 constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 #ifndef FL_STRIP_PIPE  // 1: leaf strips with the software-pipelined neighbour exchange
@@ -43,7 +43,7 @@ constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
 #endif
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
 #ifndef FL_STRIP_SLIDE  // 1: sliding-frame leaf strips (put_strip_slide) for options with the exercise margin
-#define FL_STRIP_SLIDE 0
+#define FL_STRIP_SLIDE 1
 #endif
 constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 31) / 32;  // cells per lane of the sliding frame
 constexpr int PUT_SLIDE_H = (32 * PUT_SLIDE_CPL - 2) / 2;     // tallest strip it holds

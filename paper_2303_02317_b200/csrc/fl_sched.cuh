@@ -40,6 +40,14 @@ namespace fl {
 //                subtrees, fed through a request ring (no deps scan)
 // Groups execute one task at a time over 128 threads (named barriers 1, 2).
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
+#ifndef FL_DEDUP  // 1: the chain's big, rarely-hot helpers are real calls (one copy in the kernel, fewer i-cache misses)
+#define FL_DEDUP 0  // measured: the calls add spills, 15.4 -> 17.4 ms
+#endif
+#if FL_DEDUP
+#define FL_COLD __noinline__
+#else
+#define FL_COLD
+#endif
 #ifndef FL_PROF  // 1: scheduler profile counters (FL_PROFILE=1 at run time); tool builds only --
 #define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
 #endif
@@ -369,7 +377,7 @@ __device__ __forceinline__ void warp_wait_done(const SchedShared& S, int id) {
 
 // The chain's unfinished tasks conflicting with the given ranges, in issue
 // order, into out[0..min(n,cap)); returns n.
-__device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+__device__ FL_COLD int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                               uintptr_t w0, uintptr_t w1, int* out, int cap, int* rawf = nullptr) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
@@ -403,7 +411,7 @@ __device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr
 
 // Chain c waits for its unfinished tasks that conflict with a region it is
 // about to read (r0/r1, r2/r3) and write (w0/w1).
-__device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+__device__ FL_COLD void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                                uintptr_t w0, uintptr_t w1) {
   int* ids = S.cw_ids[c];
   int* rawf = S.cw_raw[c];
@@ -446,7 +454,7 @@ __device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1
 
 // Issue a task from chain warp `c` (all 32 lanes call).  Returns its id.
 // rlo/rhi: read range; wlo/whi: write range.
-__device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
+__device__ FL_COLD int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
                      uintptr_t whi) {
   int* deps = S.cw_deps[c];
   int nd;
@@ -499,7 +507,7 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
 }
 
 // Chain c waits for all of its issued tasks.
-__device__ void wait_all_own(SchedShared& S, int c) {
+__device__ FL_COLD void wait_all_own(SchedShared& S, int c) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
   for (int i = first; i < np; ++i) warp_wait_done(S, S.pend[c][i % PEND_CAP].id);
@@ -530,7 +538,7 @@ __device__ __forceinline__ int wst_sz(int d) { return d == 1 ? WST_SZ1 : d == 2 
 constexpr int64_t KTABLE_DOUBLES = (int64_t)(KT_H + 2) * (KT_H + 2) * 2;
 
 // scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
-__device__ void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
+__device__ FL_COLD void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
   const int lane = lane_id();
   const int span = st.span;
   double* a = scratch;
@@ -824,7 +832,7 @@ __device__ __forceinline__ void warp_stage(double* dst, const double* src, int n
 
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
 // or an FFT task, on the small or big ring.
-__device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
+__device__ FL_COLD void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
                            int64_t Lout, int h, const double* kc, unsigned long long* prof, bool low = false) {
   if (Lout <= 0) return;
   Task t;
@@ -891,7 +899,7 @@ __device__ __forceinline__ void publish_done(SchedShared& S, int ring, int idx) 
 // depth d-1 correlates with W_m of its children's heights m (depth d), two
 // consecutive values per depth.  Slots are reused while they cover the
 // subtree (consecutive subtrees mostly share heights).
-__device__ void stash_weights(SchedShared& S, int c, double* wst, const double* kc, int h0, int leaf, int span) {
+__device__ FL_COLD void stash_weights(SchedShared& S, int c, double* wst, const double* kc, int h0, int leaf, int span) {
   for (int d = 1; d <= 3; ++d) {
     const int pmax = (h0 + (1 << (d - 1)) - 1) >> (d - 1);  // tallest node at depth d-1
     if (pmax <= leaf) break;                                // depth d-1 is all leaves

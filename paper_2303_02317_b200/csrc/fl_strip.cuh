@@ -273,7 +273,7 @@ __device__ int64_t put_strip_v2(const double* __restrict__ in_org, double* __res
 // payoffs of columns f-s-3, f-s-2.  Per-cell arithmetic is put_strip_warp's
 // interior order: fma(cd, left, fma(cu, right, cm * cur)), projected by max
 // (equal to the reference's lin > pay ? lin : pay), exercise iff !(lin > pay).
-// Requires 2h+2 <= 32*CPL.  pay_org must cover cols f-h-2 .. f+2h.
+// Requires 2h+2 <= 32*CPL.  pay_org must cover cols f-h-4 .. f+2h.
 template <int CPL, int PAYMODE = 0>
 __device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __restrict__ out_org,
                                    const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
@@ -296,16 +296,15 @@ __device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __
     u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
   }
   // lane 0's left fills: at row s cells -2, -1 are cols f-s-3, f-s-2 (exercise
-  // cells: their payoff).  Lane i keeps pay(f-3-i) for row i's broadcast.
-  const double fillv = (lane <= height) ? pay_org[f - 3 - lane] : 0.0;
-  double fill1 = pay_org[f - 2];
+  // cells: their payoff), loaded two rows ahead (one uniform load per row).
+  double fill1 = pay_org[f - 2], fill2 = pay_org[f - 3], fill3 = pay_org[f - 4];
   long long ta = 0;
   __syncwarp();
   if (tm) { ta = clock64() + (long long)(u[0] + fill1 == 12345.678 ? 1 : 0); }
   const double* pq = pay0 - 1;  // row s+1 payoff of cell j: pq[j - s]
   unsigned green = 0;
   for (int s = 0; s < height; ++s) {
-    const double fill2 = __shfl_sync(FULL, fillv, s);
+    const double fill4 = pay_org[f - s - 5];  // row s+2's cell -2 (never past col f-h-4)
     double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
     double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
     L2 = l0 ? fill2 : L2;
@@ -338,6 +337,8 @@ __device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __
       p[c] = np[c];
     }
     fill1 = fill2;
+    fill2 = fill3;
+    fill3 = fill4;
   }
   // exercise flags of the final row: the reference's cell is exercise iff
   // !(lin > pay), i.e. iff its projected value is exactly its payoff

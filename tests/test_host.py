@@ -113,6 +113,28 @@ def test_put_dispatch_modes():
     assert type(_native.status_error(st[3])).__name__ == "DomainError"
 
 
+def test_put_sliding_strip_flag():
+    """The host enables the sliding-frame leaf strip only when an exercise cell
+    whose three parents are exercise cells provably stays one: lin - payoff =
+    -omega dtau + e^x (1 - A) < -1e-12 for every x <= 0 (fl_put.cu put_leaf,
+    fl_strip.cuh put_strip_slide).  Restated here from the reference's grid
+    constants (bsm.py:150-229); the drawn rates straddle the cut."""
+    from paper_2303_02317_b200 import _native
+
+    rows = [(100.0, 100.0, R, V, 365.0, T) for R in (0.0, 1e-6, 1e-5, 1e-3, 0.05)
+            for V in (0.1, 0.3, 0.6) for T in (1024, 4096)]
+    S, K, R, V, E, T = (np.array([r[i] for r in rows]) for i in range(6))
+    st, mode, _, ip = _native.inspect(2, S, K, R, 0.0, V, E, T.astype(np.int64))
+    seen = set()
+    for i, r in enumerate(rows):
+        d = port.discretize_put(r[0], r[1], r[2], 0.0, r[3], r[4], int(r[5]), 0.4)
+        A = d["cd"] * math.exp(-d["d_s"]) + d["cm"] + d["cu"] * math.exp(d["d_s"])
+        want = int(d["omega"] * d["d_tau"] - max(0.0, 1.0 - A) > 1e-12)
+        assert st[i] == 0 and ip[i, 1] == want, (r, ip[i, 1], want)
+        seen.add(want)
+    assert seen == {0, 1}
+
+
 def test_status_error_mapping():
     import paper_2303_02317_b200 as fl
     from paper_2303_02317_b200 import _native

@@ -16,9 +16,12 @@ constexpr double CD = 0.39790368627109396, CM = 0.199951171875, CU = 0.402096313
 template <int MODE>
 __global__ void k(const double* in, double* out, const double* pay, long long* cyc, int reps, int height, long long f,
                   long long hi) {
-  const double* in_org = in - C0;
+  __shared__ double spay[NC], sin_[NC];
+  for (int i = threadIdx.x; i < NC; i += 32) { spay[i] = pay[i]; sin_[i] = in[i]; }
+  __syncwarp();
+  const double* in_org = (MODE >= 5 ? sin_ : in) - C0;
   double* out_org = out - C0;
-  const double* pay_org = pay - C0;
+  const double* pay_org = (MODE >= 5 ? spay : pay) - C0;
   long long t0 = clock64();
   int64_t acc = 0;
   for (int r = 0; r < reps; ++r) {
@@ -27,6 +30,12 @@ __global__ void k(const double* in, double* out, const double* pay, long long* c
     if (MODE == 2) acc += put_strip_slide<3, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
     if (MODE == 3) acc += put_strip_pipe<9>(in_org, out_org, pay_org, f - 2 * height - 1, hi, f, height, CD, CM, CU);
     if (MODE == 4) acc += put_strip_slide<5>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 5) acc += put_strip_pipe<5>(in_org, out_org, pay_org, f - 2 * height - 1, hi, f, height, CD, CM, CU);
+    if (MODE == 6) acc += put_strip_slide<3, 0>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 7) acc += put_strip_slide<3, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 8) acc += put_strip_slide<5, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 9) acc += put_strip_slide<9, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 10) acc += put_strip_warp<17>(in_org, out_org, pay_org, f - 2 * height - 1, hi, f, height, CD, CM, CU);
   }
   long long t1 = clock64();
   if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = acc / reps; }
@@ -53,12 +62,13 @@ int main() {
   cudaMalloc(&d_in, 8 * NC); cudaMalloc(&d_out, 8 * NC); cudaMalloc(&d_pay, 8 * NC); cudaMalloc(&c, 16);
   cudaMemcpy(d_in, a.data(), 8 * NC, cudaMemcpyHostToDevice);
   cudaMemcpy(d_pay, pay.data(), 8 * NC, cudaMemcpyHostToDevice);
-  for (int height : {64, 32, 31, 24, 17, 5, 1}) {
+  for (int height : {128, 100, 64, 32}) {
     std::vector<double> ref(NC);
     long long kref = 0;
-    for (int mode : {0, 3, 1, 2, 4}) {
+    for (int mode : {0, 3, 10, 1, 2, 4, 5, 6, 7, 8, 9}) {
       if ((mode == 0 && 4 * height + 2 > 160) || (mode == 1 && 2 * height + 2 > 96) ||
-          (mode == 2 && 2 * height + 2 > 96) || (mode == 4 && 2 * height + 2 > 160) || (mode == 3 && height < 33))
+          (mode == 2 && 2 * height + 2 > 96) || (mode == 4 && 2 * height + 2 > 160) ||
+          (mode == 5 && 4 * height + 2 > 160) || (mode == 6 && 2 * height + 2 > 96) || (mode == 7 && 2 * height + 2 > 96) || (mode == 8 && 2 * height + 2 > 160) || (mode == 9 && 2 * height + 2 > 288) || (mode == 10 && (4 * height + 2 > 544 || height < 65)) || (mode == 3 && height < 33))
         continue;
       const long long hi = f + 2 * height;
       cudaMemset(d_out, 0, 8 * NC);
@@ -68,13 +78,19 @@ int main() {
         if (mode == 2) k<2><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
         if (mode == 3) k<3><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
         if (mode == 4) k<4><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 5) k<5><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 6) k<6><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 7) k<7><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 8) k<8><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 9) k<9><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 10) k<10><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
       };
       run(1);
       std::vector<double> o(NC);
       long long h[2];
       cudaMemcpy(o.data(), d_out, 8 * NC, cudaMemcpyDeviceToHost);
       cudaMemcpy(h, c, 16, cudaMemcpyDeviceToHost);
-      if (mode == 0 || mode == 3) { ref = o; kref = h[1]; }
+      if (mode == 0 || mode == 3 || mode == 10) { ref = o; kref = h[1]; }
       int diff = 0;
       double maxrel = 0;
       for (int i = 0; i < NC; ++i) {
