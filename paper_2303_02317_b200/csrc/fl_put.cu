@@ -45,8 +45,11 @@ constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a le
 #ifndef FL_STRIP_SLIDE  // 1: sliding-frame leaf strips (put_strip_slide) for options with the exercise margin
 #define FL_STRIP_SLIDE 1
 #endif
-constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 31) / 32;  // cells per lane of the sliding frame
-constexpr int PUT_SLIDE_H = (32 * PUT_SLIDE_CPL - 2) / 2;     // tallest strip it holds
+#ifndef FL_STRIP_GHOST  // 1: the sliding frame with a ghost lane of exercise cells (no selects after shuffles)
+#define FL_STRIP_GHOST 1
+#endif
+constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 31 - FL_STRIP_GHOST) / (32 - FL_STRIP_GHOST);  // cells per lane
+constexpr int PUT_SLIDE_H = ((32 - FL_STRIP_GHOST) * PUT_SLIDE_CPL - 2) / 2;  // tallest strip the frame holds
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
 #endif
@@ -174,8 +177,13 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
   const int64_t kb =
       (P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height)
+#if FL_STRIP_GHOST
+          ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
+                                              FL_PROFP(X.prof) ? tm : nullptr)
+#else
           ? put_strip_slide<PUT_SLIDE_CPL, 1>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
                                               FL_PROFP(X.prof) ? tm : nullptr)
+#endif
           : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
                                     FL_PROFP(X.prof) ? tm : nullptr);
 #elif FL_STRIP_PIPE

@@ -363,6 +363,91 @@ __device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __
   return kb;
 }
 
+// put_strip_slide with a ghost lane: lane 0 holds the CPL exercise cells left
+// of the frame (cols f-s-1-CPL .. f-s-2 at row s) and lanes 1.. hold the
+// frame, so no lane needs a select after the shuffle.  Lane 0's values stay
+// exactly their payoffs: its own left inputs (shfl_up returns lane 0's own,
+// more-right cells, whose payoffs are smaller) only lower its lin, and an
+// exercise cell with a lower lin is still an exercise cell (cd, cm, cu >= 0).
+// Payoffs of the new row: PAYLDS = 0 shifts them one cell right in registers
+// and loads only the lane's first cell (one load per row); PAYLDS = 1 loads
+// every cell.  Requires 2h+2 <= 32*CPL - CPL; pay_org must cover cols
+// f-h-1-CPL .. f+2h.
+template <int CPL, int PAYLDS = 0>
+__device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 2, "two left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = (lane - 1) * CPL;  // lane 0: cells -CPL .. -1
+  // cells past the frame (idle lanes, the tail of the last lane) read the
+  // frame's last column; their values never reach a cell j < W
+  const double* pay0 = pay_org + (f - 1);
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] == 12345.678 ? 1 : 0); }
+  // row s+1 payoff of cell j: col f-s-2+j = pay0[j - 1 - s]
+  const double* pq0 = pay0 - 1 + jx[0];
+  double np0 = pq0[0];
+  unsigned green = 0;
+  for (int s = 0; s < height; ++s) {
+    const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    double np[CPL];
+    if (PAYLDS) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) np[c] = pay0[jx[c] - 1 - s];
+    } else {
+      np[0] = np0;
+#pragma unroll
+      for (int c = 1; c < CPL; ++c) np[c] = p[c - 1];
+      np0 = pq0[-(s + 1)];  // next row's first-cell payoff
+    }
+    double nu[CPL];
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) {
+      const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+      nu[c] = lin > np[c] ? lin : np[c];
+    }
+    const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+    const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
+    nu[1] = lin1 > np[1] ? lin1 : np[1];
+    nu[0] = lin0 > np[0] ? lin0 : np[0];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      u[c] = nu[c];
+      p[c] = np[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c >= 0 && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
 // Time-tiled variant of put_strip_warp: lanes exchange K halo cells per side
 // once per K rows (instead of one cell per side per row) and advance K rows on
 // an extended register tile, recomputing the halo cone redundantly.  One

@@ -19,9 +19,9 @@ __global__ void k(const double* in, double* out, const double* pay, long long* c
   __shared__ double spay[NC], sin_[NC];
   for (int i = threadIdx.x; i < NC; i += 32) { spay[i] = pay[i]; sin_[i] = in[i]; }
   __syncwarp();
-  const double* in_org = (MODE >= 5 ? sin_ : in) - C0;
+  const double* in_org = (MODE >= 5 && MODE != 10 ? sin_ : in) - C0;
   double* out_org = out - C0;
-  const double* pay_org = (MODE >= 5 ? spay : pay) - C0;
+  const double* pay_org = (MODE >= 5 && MODE != 10 ? spay : pay) - C0;
   long long t0 = clock64();
   int64_t acc = 0;
   for (int r = 0; r < reps; ++r) {
@@ -34,7 +34,9 @@ __global__ void k(const double* in, double* out, const double* pay, long long* c
     if (MODE == 6) acc += put_strip_slide<3, 0>(in_org, out_org, pay_org, f, height, CD, CM, CU);
     if (MODE == 7) acc += put_strip_slide<3, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
     if (MODE == 8) acc += put_strip_slide<5, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
-    if (MODE == 9) acc += put_strip_slide<9, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 9) acc += put_strip_ghost<5, 0>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 11) acc += put_strip_ghost<5, 1>(in_org, out_org, pay_org, f, height, CD, CM, CU);
+    if (MODE == 12) acc += put_strip_ghost<3, 0>(in_org, out_org, pay_org, f, height, CD, CM, CU);
     if (MODE == 10) acc += put_strip_warp<17>(in_org, out_org, pay_org, f - 2 * height - 1, hi, f, height, CD, CM, CU);
   }
   long long t1 = clock64();
@@ -62,13 +64,13 @@ int main() {
   cudaMalloc(&d_in, 8 * NC); cudaMalloc(&d_out, 8 * NC); cudaMalloc(&d_pay, 8 * NC); cudaMalloc(&c, 16);
   cudaMemcpy(d_in, a.data(), 8 * NC, cudaMemcpyHostToDevice);
   cudaMemcpy(d_pay, pay.data(), 8 * NC, cudaMemcpyHostToDevice);
-  for (int height : {128, 100, 64, 32}) {
+  for (int height : {64, 45, 32, 17, 1}) {
     std::vector<double> ref(NC);
     long long kref = 0;
-    for (int mode : {0, 3, 10, 1, 2, 4, 5, 6, 7, 8, 9}) {
+    for (int mode : {0, 3, 10, 5, 8, 9, 11, 12}) {
       if ((mode == 0 && 4 * height + 2 > 160) || (mode == 1 && 2 * height + 2 > 96) ||
           (mode == 2 && 2 * height + 2 > 96) || (mode == 4 && 2 * height + 2 > 160) ||
-          (mode == 5 && 4 * height + 2 > 160) || (mode == 6 && 2 * height + 2 > 96) || (mode == 7 && 2 * height + 2 > 96) || (mode == 8 && 2 * height + 2 > 160) || (mode == 9 && 2 * height + 2 > 288) || (mode == 10 && (4 * height + 2 > 544 || height < 65)) || (mode == 3 && height < 33))
+          (mode == 5 && 4 * height + 2 > 160) || (mode == 6 && 2 * height + 2 > 96) || (mode == 7 && 2 * height + 2 > 96) || (mode == 8 && 2 * height + 2 > 160) || (mode == 9 && 2 * height + 2 > 155) || (mode == 11 && 2 * height + 2 > 155) || (mode == 12 && 2 * height + 2 > 93) || (mode == 10 && (4 * height + 2 > 544 || height < 65)) || (mode == 3 && height < 33))
         continue;
       const long long hi = f + 2 * height;
       cudaMemset(d_out, 0, 8 * NC);
@@ -84,6 +86,8 @@ int main() {
         if (mode == 8) k<8><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
         if (mode == 9) k<9><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
         if (mode == 10) k<10><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 11) k<11><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
+        if (mode == 12) k<12><<<1, 32>>>(d_in, d_out, d_pay, c, reps, height, f, hi);
       };
       run(1);
       std::vector<double> o(NC);
