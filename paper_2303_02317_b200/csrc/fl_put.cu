@@ -459,7 +459,7 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
       t.x = cur_org; t.w = X.pay_org; t.y = nullptr;
       t.i0 = f; t.i1 = rem; t.i2 = ks;
       t.c0 = P.cd; t.c1 = P.cm; t.c2 = P.cu; t.h = 0; t.span = 2; t.L = 0; t.Lout = 0; t.d0 = 0.0;
-      const int ring = (2 * rem + 2 <= SMALL_SLOTS) ? RING_SMALL : RING_BIG;
+      const int ring = (2 * rem + 2 <= MED_WSLOTS) ? RING_SMALL : RING_BIG;  // two rows of the apex in one worker buffer
       const int id = issue(S, c, ring, t, U(cur_org + ks - rem - 1), U(cur_org + ks + rem + 1), 0, 0);
       FL_TR(S, c, EV_TW_B, 0);
       warp_wait_done(S, id);

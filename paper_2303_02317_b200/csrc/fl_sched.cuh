@@ -170,10 +170,14 @@ constexpr int DIRECT_H = FL_DIRECT_H;  // direct-correlation TASKS for kernels u
 #endif
 constexpr int KT_H = FL_KT_H;
 static_assert(KT_H >= DIRECT_H, "direct tasks read the table");
-constexpr int BIG_LOGN = 13;    // big-group FFT blocks <= 8192 real points
-constexpr int SMALL_LOGN = 12;  // medium-group FFT blocks <= 4096 real points
+#ifndef FL_MED_WARPS  // 1: the medium group is four independent single-warp workers on RING_SMALL
+#define FL_MED_WARPS 0  // measured: 14.6 -> 16.6 ms (1-warp blocks of 1024 points: longer tasks, more blocks)
+#endif
+constexpr int BIG_LOGN = 13;                     // big-group FFT blocks <= 8192 real points
+constexpr int SMALL_LOGN = FL_MED_WARPS ? 10 : 12;  // small-ring FFT blocks <= 1024 (4096) real points
 constexpr int BIG_SLOTS = smem_complex_slots(1 << (BIG_LOGN - 1));
-constexpr int SMALL_SLOTS = smem_complex_slots(1 << (SMALL_LOGN - 1));
+constexpr int MED_WSLOTS = smem_complex_slots(1 << (SMALL_LOGN - 1));  // one small-ring worker's buffer
+constexpr int SMALL_SLOTS = FL_MED_WARPS ? 4 * MED_WSLOTS : MED_WSLOTS;  // the medium group's buffers
 constexpr int NDEP = 6;
 
 enum : int {
@@ -1087,11 +1091,62 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
       t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
       t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
-      issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
+      for (int k = 0; k < (FL_MED_WARPS ? GROUP_WARPS : 1); ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
       issue(S, c, RING_BIG, t, 0, 0, 0, 0);
     }
     return;
   }
+#if FL_MED_WARPS
+  if (role == ROLE_MED) {
+    // ---- small-ring worker: one warp per task (claims by CAS; the big group may
+    // steal too).  Every small-ring task runs with this one-warp plan whichever
+    // worker takes it, so its arithmetic does not depend on the schedule.
+    const Grp gw{lane_id(), 32, -1};
+    double2* wbuf = medbuf + rank * MED_WSLOTS;
+    double flops = 0.0;
+    for (;;) {
+      const long long t0 = clock64();
+      int idx = 0;
+      unsigned ns = 16;
+      for (;;) {
+        int got = 0, ii = 0;
+        if (lane_id() == 0) {
+          ii = *(volatile int*)&S.claim[RING_SMALL];
+          if (ii < *(volatile int*)&S.reserve[RING_SMALL]) {
+            const Task& sl = S.ring[RING_SMALL][ii % QCAP];
+            if (sl.seq == ii) {
+              __threadfence_block();
+              bool ready = true;
+              for (int d = 0; d < sl.ndep; ++d) ready = ready && task_done(S, sl.dep[d]);
+              if (ready && atomicCAS(&S.claim[RING_SMALL], ii, ii + 1) == ii) got = 1;
+            }
+          }
+        }
+        if (__shfl_sync(FULL, got, 0)) { idx = __shfl_sync(FULL, ii, 0); break; }
+        __nanosleep(ns);
+        ns = ns < FL_IDLE_NS ? 2 * ns : ns;
+      }
+      worker_wait_ready(S, RING_SMALL, idx);
+      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
+      const long long t1 = clock64();
+      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
+      if (t.kind == TK_EXIT) break;
+      const double fl = pr.exec(S, t, wbuf, MED_WSLOTS, SMALL_LOGN, tq, gw);
+      flops += fl > 0 ? fl : 0.0;
+      __syncwarp();
+      if (lane_id() == 0) {
+        publish_done(S, RING_SMALL, idx);
+        if (FL_PROFP(prof)) {
+          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
+          prof_add(prof, ps, clock64() - t1);
+          prof_add(prof, ps + 1, 1);
+        }
+      }
+    }
+    if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
+    return;
+  }
+#endif
   // ---- FFT groups: one task at a time over 128 threads; each group is the
   // only consumer of its rings (the big group: RING_BIG, then RING_LOW; the
   // medium group: RING_SMALL), so claims need no atomics
@@ -1164,7 +1219,14 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     // a stolen small-ring task runs with the medium group's block plan (same
     // arithmetic whichever group executes it)
     const bool stolen = (gi == 0 && tring == RING_SMALL);
+#if FL_MED_WARPS
+    // a stolen small-ring task runs on the group's first warp with the workers' one-warp plan
+    double fl = 0.0;
+    if (!stolen) fl = pr.exec(S, t, buf, slots, logN, tq, g);
+    else if (rank == 0) fl = pr.exec(S, t, buf, MED_WSLOTS, SMALL_LOGN, tq, Grp{lane_id(), 32, -1});
+#else
     const double fl = pr.exec(S, t, buf, stolen ? SMALL_SLOTS : slots, stolen ? SMALL_LOGN : logN, tq, g);
+#endif
     flops += fl > 0 ? fl : 0.0;
     gsync(g);
     if (g.t == 0) {
