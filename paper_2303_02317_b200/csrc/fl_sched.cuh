@@ -53,7 +53,7 @@ namespace fl {
 #endif
 #define FL_PROFP(p) (FL_PROF ? (p) : nullptr)
 #ifndef FL_NHELP
-#define FL_NHELP 3
+#define FL_NHELP 2
 #endif
 constexpr int NCHAIN = 2;
 constexpr int NHELP = FL_NHELP;  // helper warps per chain
@@ -61,14 +61,37 @@ constexpr int GROUP_WARPS = 4;
 constexpr int GROUP_THREADS = 32 * GROUP_WARPS;
 constexpr int BIG_WARPS = GROUP_WARPS;
 constexpr int BIG_THREADS = GROUP_THREADS;
-constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP);
-constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
-enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3 };
-
 #ifndef FL_LAYOUT
-#define FL_LAYOUT 2
+#define FL_LAYOUT 4
 #endif
+// layout 4 keeps two warp slots idle so the chains' SMSP holds nothing else
+constexpr int IDLE_WARPS = (FL_LAYOUT == 4) ? 2 : 0;
+constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP) + IDLE_WARPS;
+constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
+enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3, ROLE_IDLE = 4 };
 __device__ __forceinline__ int warp_role(int w, int* rank) {
+#if FL_LAYOUT == 4
+  // The chains' leaf strips exchange neighbours by shuffle every row, and a
+  // shuffle waits behind every shared-memory access queued on its SMSP's MIO
+  // path (measured, tools/strip_noise_bench.cu: 68 cycles/row alone, 148 with
+  // three conflict-free shared-load warps on the same SMSP, 90 on the other
+  // SMSPs).  So both chains share SMSP 3 with nothing else (warps 3, 7; 11 and
+  // 15 idle), and the FFT groups and the helpers (two per chain) fill SMSPs 0-2.
+  static_assert(NCHAIN == 2 && NHELP == 2 && SCHED_WARPS == 16, "layout 4 shape");
+  if ((w & 3) == 3) {
+    if (w < 8) { *rank = w >> 2; return ROLE_CHAIN; }
+    *rank = 0;
+    return ROLE_IDLE;
+  }
+  constexpr int kRole[12] = {ROLE_BIG, ROLE_BIG, ROLE_BIG, ROLE_BIG, ROLE_MED, ROLE_MED,
+                             ROLE_MED, ROLE_MED, ROLE_HELPER, ROLE_HELPER, ROLE_HELPER, ROLE_HELPER};
+  // slot = index among the non-chain warps: 0,1,2 | 4,5,6 | 8,9,10 | 12,13,14
+  // big: warps 0,1,2,4; medium: 5,6,8,9; helpers: 10 (chain 0), 12 (chain 1), 13 (chain 0), 14 (chain 1)
+  const int slot = (w >> 2) * 3 + (w & 3);
+  constexpr int kRank[12] = {0, 1, 2, 3, 0, 1, 2, 3, 0, NHELP + 0, 1, NHELP + 1};
+  *rank = kRank[slot];
+  return kRole[slot];
+#endif
 #if FL_LAYOUT == 1
   // SMSP-aware: SMSP 0 / 1 hold one chain each plus the OTHER chain's helpers
   // (a chain and its own helpers never compete for one issue port), the FFT
@@ -993,6 +1016,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   __syncthreads();
   int rank = 0;
   const int role = warp_role(threadIdx.x >> 5, &rank);
+  if (role == ROLE_IDLE) return;
   if (role == ROLE_HELPER) {
     // ---- helper warp of chain rank / NHELP: correlations from the chain's
     // request rings, urgent ring first (claims by CAS: never commit to an

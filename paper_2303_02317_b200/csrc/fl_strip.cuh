@@ -363,6 +363,23 @@ __device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __
   return kb;
 }
 
+// Projection max(lin, pay) with the reference's tie rule (lin > pay ? lin : pay)
+// decided on the integer pipe: lin is a sum of products of nonnegative
+// coefficients and values, so lin >= +0 and its bit pattern orders like an
+// int64 against any payoff's (negative payoffs have the sign bit set, i.e.
+// compare below every lin).  Frees the FP64 pipe of the DSETP (the strip is
+// FP64-issue-bound when two strips share an SMSP).
+#ifndef FL_INT_PROJ
+#define FL_INT_PROJ 0  // measured slower: the 64-bit integer compare lengthens the row's critical path
+#endif
+__device__ __forceinline__ double proj_max(double lin, double pay) {
+#if FL_INT_PROJ
+  return __double_as_longlong(lin) > __double_as_longlong(pay) ? lin : pay;
+#else
+  return lin > pay ? lin : pay;
+#endif
+}
+
 // put_strip_slide with a ghost lane: lane 0 holds the CPL exercise cells left
 // of the frame (cols f-s-1-CPL .. f-s-2 at row s) and lanes 1.. hold the
 // frame, so no lane needs a select after the shuffle.  Lane 0's values stay
@@ -416,12 +433,12 @@ __device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __
 #pragma unroll
     for (int c = CPL - 1; c >= 2; --c) {
       const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
-      nu[c] = lin > np[c] ? lin : np[c];
+      nu[c] = proj_max(lin, np[c]);
     }
     const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
     const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
-    nu[1] = lin1 > np[1] ? lin1 : np[1];
-    nu[0] = lin0 > np[0] ? lin0 : np[0];
+    nu[1] = proj_max(lin1, np[1]);
+    nu[0] = proj_max(lin0, np[0]);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       u[c] = nu[c];
