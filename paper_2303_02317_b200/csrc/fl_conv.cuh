@@ -181,45 +181,83 @@ __device__ __forceinline__ void dit_stage(double2* buf, int logC, int logS, cons
   gsync(g);
 }
 
-// Forward: natural order in, X[k] at slot P(k) out.
-__device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* tq, Grp g) {
-  const int lr = last_radix_log(logC);
-  int logS = logC;
-  while (logS > lr) {
-    dif_stage<16>(buf, logC, logS, tq, g);
-    logS -= 4;
+// Stage plan of a C = 2^logC transform over a group of gn threads: per DIF
+// stage (largest span first) the radix log, the largest radix that still
+// gives every thread of the group a butterfly (C/R >= gn), else the largest
+// radix that fits.  Small blocks on a 4-warp group thus run radix-4/8 stages
+// with every thread busy instead of radix-16 stages on a quarter of them.
+#ifndef FL_FFT_PLAN  // 0: radix-16 stages + one remainder stage (round-1 schedule)
+#define FL_FFT_PLAN 0  // measured: every-thread-busy radix 4/8 stages are slower (N = 1024 task 9.9k -> 13.2k cycles)
+#endif
+struct FftPlan {
+  int n;
+  int lr[16];
+};
+__device__ __forceinline__ FftPlan fft_plan(int logC, int gn) {
+  FftPlan p;
+  p.n = 0;
+  int rem = logC;
+#if FL_FFT_PLAN
+  while (rem > 0) {
+    int l = 0;
+    for (int c = 4; c >= 1 && !l; --c)
+      if (c <= rem && (1 << (logC - c)) >= gn) l = c;
+    if (!l) l = rem < 4 ? rem : 4;
+    p.lr[p.n++] = l;
+    rem -= l;
   }
-  if (lr == 1) dif_stage<2>(buf, logC, logS, tq, g);
-  else if (lr == 2) dif_stage<4>(buf, logC, logS, tq, g);
-  else if (lr == 3) dif_stage<8>(buf, logC, logS, tq, g);
-  else dif_stage<16>(buf, logC, logS, tq, g);
+#else
+  const int last = last_radix_log(logC);
+  while (rem > last) {
+    p.lr[p.n++] = 4;
+    rem -= 4;
+  }
+  p.lr[p.n++] = last;
+#endif
+  return p;
+}
+
+template <bool DIF>
+__device__ __forceinline__ void fft_stage(double2* buf, int lr, int logC, int logS, const double2* tq, const Grp& g) {
+  switch (lr) {
+    case 1: DIF ? dif_stage<2>(buf, logC, logS, tq, g) : dit_stage<2>(buf, logC, logS, tq, g); break;
+    case 2: DIF ? dif_stage<4>(buf, logC, logS, tq, g) : dit_stage<4>(buf, logC, logS, tq, g); break;
+    case 3: DIF ? dif_stage<8>(buf, logC, logS, tq, g) : dit_stage<8>(buf, logC, logS, tq, g); break;
+    default: DIF ? dif_stage<16>(buf, logC, logS, tq, g) : dit_stage<16>(buf, logC, logS, tq, g); break;
+  }
+}
+
+// Forward: natural order in, X[k] at slot P(k) out.
+__device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
+  int logS = logC;
+  for (int s = 0; s < pl.n; ++s) {
+    fft_stage<true>(buf, pl.lr[s], logC, logS, tq, g);
+    logS -= pl.lr[s];
+  }
 }
 
 // Inverse (unnormalised, x C): slot P(k) in, natural order out.
-__device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g) {
-  const int lr = last_radix_log(logC);
-  if (lr == 1) dit_stage<2>(buf, logC, lr, tq, g);
-  else if (lr == 2) dit_stage<4>(buf, logC, lr, tq, g);
-  else if (lr == 3) dit_stage<8>(buf, logC, lr, tq, g);
-  else dit_stage<16>(buf, logC, lr, tq, g);
-  for (int logS = lr + 4; logS <= logC; logS += 4) dit_stage<16>(buf, logC, logS, tq, g);
+__device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
+  int logS = 0;
+  for (int s = pl.n - 1; s >= 0; --s) {
+    logS += pl.lr[s];
+    fft_stage<false>(buf, pl.lr[s], logC, logS, tq, g);
+  }
 }
 
-// Slot holding frequency k after fft_dif: digits of k (radix 16 from the
-// least significant end, the last remainder digit most significant in k)
-// written most-significant-first into the slot index.
-__device__ __forceinline__ int slot_of(int k, int logC) {
-  const int lr = last_radix_log(logC);
-  const int nfull = (logC - lr) / 4;  // radix-16 stages
+// Slot holding frequency k after fft_dif: the mixed-radix digits of k (first
+// stage's radix least significant) written most-significant-first into the
+// slot index.
+__device__ __forceinline__ int slot_of(int k, int logC, const FftPlan& pl) {
   int p = 0;
   int logS = logC;
 #pragma unroll 1
-  for (int s = 0; s < nfull; ++s) {
-    logS -= 4;
-    p |= (k & 15) << logS;
-    k >>= 4;
+  for (int s = 0; s < pl.n; ++s) {
+    logS -= pl.lr[s];
+    p |= (k & ((1 << pl.lr[s]) - 1)) << logS;
+    k >>= pl.lr[s];
   }
-  return p | k;  // remainder digit (< 2^lr) in the lowest lr bits
+  return p;
 }
 
 // ---------------------------------------------------------------------------
@@ -309,6 +347,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
   const int64_t rlo_modN = pl.rlo & (N - 1);
   const double rlo_sign = (pl.rlo & 1) ? -1.0 : 1.0;
   const int64_t nblk = (Lout + pl.P - 1) / pl.P;
+  const FftPlan fp = fft_plan(logC, g.n);
 
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
@@ -321,7 +360,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       buf[pidx(n)] = make_double2(a, b);
     }
     gsync(g);
-    fft_dif(buf, logC, tq, g);
+    fft_dif(buf, logC, tq, g, fp);
     // -- split to the real spectrum, multiply, re-pack for the inverse (/C)
     // W_N^k and the window phase W_N^(k rlo) advance by fixed steps per iteration
     // (one table lookup each instead of conflicted strided lookups per bin)
@@ -332,7 +371,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
 #pragma unroll 1
     for (int k = g.t; k <= C / 2; k += g.n) {
       const int kc = (C - k) & (C - 1);
-      const int pk = slot_of(k, logC), pc = slot_of(kc, logC);
+      const int pk = slot_of(k, logC, fp), pc = slot_of(kc, logC, fp);
 #if FL_SPEC_SKIP
       {  // both spectrum values below the 1e-24 cut: the bin pair is zero, skip its loads and math
         const double2 omk = cconj(Wk), omc = make_double2(-Wk.x, -Wk.y);
@@ -377,7 +416,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       ph = cmul(ph, phstep);
     }
     gsync(g);
-    fft_dit(buf, logC, tq, g);
+    fft_dit(buf, logC, tq, g, fp);
     // -- store valid outputs: y[2n] = Re, y[2n+1] = Im
     const int64_t lim = (Lout - k0 < pl.P) ? (Lout - k0) : pl.P;
 #pragma unroll 4
