@@ -731,6 +731,70 @@ __device__ __forceinline__ void conv_direct_blk(const double* __restrict__ x, do
   if (k + 1 < Lout) y[k + 1] = k2[1];
 }
 
+// conv_direct_blk without shared-memory bank conflicts.  The helpers' x loads
+// were the SM's largest source of conflict wavefronts (output groups 8 apart
+// put lanes og and og+2 on one bank), and every queued wavefront delays the
+// chain warps' shuffles.  Here the taps are shifted by 3 (three leading zero
+// weights, M' = M + 3), lane (og, tg) takes the taps [tg Q + og%4, + Q) of the
+// shifted kernel with Q = 4 (mod 16): within a half-warp the x addresses
+// 8 og + og%4 + tg Q (+ step) and the weight addresses og%4 + tg Q (+ step)
+// then fall on 16 distinct banks.  Rounding Q up adds zero taps (<= 15 per
+// quarter).  Same outputs as conv_direct_blk up to the summation order.
+__device__ __forceinline__ void conv_direct_blk_cf(const double* __restrict__ x, double* __restrict__ y, int Lout,
+                                                   const double* __restrict__ w, int M) {
+  const int lane = lane_id();
+  const int tg = lane & 3, og = lane >> 2;
+  const int Mp = M + 3;
+  int Q = (Mp + 3) >> 2;
+  Q += (20 - (Q & 15)) & 15;  // Q = 4 (mod 16)
+  const int s = tg * Q + (og & 3);
+  const int e = s + Q;
+  const int xlen = Lout + M - 1;
+  const int xb = 8 * og - 3;  // x index of output 8 og at shifted tap 0
+  double acc[8], xw[12];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    acc[b] = 0.0;
+    const int i = xb + s + b;
+    xw[b] = (i >= 0 && i < xlen) ? x[i] : 0.0;
+  }
+  for (int r = s; r < e; r += 4) {
+    double wv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = xb + r + 8 + j;
+      xw[8 + j] = (i >= 0 && i < xlen) ? x[i] : 0.0;
+      const int t = r + j - 3;  // unshifted tap
+      wv[j] = (t >= 0 && t < M) ? w[t] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[b] = fma(wv[j], xw[b + j], acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) xw[b] = xw[b + 4];
+  }
+  const bool b0 = tg & 1, b1 = (tg >> 1) & 1;
+  double k4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b0 ? acc[i] : acc[i + 4];
+    const double keep = b0 ? acc[i + 4] : acc[i];
+    k4[i] = keep + __shfl_xor_sync(FULL, send, 1);
+  }
+  double k2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b1 ? k4[i] : k4[i + 2];
+    const double keep = b1 ? k4[i + 2] : k4[i];
+    k2[i] = keep + __shfl_xor_sync(FULL, send, 2);
+  }
+  const int k = 8 * og + 4 * b0 + 2 * b1;
+  if (k < Lout) y[k] = k2[0];
+  if (k + 1 < Lout) y[k + 1] = k2[1];
+}
+
 // conv_direct_blk with the weights held in registers: w normally lives in HBM
 // (the per-option kernel table), where one L2 round trip per 4 taps dominated.
 // Lane (og, tg) loads the 9 weights w[s + 9 og + i] of its tap quarter up front
@@ -810,6 +874,12 @@ __device__ double warp_conv_direct(const double* __restrict__ x, double* __restr
 #if FL_CONV_PAIRS == 2
   for (int64_t k0 = 0; k0 < Lout; k0 += 64)
     conv_direct_blk(x + k0, y + k0, (Lout - k0 < 64) ? (int)(Lout - k0) : 64, w, M);
+  __syncwarp();
+  return 2.0 * (double)Lout * (double)M;
+#endif
+#if FL_CONV_PAIRS == 4
+  for (int64_t k0 = 0; k0 < Lout; k0 += 64)
+    conv_direct_blk_cf(x + k0, y + k0, (Lout - k0 < 64) ? (int)(Lout - k0) : 64, w, M);
   __syncwarp();
   return 2.0 * (double)Lout * (double)M;
 #endif
