@@ -260,11 +260,13 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
                                 double* out_org, int h0, int ph0, int32_t* err) {
   const int64_t lo0 = j0 - h0 + 1;
   const long long t0 = clock64();
+  // the composed weights depend on nothing in flight: stage them while the
+  // jump writing this subtree's input row may still be running
+  if (h0 > CALL_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, CALL_LEAF, 1);
   wait_conflicts(*X.S, X.c, U(in_org + lo0), U(in_org + j0 + 1), 0, 0, U(out_org + lo0), U(out_org + j0 + 1));
   const long long t1 = clock64();
   double* s_in = X.scratch + CSUB_IN;
   warp_stage(s_in, in_org + lo0, h0);
-  if (h0 > CALL_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, CALL_LEAF, 1);
   long long twait = 0;
   static_assert(sizeof(CallSubFrame) * 5 <= FRAME_SOLVE_OFF - FRAME_SUB_OFF, "subtree frames");
   CallSubFrame* stk = chain_frames<CallSubFrame>(X.scratch, FRAME_SUB_OFF);

@@ -145,6 +145,7 @@ struct PutChainCtx {
   uint64_t flops;      // executed chain-side flops (lane-uniform)
   uint64_t ref_flops;  // reference-algorithmic flops (lane-uniform)
   unsigned long long* prof;
+  bool pay_ready = false;  // the option's payoff table is written (see put_subtree)
 };
 
 // Reference cost of a recursion node of height h whose parent has height ph:
@@ -231,17 +232,29 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
                                double* out_org, int h0, int ph0, int32_t* err) {
   const long long t0 = clock64();
   FL_TR(*X.S, X.c, EV_SUB_B, h0);
-  wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
-                 U(out_org + f0 + h0 + 1));
-  const long long t1 = clock64();
-  FL_TR(*X.S, X.c, EV_STG_B, 0);
   double* s_pay = X.scratch + SUB_PAY;
   double* s_in = X.scratch + SUB_IN;
   const int64_t plo = f0 - 2 * (int64_t)h0 - 1;
-  warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
-  warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+  // once the option's payoff table is known written (the first subtree's input
+  // wait covers the init task that writes it), the payoff columns and the
+  // composed weights depend on nothing in flight: stage them first, so their
+  // load latency overlaps the wait for the jump writing this subtree's input
+  const bool early = X.pay_ready;
+  if (early) {
+    warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+    if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
+  }
   const double* pay_s = s_pay - plo;
-  if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
+  wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
+                 U(out_org + f0 + h0 + 1));
+  if (!early) {
+    warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+    if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
+    X.pay_ready = true;
+  }
+  const long long t1 = clock64();
+  FL_TR(*X.S, X.c, EV_STG_B, 0);
+  warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
   const long long t2 = clock64();
   FL_TR(*X.S, X.c, EV_STG_E, 0);
   long long twait = 0, tpost = 0;
