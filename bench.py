@@ -330,7 +330,8 @@ def main():
                    "options_per_gpu": n_local, "lambda": 0.4, "put_cutoff": 128, "call_cutoff": 256,
                    "l2": "flushed between timed steps (256 MiB write outside the events); the chain "
                          "arenas (~3 MB per option) exceed L2 as well",
-                   "parallelism": f"option-sharded x{world}, no collective on the data path"},
+                   "parallelism": f"option-sharded x{world}, no collective on the data path",
+                   "device_bytes_per_gpu": db.device_bytes()},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None,
                      "traffic": ncu_traffic(args.workload),

@@ -88,6 +88,11 @@ int fl_batch_prepare(fl_batch** out, int64_t n, const int8_t* kind, const double
 int fl_batch_run(fl_batch* b, void* stream);
 int fl_batch_fetch(fl_batch* b, double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols,
                    int32_t* bnd_count, void* stream);
+/* Device memory the batch holds (bytes): parameter records, outputs and the
+ * per-chain workspaces (the arenas of the recursion rows, payoff tables and
+ * kernel tables); -1 on a null batch.  The workspace-size query of SURVEY
+ * 8(b): size a batch against the 180 GB of one B200 before pricing. */
+int64_t fl_batch_device_bytes(const fl_batch* b);
 /* Number of kernel launches one fl_batch_run enqueues. */
 int fl_batch_launches(const fl_batch* b);
 /* After a run: fp64 flops the fast kernels executed in it (FFT convention

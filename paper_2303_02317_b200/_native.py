@@ -38,7 +38,7 @@ _lib = None
 
 #: Every symbol include/fftlattice_b200.h declares.
 EXPORTED_SYMBOLS = (
-    "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run",
+    "fl_version", "fl_last_error", "fl_price_batch", "fl_batch_prepare", "fl_batch_run", "fl_batch_device_bytes",
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_timeline", "fl_batch_free",
     "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
     "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
@@ -81,6 +81,8 @@ def lib():
         L.fl_batch_fetch.restype = c_int
         L.fl_batch_launches.argtypes = [P]
         L.fl_batch_launches.restype = c_int
+        L.fl_batch_device_bytes.argtypes = [P]
+        L.fl_batch_device_bytes.restype = ctypes.c_int64
         L.fl_batch_free.argtypes = [P]
         L.fl_batch_free.restype = None
         L.fl_apply_linear_steps.argtypes = [P, i64, c_int, d, d, d, i64, P, P]
@@ -258,6 +260,13 @@ class DeviceBatch:
 
     def launches(self) -> int:
         return int(lib().fl_batch_launches(self._h))
+
+    def device_bytes(self) -> int:
+        """Device memory this batch holds (fl_batch_device_bytes)."""
+        v = int(lib().fl_batch_device_bytes(self._h))
+        if v < 0:
+            raise NativeLibraryError(lib().fl_last_error().decode())
+        return v
 
     def stats(self, stream=None) -> dict:
         """Executed fp64 flops of the last run and the H2D / D2H bytes moved."""

@@ -858,6 +858,19 @@ int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double
   return 0;
 }
 
+int64_t fl_batch_device_bytes(const fl_batch* b) {
+  if (!b) {
+    fail("fl_batch_device_bytes: null batch");
+    return -1;
+  }
+  int64_t t = 0;
+  for (const DevBuf* d : {&b->d_stats, &b->d_snap, &b->d_snaplen, &b->d_put, &b->d_call, &b->d_euro, &b->d_orders,
+                          &b->d_price, &b->d_status, &b->d_bt, &b->d_bc, &b->d_bcount, &b->d_counter, &b->d_ws_put,
+                          &b->d_ws_call, &b->d_ws_base})
+    t += (int64_t)d->bytes;
+  return t;
+}
+
 int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
   if (!b) return fail("fl_batch_profile: null batch");
   if (!FL_PROF) return fail("fl_batch_profile: library built without profile counters (build with FL_NVCC_FLAGS=-DFL_PROF=1)");

@@ -239,3 +239,19 @@ def test_european_approximations(api):
                     fn(spec)
             else:
                 assert price_close(fn(spec), ref, K), (fn.__name__, row)
+
+
+def test_batch_device_bytes():
+    """fl_batch_device_bytes: the device footprint of a prepared batch (the
+    per-chain arenas dominate) is positive and grows with T."""
+    from paper_2303_02317_b200 import _native
+
+    fp = []
+    for T in (1024, 8192):
+        db = _native.DeviceBatch(np.full(4, 2, dtype=np.int8), np.full(4, 100.0), np.full(4, 100.0),
+                                 np.full(4, 0.05), np.zeros(4), np.full(4, 0.3), np.full(4, 365.0),
+                                 np.full(4, T, dtype=np.int64))
+        db.run()
+        db.fetch()
+        fp.append(db.device_bytes())
+    assert 0 < fp[0] < fp[1], fp
