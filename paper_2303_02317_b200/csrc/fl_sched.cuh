@@ -65,11 +65,27 @@ constexpr int BIG_THREADS = GROUP_THREADS;
 #define FL_LAYOUT 4
 #endif
 // layout 4 keeps two warp slots idle so the chains' SMSP holds nothing else
-constexpr int IDLE_WARPS = (FL_LAYOUT == 4) ? 2 : 0;
+constexpr int IDLE_WARPS = (FL_LAYOUT == 4 || FL_LAYOUT == 5) ? 2 : 0;
 constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP) + IDLE_WARPS;
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
 enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3, ROLE_IDLE = 4 };
 __device__ __forceinline__ int warp_role(int w, int* rank) {
+#if FL_LAYOUT == 5
+  // each chain on its own SMSP (2 / 3) with two medium-group warps; the big
+  // group and the helpers (two per chain) on SMSPs 0 / 1; warps 14, 15 idle
+  static_assert(NCHAIN == 2 && NHELP == 2 && SCHED_WARPS == 16, "layout 5 shape");
+  const int smsp = w & 3, slot = w >> 2;
+  if (smsp >= 2) {
+    if (slot == 0) { *rank = smsp - 2; return ROLE_CHAIN; }
+    if (slot == 3) { *rank = 0; return ROLE_IDLE; }
+    *rank = (slot - 1) * 2 + (smsp - 2);
+    return ROLE_MED;
+  }
+  if (slot < 2) { *rank = slot * 2 + smsp; return ROLE_BIG; }
+  // helpers: SMSP 0 serves chain 0, SMSP 1 chain 1
+  *rank = smsp * NHELP + (slot - 2);
+  return ROLE_HELPER;
+#endif
 #if FL_LAYOUT == 4
   // The chains' leaf strips exchange neighbours by shuffle every row, and a
   // shuffle waits behind every shared-memory access queued on its SMSP's MIO
