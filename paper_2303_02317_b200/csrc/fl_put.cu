@@ -167,7 +167,11 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
 }
 
 // Leaf strip on the chain warp.  in_org / out_org / pay_org may address shared memory.
-template <bool ACCT = true>
+// SL: 1 the sliding frame (the caller guarantees P.slide, height <= PUT_SLIDE_H
+// and hi == f + 2 height), 0 the full frame, -1 decided here.  The subtree
+// walk is instantiated per strip kind so the hot walk carries one strip only
+// (instruction-cache footprint).
+template <bool ACCT = true, int SL = -1>
 __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
                                             double* out_org, const double* pay_org, int64_t lo, int64_t hi,
                                             int64_t f, int height) {
@@ -177,7 +181,7 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
 #if FL_STRIP_SLIDE
   // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
   const int64_t kb =
-      (P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height)
+      (SL == 1 || (SL < 0 && P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height))
 #if FL_STRIP_GHOST
           ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
                                               FL_PROFP(X.prof) ? tm : nullptr)
@@ -227,7 +231,7 @@ struct SubFrame {
 // (instantiated with and without the flop accounting: the counting code in the
 // walk costs ~5 % even when switched off at run time, so production runs use
 // the ACCT = false instance and accounting runs the other)
-template <bool ACCT>
+template <bool ACCT, int SL>
 __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
                                double* out_org, int h0, int ph0, int32_t* err) {
   const long long t0 = clock64();
@@ -272,7 +276,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       ref_node_enter(X, h, ph);
       FL_TR(*X.S, X.c, EV_MARK, 4);
       if (h <= PUT_LEAF) {
-        const int64_t kb = put_leaf(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
+        const int64_t kb = put_leaf<ACCT, SL>(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
         --sp;
@@ -355,7 +359,9 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     FL_TR(*X.S, X.c, EV_NODE, h * 4 + F.state);
     if (F.state == 0) {
       if (h <= PUT_HS) {
-        ret = put_subtree<ACCT>(X, P, F.f, F.in_org, F.out_org, h, ph, err);
+        ret = (FL_STRIP_SLIDE && P.slide && PUT_LEAF <= PUT_SLIDE_H)
+                  ? put_subtree<ACCT, 1>(X, P, F.f, F.in_org, F.out_org, h, ph, err)
+                  : put_subtree<ACCT, 0>(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
         --sp;
         continue;

@@ -17,6 +17,12 @@
 namespace fl {
 
 constexpr int64_t NONE_SEEN = -(((int64_t)1) << 60);  // _accel.py:46
+#ifndef FL_GHOST_UNROLL  // rows per unrolled step of the ghost-lane strip loop
+#define FL_GHOST_UNROLL 2
+#endif
+#ifndef FL_PIPE_NOINLINE  // 1: the full-frame fallback strip is a real call (measured slower: spills)
+#define FL_PIPE_NOINLINE 0
+#endif
 #ifndef FL_STRIP_ORDER
 #define FL_STRIP_ORDER 1
 #endif
@@ -99,6 +105,9 @@ __device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __r
 // the shuffle latency instead of preceding it.  Same per-cell arithmetic as
 // put_strip_warp (bit-identical rows, boundary and outputs).
 template <int CPL>
+#if FL_PIPE_NOINLINE
+__noinline__
+#endif
 __device__ int64_t put_strip_pipe(const double* __restrict__ in_org, double* __restrict__ out_org,
                                   const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
                                   int height, double cd, double cm, double cu, long long* tm = nullptr) {
@@ -416,6 +425,11 @@ __device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __
   const double* pq0 = pay0 - 1 + jx[0];
   double np0 = pq0[0];
   unsigned green = 0;
+  // unrolled by 2 only: in the kernel the strip shares the SM's instruction
+  // cache with every other role, and a longer body measured slower there
+  // (4 -> 14.2, 5 -> 14.8, 10 -> 15.8 ms; 2 -> 14.0 ms) although faster alone
+  constexpr int kUnroll = FL_GHOST_UNROLL;
+#pragma unroll kUnroll
   for (int s = 0; s < height; ++s) {
     const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
     const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
