@@ -231,6 +231,9 @@ struct SubFrame {
 // (instantiated with and without the flop accounting: the counting code in the
 // walk costs ~5 % even when switched off at run time, so production runs use
 // the ACCT = false instance and accounting runs the other)
+#ifndef FL_WALK_MERGE
+#define FL_WALK_MERGE 1
+#endif
 template <bool ACCT, int SL>
 __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
                                double* out_org, int h0, int ph0, int32_t* err) {
@@ -267,6 +270,64 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   stk[0].f = f0; stk[0].h = h0; stk[0].in = s_in - (f0 + 1); stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
+#if FL_WALK_MERGE
+  // one helper post site and one wait site (the walk runs for every 256 rows:
+  // its code footprint counts, see profiles/r01_experiments.md)
+  while (sp > 0) {
+    SubFrame& F = stk[sp - 1];
+    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
+    if (F.state == 0) {
+      ref_node_enter(X, h, (sp >= 2) ? stk[sp - 2].h : ph0);
+      if (h <= PUT_LEAF) {
+        const int64_t kb = put_leaf<ACCT, SL>(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
+        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
+        ret = kb;
+        --sp;
+        continue;
+      }
+      F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : sp == 2 ? SUB_ASM1 : SUB_ASM2) - (F.f - h1 + 1);
+      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
+    } else {
+      // a child finished: its boundary must stay within its height (state 1:
+      // first child from f, state 2: second child from km); then the jump
+      // posted before it (mid / bottom) must be complete
+      const bool first = (F.state == 1);
+      const int64_t fr = first ? F.f : F.km;
+      const int hr = first ? h1 : h2;
+      if (ret < fr - hr || ret > fr) { *err = FL_E_GEOMETRY | (first ? 2 : 3); return 0; }
+      const long long tw = clock64();
+      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
+      twait += clock64() - tw;
+      if (!first) {
+        --sp;
+        continue;
+      }
+      F.km = ret;
+    }
+    // state 0: mid jump, cols f+h1+1 .. f+2h-h1 of row t+h1 from the 2h inputs
+    // (overlaps the first child); state 1: bottom jump, cols km+h2+1 .. f+h of
+    // row t+h from the assembled cols km+1 .. f+2h-h1 (overlaps the second child)
+    const bool mid = (F.state == 0);
+    const int64_t km = F.km;
+    const int64_t A = F.f + 2 * (int64_t)h - h1 - km;
+    if (!mid) ref_node_bottom<ACCT>(X, h, A);
+    const int m = mid ? h1 : h2;
+    const int Lj = mid ? 2 * (h - h1) : (int)(A - 2 * h2), Mj = 2 * m + 1;
+    const double* xj = mid ? F.in + F.f + 1 : F.asmo + km + 1;
+    double* yj = mid ? F.asmo + F.f + h1 + 1 : F.out + km + h2 + 1;
+    const long long tp = clock64();
+    F.tk = helper_post(*X.S, X.c, F.q, xj, yj, Lj, wslot(*X.S, X.c, X.wst, sp, m), Mj, &F.tk0);
+    tpost += clock64() - tp;
+    if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lj * Mj);
+    F.state = mid ? 1 : 2;
+    SubFrame& C = stk[sp++];
+    C.f = mid ? F.f : km;
+    C.h = m;
+    C.in = mid ? F.in : F.asmo;
+    C.out = mid ? F.asmo : F.out;
+    C.state = 0;
+  }
+#else
   while (sp > 0) {
     SubFrame& F = stk[sp - 1];
     const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
@@ -324,6 +385,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       --sp;
     }
   }
+#endif
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_STAGE, t2 - t1);

@@ -48,6 +48,14 @@ namespace fl {
 #else
 #define FL_COLD
 #endif
+#ifndef FL_COLD_INIT  // 1: once-per-option setup / teardown helpers are real calls (out of the hot code)
+#define FL_COLD_INIT 0
+#endif
+#if FL_COLD_INIT || FL_DEDUP
+#define FL_COLD1 __noinline__
+#else
+#define FL_COLD1
+#endif
 #ifndef FL_PROF  // 1: scheduler profile counters (FL_PROFILE=1 at run time); tool builds only --
 #define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
 #endif
@@ -550,7 +558,7 @@ __device__ FL_COLD int issue(SchedShared& S, int c, int ring, const Task& t, uin
 }
 
 // Chain c waits for all of its issued tasks.
-__device__ FL_COLD void wait_all_own(SchedShared& S, int c) {
+__device__ FL_COLD1 void wait_all_own(SchedShared& S, int c) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
   for (int i = first; i < np; ++i) warp_wait_done(S, S.pend[c][i % PEND_CAP].id);
@@ -581,7 +589,7 @@ __device__ __forceinline__ int wst_sz(int d) { return d == 1 ? WST_SZ1 : d == 2 
 constexpr int64_t KTABLE_DOUBLES = (int64_t)(KT_H + 2) * (KT_H + 2) * 2;
 
 // scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
-__device__ FL_COLD void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
+__device__ FL_COLD1 void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
   const int lane = lane_id();
   const int span = st.span;
   double* a = scratch;
