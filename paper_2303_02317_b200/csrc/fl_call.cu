@@ -279,6 +279,62 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in = s_in - lo0; stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
+#if FL_WALK_MERGE
+  // one helper post site and one wait site (as put_subtree)
+  while (sp > 0) {
+    CallSubFrame& F = stk[sp - 1];
+    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
+    const int64_t lo = F.j - h + 1;
+    if (F.state == 0) {
+      call_ref_enter(X, h, (sp >= 2) ? stk[sp - 2].h : ph0);
+      if (h <= CALL_LEAF) {
+        ret = call_leaf(X, P, F.in, F.out, F.i, F.j, h);
+        --sp;
+        continue;
+      }
+      F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : sp == 2 ? CSUB_ASM1 : CSUB_ASM2) - lo;
+      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
+    } else {
+      // a child finished (state 1: first child from j, state 2: second from jm);
+      // then the jump posted before it (mid / bottom, if any) must be complete
+      const bool first = (F.state == 1);
+      const int64_t jr = first ? F.j : F.jm;
+      const int hr = first ? h1 : h2;
+      if (ret < jr - hr || ret > jr) { *err = FL_E_GEOMETRY | (first ? 1 : 2); return 0; }
+      if (first || F.tk >= 0) {
+        const long long tw = clock64();
+        helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
+        twait += clock64() - tw;
+      }
+      if (!first) {
+        --sp;
+        continue;
+      }
+      F.jm = ret;
+    }
+    // state 0: mid (helper), cols lo .. j-h1 of row i-h1; state 1: bottom, cols
+    // lo .. jm-h2 of row i-h from the assembled cols lo .. jm (if any)
+    const bool mid = (F.state == 0);
+    const int64_t A = F.jm - lo + 1;
+    if (!mid) call_ref_bottom(X, h, A);
+    const int m = mid ? h1 : h2;
+    const int Lj = mid ? h2 : (int)(A - h2);
+    F.tk = -1;
+    if (mid || A > h2) {
+      F.tk = helper_post(*X.S, X.c, F.q, (mid ? F.in : F.asmo) + lo, (mid ? F.asmo : F.out) + lo, Lj,
+                         wslot(*X.S, X.c, X.wst, sp, m), m + 1, &F.tk0);
+      if (X.acct) X.flops += 2ull * (uint64_t)((int64_t)Lj * (m + 1));
+    }
+    F.state = mid ? 1 : 2;
+    CallSubFrame& C = stk[sp++];
+    C.i = mid ? F.i : F.i - h1;
+    C.j = mid ? F.j : F.jm;
+    C.h = m;
+    C.in = mid ? F.in : F.asmo;
+    C.out = mid ? F.asmo : F.out;
+    C.state = 0;
+  }
+#else
   while (sp > 0) {
     CallSubFrame& F = stk[sp - 1];
     const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
@@ -328,6 +384,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
       --sp;
     }
   }
+#endif
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_MID, twait);

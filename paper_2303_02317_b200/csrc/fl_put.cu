@@ -231,9 +231,6 @@ struct SubFrame {
 // (instantiated with and without the flop accounting: the counting code in the
 // walk costs ~5 % even when switched off at run time, so production runs use
 // the ACCT = false instance and accounting runs the other)
-#ifndef FL_WALK_MERGE
-#define FL_WALK_MERGE 1
-#endif
 template <bool ACCT, int SL>
 __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, const double* in_org,
                                double* out_org, int h0, int ph0, int32_t* err) {

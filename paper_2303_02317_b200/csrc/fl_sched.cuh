@@ -56,6 +56,9 @@ namespace fl {
 #else
 #define FL_COLD1
 #endif
+#ifndef FL_WALK_MERGE  // 1: subtree walks with one helper-post and one helper-wait site (smaller hot loop)
+#define FL_WALK_MERGE 1
+#endif
 #ifndef FL_PROF  // 1: scheduler profile counters (FL_PROFILE=1 at run time); tool builds only --
 #define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
 #endif
