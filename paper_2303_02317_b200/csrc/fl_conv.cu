@@ -17,6 +17,9 @@ void init_twiddles(cudaStream_t stream) {
     h[m] = make_double2((double)cosl(a), (double)(-sinl(a)));
   }
   cudaMemcpyToSymbolAsync(fl_tw, h.data(), sizeof(double2) * TW_N, 0, cudaMemcpyHostToDevice, stream);
+  std::vector<double2> q(TWQ);
+  for (int i = 0; i < TWQ; ++i) q[twq_swz(i)] = h[i];
+  cudaMemcpyToSymbolAsync(fl_twq, q.data(), sizeof(double2) * TWQ, 0, cudaMemcpyHostToDevice, stream);
   cudaStreamSynchronize(stream);
 }
 
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(CTA_THREADS)
 linear_steps_kernel(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
                     Stencil st) {
   extern __shared__ double2 sbuf[];
-  conv_fft(x, L, y, Lout, h, st, sbuf, LS_LOGN_MAX, fl_tw, Grp{(int)threadIdx.x, CTA_THREADS, 0});
+  conv_fft(x, L, y, Lout, h, st, sbuf, LS_LOGN_MAX, fl_twq, Grp{(int)threadIdx.x, CTA_THREADS, 0});
 }
 
 int linear_steps_smem_bytes() { return smem_complex_slots(1 << (LS_LOGN_MAX - 1)) * (int)sizeof(double2); }

@@ -1107,7 +1107,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double2* bigbuf = tq + TWQ;              // big-group FFT buffer
   double2* medbuf = bigbuf + BIG_SLOTS;   // medium-group FFT buffer
   __shared__ int s_idx[2], s_ring[2];
-  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[twq_swz(i)] = fl_tw[i];
   sched_init(S);
   if (threadIdx.x == 0) S.prof = prof;
   __syncthreads();

@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(128, 1) kb(const double* x, double* y, int64_t
                                              int logN, long long* cyc, int reps) {
   extern __shared__ double2 sd[];
   double2* tq = sd;
-  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[twq_swz(i)] = fl_tw[i];
   __syncthreads();
   const int grp = threadIdx.x / nthr;
   double2* buf = sd + TWQ + grp * smem_complex_slots(1 << (logN - 1));
