@@ -208,6 +208,9 @@ constexpr int NRINGS = 3;
 #ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
 #define FL_IDLE_NS 2048
 #endif
+#ifndef FL_HELPER_GAP  // ns a helper pauses after each background (subtree-root) chunk (0: none)
+#define FL_HELPER_GAP 0
+#endif
 #ifndef FL_HELPER_NS  // longest back-off sleep of an idle helper poll
 #define FL_HELPER_NS 512
 #endif
@@ -1155,6 +1158,9 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
         prof_add(prof, PROF_HELP_CYC + q, clock64() - th);
         prof_add(prof, PROF_HELP_FMA, (unsigned long long)Lout * M);
       }
+#if FL_HELPER_GAP
+      if (q == 1) __nanosleep(FL_HELPER_GAP);  // background chunks: spread the shared-memory bursts
+#endif
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     return;
