@@ -15,8 +15,11 @@
  *  - Boundary records are optional (pass NULL); at most bnd_cap records per
  *    option are stored row-major at [i * bnd_cap], bnd_count[i] holds the true
  *    count.  Columns use the reference sentinel NO_GREEN = INT64_MIN.
- *  - All entry points synchronize the given stream before returning, except
- *    fl_batch_run, which only enqueues.
+ *  - The host-buffer entry points synchronize the given stream before
+ *    returning, except fl_batch_run, which only enqueues.  The device-pointer
+ *    entry points (fl_price_batch_dev, fl_price_put_bsm,
+ *    fl_price_american_call, fl_price_european) never synchronize: they only
+ *    enqueue on the caller's stream (fl_sync waits for it).
  *  - Reentrant across devices; one library context per device.
  */
 #ifndef FFTLATTICE_B200_H
@@ -61,6 +64,65 @@ int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double*
                    const double* Y, const double* V, const double* E, const int64_t* T, double lam,
                    int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
                    int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
+
+/* Release the calling thread's cached batch buffers (fl_price_batch keeps one
+ * grow-only batch per (thread, device); they are also freed at thread exit). */
+void fl_release_cache(void);
+
+/* Cost-balanced shard plan: longest-processing-time greedy over
+ * the per-option cost model (put 24.8 T log2^2 T, American call 10 T log2^2 T,
+ * European 8 T); owner[i] in [0, nshard).  Host-only. */
+int fl_shard_plan(int64_t n, const int8_t* kind, const int64_t* T, int nshard, int32_t* owner);
+
+/* fl_price_batch across several GPUs of this process in one call: options are
+ * LPT-sharded over devices[0..ndev), each shard priced by its own host thread
+ * on its own stream and device, results scattered back into the host outputs.
+ * Per-option results are bit-identical to fl_price_batch on one device.
+ * Replaces the reference's sequential portfolio loop (cli.py:820-841). */
+int fl_price_batch_multi(int ndev, const int* devices, int64_t n, const int8_t* kind, const double* S,
+                         const double* K, const double* R, const double* Y, const double* V, const double* E,
+                         const int64_t* T, double lam, int64_t call_cutoff, int64_t put_cutoff, int method,
+                         double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count,
+                         int32_t bnd_cap);
+
+/* Device-pointer entry: every array argument is a DEVICE
+ * pointer owned by the caller (e.g. torch data_ptr()), the work is enqueued on
+ * `stream` and the call returns without synchronizing.  Same semantics,
+ * statuses and boundary records as fl_price_batch; kind == NULL prices every
+ * option as kind_all.  The plan (validation, lattice constants, dispatch,
+ * costliest-first work lists) runs on the device from the same derivation code
+ * with the CUDA libm, so constants may differ from the host path's in the
+ * last bit (prices agree within the parity tolerance).  Workspaces are sized
+ * for T <= max_steps; an option with T > max_steps (other than a European,
+ * which needs none) gets status FL_E_CAPACITY | 7.  Replaces, per kind, the
+ * call sites binomial.py:161, american.py:428 and bsm.py:585. */
+int fl_price_batch_dev(int64_t n, const int8_t* kind, int kind_all, const double* S, const double* K, const double* R,
+                       const double* Y, const double* V, const double* E, const int64_t* T, double lam,
+                       int64_t call_cutoff, int64_t put_cutoff, int method, int64_t max_steps, double* price,
+                       int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap,
+                       void* stream);
+/* bsm.py:585 fast_put_bsm over a device batch (fl_price_batch_dev, kind PUT). */
+int fl_price_put_bsm(int64_t n, const double* S, const double* K, const double* R, const double* Y, const double* V,
+                     const double* E, const int64_t* T, double lam, int64_t base_cutoff, int64_t max_steps,
+                     double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count,
+                     int32_t bnd_cap, void* stream);
+/* american.py:428 fast_american_call over a device batch (kind CALL). */
+int fl_price_american_call(int64_t n, const double* S, const double* K, const double* R, const double* Y,
+                           const double* V, const double* E, const int64_t* T, int64_t base_cutoff, int64_t max_steps,
+                           double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols,
+                           int32_t* bnd_count, int32_t bnd_cap, void* stream);
+/* binomial.py:161 fast_european over a device batch (kind EURO; no workspace). */
+int fl_price_european(int64_t n, const double* S, const double* K, const double* R, const double* Y, const double* V,
+                      const double* E, const int64_t* T, double* price, int32_t* status, void* stream);
+/* Device bytes fl_price_batch_dev allocates for (n, max_steps) on the current
+ * device (library-owned, cached per thread, device and stream). */
+int fl_dev_workspace_bytes(int64_t n, int64_t max_steps, int method, int64_t call_cutoff, int64_t put_cutoff,
+                           int64_t* bytes);
+/* Wait for every call enqueued on `stream` (the only synchronizing call of the
+ * device-pointer API). */
+int fl_sync(void* stream);
+/* Free the calling thread's device-pointer workspaces. */
+void fl_release_dev_cache(void);
 
 /* Host-only (no CUDA call): the per-option constants and dispatch the batch
  * entry points derive, for inspection and CPU-side parity tests.

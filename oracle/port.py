@@ -45,6 +45,17 @@ __all__ = [
 ]
 
 NONE_SEEN = -(1 << 60)  # _accel.py:46
+# Boundary margins (tie evidence).  north_star lets a device boundary index
+# differ from the reference's only at a tie within tolerance.  With
+# ``margins=True`` the fast pricers also return, per boundary record produced
+# by a leaf strip, lin - exercise on that record's row at the NMARG cells
+# b-3 .. b+3 around the oracle's boundary b (b = last exercise column for the
+# put, last continuation column for the call), in the reference's own
+# expression order; NaN where a record is not a strip result.  Put margins
+# are in units of K, call margins in currency.  Same definition as the
+# golden fixtures' ``bnd_marg`` (tests/golden/make_golden.py).
+NMARG = 7
+_NOMARG = np.full(NMARG, np.nan)
 NO_GREEN = int(np.iinfo(np.int64).min)  # model.py:41
 DAYS = 365.0  # model.py:37
 
@@ -336,12 +347,42 @@ class _CallCtx:
             self.e2 = np.exp(2.0 * np.arange(m, dtype=np.float64) * self.p["lu"])
         return self.e2
 
+    want_marg = False
+    marg_last = None
+
     def strip(self, buf, lo, top_row, boundary, height, e2_len):
         p = self.p
         e2 = self.e2_min(e2_len)
-        return int(load_loops().orc_binomial_strip_sweep(
+        buf0 = buf.copy() if self.want_marg else None
+        jr = int(load_loops().orc_binomial_strip_sweep(
             _ptr(buf), _ptr(e2), lo, top_row, boundary, height,
             self.S, self.K, p["wd"], p["wu"], p["lu"]))
+        if buf0 is not None:
+            self.marg_last = self._margins(buf0, e2, lo, top_row, boundary, height, jr)
+        return jr
+
+    def _margins(self, buf, e2, lo, top_row, boundary, height, jr):
+        """lin - exercise of the strip's last row at cells jr-3 .. jr+3
+        (_accel.py:143-153 expression order); see ``boundary_margins``."""
+        p = self.p
+        j1 = boundary
+        if height > 1:
+            j1 = int(load_loops().orc_binomial_strip_sweep(
+                _ptr(buf), _ptr(e2), lo, top_row, boundary, height - 1,
+                self.S, self.K, p["wd"], p["wu"], p["lu"]))
+        m = np.full(NMARG, np.nan)
+        parent = top_row - (height - 1)
+        child = parent - 1
+        if j1 >= lo:
+            top = j1 if j1 < child else child
+            bc = self.S * math.exp((2 * lo - child) * p["lu"])
+            bp = self.S * math.exp((2 * lo - parent) * p["lu"])
+            for d in range(-(NMARG // 2), NMARG // 2 + 1):
+                c = jr + d
+                if lo <= c <= top:
+                    vr = buf[c + 1 - lo] if c + 1 <= j1 else bp * e2[c + 1 - lo] - self.K
+                    m[d + NMARG // 2] = (p["wd"] * buf[c - lo] + p["wu"] * vr) - (bc * e2[c - lo] - self.K)
+        return m
 
 
 def _call_solve(i, j, h, vals, ctx):
@@ -414,8 +455,15 @@ def _call_junction(S, K, R, Y, p, n, top_b):
     return i, j, vals
 
 
-def call_fast(S, K, R, Y, V, E, T, base_cutoff=256):
-    """american.py:428-530: (price, times, cols)."""
+def call_fast(S, K, R, Y, V, E, T, base_cutoff=256, margins=False):
+    """american.py:428-530: (price, times, cols), plus the per-record boundary
+    margins (``boundary_margins``) when ``margins``."""
+    if margins:
+        return _with_margins(_call_fast, S, K, R, Y, V, E, T, base_cutoff)
+    return _call_fast(S, K, R, Y, V, E, T, base_cutoff)[:3]
+
+
+def _call_fast(S, K, R, Y, V, E, T, base_cutoff=256, want_marg=False):
     p = derive_binomial(S, K, R, Y, V, E, T)
     n = int(T)
     if Y == 0.0:
@@ -440,25 +488,31 @@ def call_fast(S, K, R, Y, V, E, T, base_cutoff=256):
         raise OracleError("ValidationError", "times")
     resid = math.isqrt(n - 1) + 1
     ctx = _CallCtx(S, K, p, base_cutoff)
+    ctx.want_marg = want_marg
+    marg = [_NOMARG, _NOMARG]
     while i > resid and j >= 0:
         h = min(j + 1, i - resid)
+        ctx.marg_last = None
         j, vals = call_trapezoid(i, j, h, vals, ctx)
         i -= h
         times.append(i)
         bounds.append(_first_green(i, j))
+        marg.append(_NOMARG if ctx.marg_last is None else ctx.marg_last)
     if j < 0:
         price = S - K
     else:
         buf = vals.copy()
+        ctx.marg_last = None
         j0 = ctx.strip(buf, 0, i, j, i, buf.shape[0] + 1)
         price = float(buf[0]) if j0 >= 0 else S - K
         if i > 0:
             times.append(0)
             bounds.append(_first_green(0, j0))
+            marg.append(_NOMARG if ctx.marg_last is None else ctx.marg_last)
     t = np.asarray(times, dtype=np.int64)
     b = np.asarray(bounds, dtype=np.int64)
     order = np.argsort(t)
-    return price, t[order], b[order]
+    return price, t[order], b[order], np.asarray(marg)[order]
 
 
 # ---------------------------------------------------------------------------
@@ -496,10 +550,29 @@ class _PutCtx:
         self.d, self.cutoff = d, cutoff
         self.power = _Powers([d["cd"], d["cm"], d["cu"]])
 
+    want_marg = False
+    marg_last = None
+
     def sweep(self, arr, pay, lo, height):
         d = self.d
         return int(load_loops().orc_bsm_strip_sweep(
             _ptr(arr), arr.shape[0], _ptr(pay), lo, height, d["cd"], d["cm"], d["cu"]))
+
+    def margins(self, arr, pay, lo, height, kb):
+        """lin - payoff of the strip's last row at cells kb-3 .. kb+3
+        (_accel.py:232 expression order), units of K; see ``boundary_margins``."""
+        d = self.d
+        a = arr.copy()
+        if height > 1:
+            self.sweep(a, pay, lo, height - 1)
+        hi = lo + a.shape[0] - 1
+        m = np.full(NMARG, np.nan)
+        for dd in range(-(NMARG // 2), NMARG // 2 + 1):
+            k = kb + dd
+            if lo + height <= k <= hi - height:
+                lin = d["cm"] * a[k - lo] + d["cu"] * a[k + 1 - lo] + d["cd"] * a[k - 1 - lo]
+                m[dd + NMARG // 2] = lin - pay[k - lo]
+        return m
 
 
 def _put_strip(ctx, f, seg, height):
@@ -510,7 +583,10 @@ def _put_strip(ctx, f, seg, height):
     arr = np.empty(hi - lo + 1, dtype=np.float64)
     arr[: f - lo + 1] = pay[: f - lo + 1]
     arr[f - lo + 1:] = seg
+    arr0 = arr.copy() if ctx.want_marg else None
     kb = ctx.sweep(arr, pay, lo, height)
+    if arr0 is not None:
+        ctx.marg_last = ctx.margins(arr0, pay, lo, height, kb)
     if kb == NONE_SEEN or not f - height <= kb <= f:
         raise OracleError("GeometryError", None)
     return kb, arr[kb + 1 - lo: hi - height - lo + 1].copy()
@@ -564,8 +640,15 @@ def _put_apex(ctx, f, seg, rem, k_star) -> float:
     return float(arr[k_star - lo])
 
 
-def put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128):
-    """bsm.py:585-676: (price, times, cols)."""
+def put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128, margins=False):
+    """bsm.py:585-676: (price, times, cols), plus the per-record boundary
+    margins (``boundary_margins``) when ``margins``."""
+    if margins:
+        return _with_margins(_put_fast, S, K, R, Y, V, E, T, lam, base_cutoff)
+    return _put_fast(S, K, R, Y, V, E, T, lam, base_cutoff)[:3]
+
+
+def _put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128, want_marg=False):
     d = discretize_put(S, K, R, Y, V, E, T, lam)
     n, ks = d["n"], d["k_star"]
     if base_cutoff < 1:
@@ -575,7 +658,8 @@ def put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128):
     if n <= 2 * base_cutoff:
         return put_baseline(S, K, R, Y, V, E, T, lam)
     ctx = _PutCtx(d, base_cutoff)
-    times, cols = [0], [0]
+    ctx.want_marg = want_marg
+    times, cols, marg = [0], [0], [_NOMARG]
     m, f = 0, 0
     if ks + n < 1:
         raise OracleError("DomainError", "width")
@@ -592,6 +676,7 @@ def put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128):
             price = K * _put_apex(ctx, f, seg, rem, ks)
             break
         h = min(rem // 2, red // 2)
+        ctx.marg_last = None
         if h < 1:
             f, seg = _put_strip(ctx, f, seg, 1)
             m += 1
@@ -600,10 +685,21 @@ def put_fast(S, K, R, Y, V, E, T, lam=0.4, base_cutoff=128):
             m += h
         times.append(m)
         cols.append(f)
+        marg.append(_NOMARG if ctx.marg_last is None else ctx.marg_last)
     t = np.asarray(times, dtype=np.int64)
     c = np.asarray(cols, dtype=np.int64)
     order = np.argsort(t)
-    return price, t[order], c[order]
+    return price, t[order], c[order], np.asarray(marg)[order]
+
+
+def _with_margins(fn, *args):
+    """Run a fast pricer with margin recording; early-dispatch results (and
+    baseline delegation) carry NaN margins -- no tie slack."""
+    out = fn(*args, want_marg=True)
+    if len(out) == 4:
+        return out
+    p, t, c = out
+    return p, t, c, np.full((len(t), NMARG), np.nan)
 
 
 # ---------------------------------------------------------------------------

@@ -42,7 +42,9 @@ EXPORTED_SYMBOLS = (
     "fl_batch_fetch", "fl_batch_launches", "fl_batch_stats", "fl_batch_profile", "fl_batch_timeline", "fl_batch_free",
     "fl_batch_ref_flops", "fl_inspect", "fl_apply_linear_steps", "fl_put_trapezoid", "fl_call_trapezoid",
     "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
-    "fl_probe_fp64",
+    "fl_probe_fp64", "fl_release_cache", "fl_shard_plan", "fl_price_batch_multi", "fl_price_batch_dev",
+    "fl_price_put_bsm", "fl_price_american_call", "fl_price_european", "fl_dev_workspace_bytes", "fl_sync",
+    "fl_release_dev_cache",
 )
 
 
@@ -115,6 +117,28 @@ def lib():
         L.fl_euro_approx.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
+        L.fl_release_cache.argtypes = []
+        L.fl_release_cache.restype = None
+        L.fl_release_dev_cache.argtypes = []
+        L.fl_release_dev_cache.restype = None
+        L.fl_shard_plan.argtypes = [i64, P, P, c_int, P]
+        L.fl_shard_plan.restype = c_int
+        L.fl_price_batch_multi.argtypes = [c_int, P, i64, P, P, P, P, P, P, P, P, d, i64, i64, c_int,
+                                           P, P, P, P, P, i32]
+        L.fl_price_batch_multi.restype = c_int
+        L.fl_price_batch_dev.argtypes = [i64, P, c_int, P, P, P, P, P, P, P, d, i64, i64, c_int, i64,
+                                         P, P, P, P, P, i32, P]
+        L.fl_price_batch_dev.restype = c_int
+        L.fl_price_put_bsm.argtypes = [i64, P, P, P, P, P, P, P, d, i64, i64, P, P, P, P, P, i32, P]
+        L.fl_price_put_bsm.restype = c_int
+        L.fl_price_american_call.argtypes = [i64, P, P, P, P, P, P, P, i64, i64, P, P, P, P, P, i32, P]
+        L.fl_price_american_call.restype = c_int
+        L.fl_price_european.argtypes = [i64, P, P, P, P, P, P, P, P, P, P]
+        L.fl_price_european.restype = c_int
+        L.fl_dev_workspace_bytes.argtypes = [i64, i64, c_int, i64, i64, P]
+        L.fl_dev_workspace_bytes.restype = c_int
+        L.fl_sync.argtypes = [P]
+        L.fl_sync.restype = c_int
         _lib = L
         return L
 
@@ -470,3 +494,101 @@ def euro_approx(S, K, R, Y, V, E, T, method):
     _check(lib().fl_euro_approx(n, _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), int(method),
                                 _ptr(price), _ptr(status), None))
     return price, status
+
+
+# --------------------------------------------------------------------------
+# multi-device and device-pointer entry points
+
+
+def shard_plan(kind, T, nshard: int) -> np.ndarray:
+    """fl_shard_plan: owner shard of every option (LPT over the cost model)."""
+    k = np.ascontiguousarray(np.asarray(kind, dtype=np.int8))
+    t = np.ascontiguousarray(np.broadcast_to(np.asarray(T, dtype=np.int64), k.shape))
+    owner = np.empty(k.shape[0], dtype=np.int32)
+    _check(lib().fl_shard_plan(k.shape[0], _ptr(k), _ptr(t), int(nshard), _ptr(owner)))
+    return owner
+
+
+def price_batch_multi(kind, S, K, R, Y, V, E, T, *, devices=None, lam=0.4, call_cutoff=256, put_cutoff=128,
+                      method=METHOD_FAST, bnd_cap=0) -> BatchResult:
+    """One call over several GPUs (fl_price_batch_multi): LPT shards, one host
+    thread and stream per device, results gathered into host arrays."""
+    if devices is None:
+        import torch
+
+        devices = list(range(torch.cuda.device_count()))
+    devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
+    price = np.empty(n)
+    status = np.empty(n, dtype=np.int32)
+    cap = int(bnd_cap)
+    bt = np.empty((n, max(cap, 1)), dtype=np.int64)
+    bc = np.empty((n, max(cap, 1)), dtype=np.int64)
+    bcount = np.zeros(n, dtype=np.int32)
+    _check(lib().fl_price_batch_multi(
+        int(devs.shape[0]), _ptr(devs), n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E),
+        _ptr(T), float(lam), int(call_cutoff), int(put_cutoff), int(method), _ptr(price), _ptr(status),
+        _ptr(bt) if cap else None, _ptr(bc) if cap else None, _ptr(bcount) if cap else None, cap))
+    return BatchResult(price, status, bt, bc, bcount, cap)
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def price_batch_dev(kind, S, K, R, Y, V, E, T, *, max_steps=None, lam=0.4, call_cutoff=256, put_cutoff=128,
+                    method=METHOD_FAST, bnd_cap=0, kind_all=None, stream=None):
+    """fl_price_batch_dev on torch CUDA tensors (caller-owned device buffers).
+
+    Inputs: float64 S..E, int64 T, int8 ``kind`` (or ``kind=None`` with
+    ``kind_all``), all on one CUDA device.  Returns torch tensors
+    ``(price, status)`` (plus ``(bnd_times, bnd_cols, bnd_count)`` when
+    ``bnd_cap > 0``), enqueued on ``stream`` (default: torch's current stream)
+    with no synchronization.  ``max_steps`` sizes the workspaces; when omitted
+    it is read from ``T`` (one device-to-host read)."""
+    import torch
+
+    dev = S.device
+    n = int(S.shape[0])
+    cols = []
+    for x, dt in ((S, torch.float64), (K, torch.float64), (R, torch.float64), (Y, torch.float64),
+                  (V, torch.float64), (E, torch.float64), (T, torch.int64)):
+        if x.device != dev or x.dtype != dt or not x.is_contiguous():
+            raise ValueError("price_batch_dev: inputs must be contiguous tensors of one CUDA device "
+                             "(float64 S..E, int64 T)")
+        cols.append(x)
+    if kind is not None and (kind.dtype != torch.int8 or kind.device != dev):
+        raise ValueError("price_batch_dev: kind must be an int8 tensor on the inputs' device")
+    if kind is None and kind_all is None:
+        raise ValueError("price_batch_dev: pass kind or kind_all")
+    if max_steps is None:
+        max_steps = int(T.max().item()) if n else 1
+    price = torch.empty(n, dtype=torch.float64, device=dev)
+    status = torch.empty(n, dtype=torch.int32, device=dev)
+    cap = int(bnd_cap)
+    bt = torch.empty((n, cap), dtype=torch.int64, device=dev) if cap else None
+    bc = torch.empty((n, cap), dtype=torch.int64, device=dev) if cap else None
+    bn = torch.zeros(n, dtype=torch.int32, device=dev) if cap else None
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        _check(lib().fl_price_batch_dev(
+            n, _dptr(kind), -1 if kind_all is None else int(kind_all), *(_dptr(c) for c in cols), float(lam),
+            int(call_cutoff), int(put_cutoff), int(method), int(max_steps), _dptr(price), _dptr(status),
+            _dptr(bt), _dptr(bc), _dptr(bn), cap, ctypes.c_void_p(stream) if stream else None))
+    if cap:
+        return price, status, bt, bc, bn
+    return price, status
+
+
+def dev_workspace_bytes(n: int, max_steps: int, method=METHOD_FAST, call_cutoff=256, put_cutoff=128) -> int:
+    b = ctypes.c_int64(0)
+    _check(lib().fl_dev_workspace_bytes(int(n), int(max_steps), int(method), int(call_cutoff), int(put_cutoff),
+                                        ctypes.byref(b)))
+    return b.value
+
+
+def release_caches() -> None:
+    """Free this thread's cached host-path batches and device-path workspaces."""
+    lib().fl_release_cache()
+    lib().fl_release_dev_cache()

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fftlattice_b200.h"
@@ -163,6 +164,7 @@ struct fl_batch {
   DevBuf d_put, d_call, d_euro, d_orders, d_price, d_status, d_bt, d_bc, d_bcount, d_counter;
   DevBuf d_ws_put, d_ws_call, d_ws_base;
   int64_t ws_put_stride = 0, ws_call_stride = 0, ws_base_stride = 0;
+  int64_t n_put_base = 0, n_call_base = 0, n_euro_base = 0;  // widest baseline row per list
   int grid_put = 0, grid_call = 0;
   size_t off_put_fast = 0, off_put_base = 0, off_call_fast = 0, off_call_base = 0, off_euro_fast = 0,
          off_euro_base = 0;
@@ -315,9 +317,16 @@ int upload(fl_batch* b, cudaStream_t stream) {
     ksmax = std::max<int64_t>(ksmax, std::max<int64_t>(b->put[o].ks, 0));
   }
   for (int32_t o : b->o_call_fast) nmax_call = std::max(nmax_call, b->call[o].n);
-  for (int32_t o : b->o_put_base) nmax_base = std::max(nmax_base, b->put[o].n * 2 + 2);
-  for (int32_t o : b->o_call_base) nmax_base = std::max(nmax_base, b->call[o].n + 2);
-  for (int32_t o : b->o_euro_base) nmax_base = std::max(nmax_base, b->euro[o].n + 2);
+  b->n_put_base = b->n_call_base = b->n_euro_base = 0;
+  for (int32_t o : b->o_put_base) b->n_put_base = std::max(b->n_put_base, b->put[o].n);
+  for (int32_t o : b->o_call_base) b->n_call_base = std::max(b->n_call_base, b->call[o].n);
+  for (int32_t o : b->o_euro_base) b->n_euro_base = std::max(b->n_euro_base, b->euro[o].n);
+  // the global-memory fallback march needs a workspace row set per CTA; the
+  // register-resident sweeps (fl_sweep.cu) need none
+  const int64_t cells_max = fl::sweep_max_cells();
+  if (2 * b->n_put_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_put_base * 2 + 2);
+  if (b->n_call_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_call_base + 2);
+  if (b->n_euro_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_euro_base + 2);
   if (!b->o_put_fast.empty()) {
     b->ws_put_stride = fl::put_ws_doubles(nmax_put, ksmax);
     const int nc = fl::put_chains_per_cta();
@@ -337,7 +346,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
     FL_CUDA(b->d_ws_put.ensure(sizeof(double) * b->ws_mixed_stride * b->grid_mixed * nc));
   }
   const int64_t nbase = (int64_t)std::max({b->o_put_base.size(), b->o_call_base.size(), b->o_euro_base.size()});
-  if (nbase > 0) {
+  if (nbase > 0 && nmax_base > 0) {
     b->ws_base_stride = 3 * nmax_base + 16;
     FL_CUDA(b->d_ws_base.ensure(sizeof(double) * b->ws_base_stride * nbase));
   }
@@ -413,24 +422,25 @@ int run(fl_batch* b, cudaStream_t stream) {
   }
   if (!b->o_euro_fast.empty()) {
     FL_CUDA(fl::launch_euro_fast(b->d_euro.as<fl::EuroParams>(), ord + b->off_euro_fast, (int)b->o_euro_fast.size(),
-                                 out, stream));
+                                 (int)b->o_euro_fast.size(), out, stream));
     ++b->launches;
   }
   if (!b->o_put_base.empty()) {
-    FL_CUDA(fl::launch_put_baseline(b->d_put.as<fl::PutParams>(), ord + b->off_put_base, (int)b->o_put_base.size(),
+    const int nb = (int)b->o_put_base.size();
+    FL_CUDA(fl::launch_put_baseline(b->d_put.as<fl::PutParams>(), ord + b->off_put_base, nb, b->n_put_base, nb,
                                     b->d_ws_base.as<double>(), b->ws_base_stride, out, stream));
     ++b->launches;
   }
   if (!b->o_call_base.empty()) {
-    FL_CUDA(fl::launch_call_baseline(b->d_call.as<fl::CallParams>(), ord + b->off_call_base,
-                                     (int)b->o_call_base.size(), b->d_ws_base.as<double>(), b->ws_base_stride, out,
-                                     stream));
+    const int nb = (int)b->o_call_base.size();
+    FL_CUDA(fl::launch_call_baseline(b->d_call.as<fl::CallParams>(), ord + b->off_call_base, nb, b->n_call_base, nb,
+                                     b->d_ws_base.as<double>(), b->ws_base_stride, out, stream));
     ++b->launches;
   }
   if (!b->o_euro_base.empty()) {
-    FL_CUDA(fl::launch_euro_baseline(b->d_euro.as<fl::EuroParams>(), ord + b->off_euro_base,
-                                     (int)b->o_euro_base.size(), b->d_ws_base.as<double>(), b->ws_base_stride, out,
-                                     stream));
+    const int nb = (int)b->o_euro_base.size();
+    FL_CUDA(fl::launch_euro_baseline(b->d_euro.as<fl::EuroParams>(), ord + b->off_euro_base, nb, b->n_euro_base, nb,
+                                     b->d_ws_base.as<double>(), b->ws_base_stride, out, stream));
     ++b->launches;
   }
   return 0;
@@ -912,24 +922,154 @@ void fl_batch_free(fl_batch* b) {
   delete b;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One cached batch per (thread, device): device buffers grow and are reused
+// across calls; released when the thread exits or on fl_release_cache().
+struct BatchCache {
+  fl_batch* b[64] = {nullptr};
+  void release_all() {
+    for (fl_batch*& p : b)
+      if (p) {
+        p->release();
+        delete p;
+        p = nullptr;
+      }
+  }
+  ~BatchCache() { release_all(); }
+};
+thread_local BatchCache t_cache;
+
+int price_with(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+               const double* Y, const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
+               int64_t put_cutoff, int method, double* price, int32_t* status, int64_t* bnd_times,
+               int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, cudaStream_t stream) {
+  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+  if (rc) return rc;
+  rc = upload(b, stream);
+  if (rc) return rc;
+  rc = run(b, stream);
+  if (rc) return rc;
+  return fetch(b, price, status, bnd_times, bnd_cols, bnd_count, stream);
+}
+
+// Process-wide per-device batches for the multi-device entry (its worker
+// threads are short-lived; the buffers persist per device, one user at a time).
+std::mutex g_dev_mu[64];
+fl_batch* g_dev_batch[64] = {nullptr};
+
+}  // namespace
+
+extern "C" {
+
 int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
                    const double* Y, const double* V, const double* E, const int64_t* T, double lam,
                    int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
                    int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream) {
-  // one cached batch per (thread, device): device buffers grow and are reused
-  thread_local fl_batch* cache[64] = {nullptr};
   int dev = 0;
   FL_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return fail("fl_price_batch: device index out of range");
-  if (!cache[dev]) cache[dev] = new fl_batch();
-  fl_batch* b = cache[dev];
-  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
-  if (rc) return rc;
-  rc = upload(b, (cudaStream_t)stream);
-  if (rc) return rc;
-  rc = run(b, (cudaStream_t)stream);
-  if (rc) return rc;
-  return fetch(b, price, status, bnd_times, bnd_cols, bnd_count, (cudaStream_t)stream);
+  if (!t_cache.b[dev]) t_cache.b[dev] = new fl_batch();
+  return price_with(t_cache.b[dev], n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, price,
+                    status, bnd_times, bnd_cols, bnd_count, bnd_cap, (cudaStream_t)stream);
+}
+
+void fl_release_cache(void) { t_cache.release_all(); }
+
+int fl_shard_plan(int64_t n, const int8_t* kind, const int64_t* T, int nshard, int32_t* owner) {
+  if (nshard < 1 || !owner) return fail("fl_shard_plan: nshard must be >= 1");
+  // longest-processing-time greedy over the survey's cost model (shard.py)
+  std::vector<double> cost(n);
+  for (int64_t i = 0; i < n; ++i)
+    cost[i] = kind[i] == FL_KIND_PUT ? cost_put(T[i]) : kind[i] == FL_KIND_CALL ? cost_call(T[i]) : 8.0 * (double)T[i];
+  std::vector<int64_t> ord(n);
+  for (int64_t i = 0; i < n; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+  std::vector<double> load(nshard, 0.0);
+  for (int64_t i : ord) {
+    const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[i] = r;
+    load[r] += cost[i];
+  }
+  return 0;
+}
+
+int fl_price_batch_multi(int ndev, const int* devices, int64_t n, const int8_t* kind, const double* S,
+                         const double* K, const double* R, const double* Y, const double* V, const double* E,
+                         const int64_t* T, double lam, int64_t call_cutoff, int64_t put_cutoff, int method,
+                         double* price, int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count,
+                         int32_t bnd_cap) {
+  if (ndev < 1 || !devices) return fail("fl_price_batch_multi: need at least one device");
+  int ndev_vis = 0;
+  FL_CUDA(cudaGetDeviceCount(&ndev_vis));
+  for (int d = 0; d < ndev; ++d)
+    if (devices[d] < 0 || devices[d] >= ndev_vis || devices[d] >= 64)
+      return fail("fl_price_batch_multi: invalid device " + std::to_string(devices[d]));
+  std::vector<int32_t> owner(n);
+  if (const int rc = fl_shard_plan(n, kind, T, ndev, owner.data())) return rc;
+  const bool want_b = bnd_cap > 0 && bnd_times && bnd_cols && bnd_count;
+  std::vector<std::string> err(ndev);
+  std::vector<std::thread> th;
+  for (int d = 0; d < ndev; ++d) {
+    th.emplace_back([&, d] {
+      std::vector<int64_t> idx;
+      for (int64_t i = 0; i < n; ++i)
+        if (owner[i] == d) idx.push_back(i);
+      const int64_t m = (int64_t)idx.size();
+      if (m == 0) return;
+      const int dev = devices[d];
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        err[d] = "cudaSetDevice failed";
+        return;
+      }
+      // gather this shard's inputs (contiguous), price on the device's own
+      // stream, scatter the results back: option i's arithmetic does not
+      // depend on its shard, so results equal the single-device call's
+      std::vector<int8_t> k(m);
+      std::vector<double> s(m), kk(m), r(m), y(m), v(m), e(m), p(m);
+      std::vector<int64_t> t(m), bt(want_b ? m * bnd_cap : 0), bc(want_b ? m * bnd_cap : 0);
+      std::vector<int32_t> st(m), cnt(want_b ? m : 0);
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t i = idx[j];
+        k[j] = kind[i]; s[j] = S[i]; kk[j] = K[i]; r[j] = R[i]; y[j] = Y[i]; v[j] = V[i]; e[j] = E[i]; t[j] = T[i];
+      }
+      cudaStream_t stream = nullptr;
+      if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess) {
+        err[d] = "cudaStreamCreate failed";
+        return;
+      }
+      int rc = 0;
+      {
+        std::lock_guard<std::mutex> lk(g_dev_mu[dev]);
+        if (!g_dev_batch[dev]) g_dev_batch[dev] = new fl_batch();
+        rc = price_with(g_dev_batch[dev], m, k.data(), s.data(), kk.data(), r.data(), y.data(), v.data(), e.data(),
+                        t.data(), lam, call_cutoff, put_cutoff, method, p.data(), st.data(),
+                        want_b ? bt.data() : nullptr, want_b ? bc.data() : nullptr, want_b ? cnt.data() : nullptr,
+                        want_b ? bnd_cap : 0, stream);
+      }
+      cudaStreamDestroy(stream);
+      if (rc) {
+        err[d] = "device " + std::to_string(dev) + ": " + g_last_error;
+        return;
+      }
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t i = idx[j];
+        price[i] = p[j];
+        status[i] = st[j];
+        if (want_b) {
+          bnd_count[i] = cnt[j];
+          std::copy(bt.begin() + j * bnd_cap, bt.begin() + (j + 1) * bnd_cap, bnd_times + i * bnd_cap);
+          std::copy(bc.begin() + j * bnd_cap, bc.begin() + (j + 1) * bnd_cap, bnd_cols + i * bnd_cap);
+        }
+      }
+    });
+  }
+  for (auto& x : th) x.join();
+  for (int d = 0; d < ndev; ++d)
+    if (!err[d].empty()) return fail("fl_price_batch_multi: " + err[d]);
+  return 0;
 }
 
 int fl_apply_linear_steps(const double* x, int64_t L, int taps, double c0, double c1, double c2, int64_t h,

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(SCHED_THREADS, 1)
 american_fast_kernel(const PutParams* __restrict__ put, const CallParams* __restrict__ call,
                      const int32_t* __restrict__ order, int nwork, int32_t* counter, double* __restrict__ ws,
                      int64_t ws_stride, BatchOut out) {
+  apply_dlist(out, order, nwork);
   const AmericanPricer<ACCT> pr{put, call, order, out};
   sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
@@ -45,14 +46,16 @@ american_fast_kernel(const PutParams* __restrict__ put, const CallParams* __rest
 cudaError_t launch_american_fast(const PutParams* put, const CallParams* call, const int32_t* order, int nwork,
                                  int32_t* counter, double* ws, int64_t ws_stride, int grid, BatchOut out,
                                  cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<unsigned long long> configured{0};
   const int smem = sched_smem_bytes();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(american_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(american_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = once_per_device(configured, [&] {
+      cudaError_t r = cudaFuncSetAttribute(american_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(american_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      return r;
+    });
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   if (nwork <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(int32_t), stream);

@@ -660,6 +660,7 @@ struct CallPricer {
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 call_fast_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                  int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
+  apply_dlist(out, order, nwork);
   const CallPricer pr{opts, order, out};
   sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
@@ -729,8 +730,8 @@ __global__ void __launch_bounds__(CTA_THREADS)
 call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                      double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
   __shared__ int s_fg;
-  const int w = blockIdx.x;
-  if (w >= nwork) return;
+  apply_dlist(out, order, nwork);
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
   const int o = order[w];
   const CallParams P = opts[o];
   const int64_t n = P.n;
@@ -787,20 +788,22 @@ call_baseline_kernel(const CallParams* __restrict__ opts, const int32_t* __restr
     out.status[o] = 0;
     if (out.bcount) out.bcount[o] = (int32_t)(n + 1);
   }
+  __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
 // launchers
 
 static cudaError_t call_configure() {
-  static bool configured = false;
-  if (configured) return cudaSuccess;
-  const int smem = sched_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(call_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(call_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) configured = true;
-  return e;
+  static std::atomic<unsigned long long> configured{0};
+  return once_per_device(configured, [] {
+    const int smem = sched_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(call_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(call_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return e;
+  });
 }
 
 int call_chains_per_cta() { return NCHAIN; }
@@ -886,10 +889,11 @@ cudaError_t launch_call_grid(const CallParams& P, double* rows, uint8_t* masks, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,
-                                 int64_t ws_stride, BatchOut out, cudaStream_t stream) {
-  if (nwork <= 0) return cudaSuccess;
-  call_baseline_kernel<<<nwork, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
+cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                 double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream) {
+  if (nwork <= 0 || grid <= 0) return cudaSuccess;
+  if (n_max + 1 <= sweep_max_cells()) return launch_call_sweep(opts, order, nwork, n_max, grid, out, stream);
+  call_baseline_kernel<<<grid, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
   return cudaGetLastError();
 }
 

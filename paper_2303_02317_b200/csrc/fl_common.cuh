@@ -4,6 +4,7 @@
 // per-option parameter records produced by the host (host_params.h).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -72,5 +73,22 @@ constexpr unsigned FULL = 0xffffffffu;
 
 __device__ __forceinline__ int warp_max_i32(int v) { return __reduce_max_sync(FULL, v); }
 __device__ __forceinline__ int warp_min_i32(int v) { return __reduce_min_sync(FULL, v); }
+
+// ---------------------------------------------------------------------------
+// Kernel attributes (cudaFuncSetAttribute) belong to the current device's
+// context: run `set` once per device, tracked in a bit mask (a lost race only
+// sets the same attribute twice).
+template <class F>
+inline cudaError_t once_per_device(std::atomic<unsigned long long>& mask, F&& set) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  const unsigned long long bit = 1ull << dev;
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = set();
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 }  // namespace fl

@@ -81,12 +81,13 @@ int linear_steps_smem_bytes() { return smem_complex_slots(1 << (LS_LOGN_MAX - 1)
 
 cudaError_t launch_linear_steps(const double* x, int64_t L, double* y, int64_t Lout, int h, double c0, double c1,
                                 double c2, int span, cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<unsigned long long> configured{0};
   const int smem = linear_steps_smem_bytes();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(linear_steps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = once_per_device(configured, [&] {
+      return cudaFuncSetAttribute(linear_steps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   Stencil st{c0, c1, c2, span};
   linear_steps_kernel<<<1, CTA_THREADS, smem, stream>>>(x, L, y, Lout, h, st);

@@ -109,8 +109,8 @@ constexpr int EURO_THREADS = 256;
 __global__ void __launch_bounds__(EURO_THREADS)
 euro_fast_kernel(const EuroParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork, BatchOut out) {
   __shared__ double red[EURO_THREADS / 32];
-  const int w = blockIdx.x;
-  if (w >= nwork) return;
+  apply_dlist(out, order, nwork);
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
   const int o = order[w];
   const EuroParams E = opts[o];
   const int64_t T = E.n;
@@ -137,14 +137,16 @@ euro_fast_kernel(const EuroParams* __restrict__ opts, const int32_t* __restrict_
     out.status[o] = 0;
     if (out.bcount) out.bcount[o] = 0;
   }
+  __syncthreads();
+  }
 }
 
 // O(T^2) backward induction of the leaf row (european_backward), one CTA per option.
 __global__ void __launch_bounds__(EURO_THREADS)
 euro_baseline_kernel(const EuroParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork, double* __restrict__ ws, int64_t ws_stride,
                      BatchOut out) {
-  const int w = blockIdx.x;
-  if (w >= nwork) return;
+  apply_dlist(out, order, nwork);
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
   const int o = order[w];
   const EuroParams E = opts[o];
   const double wd = E.wd, wu = E.wu;
@@ -168,19 +170,22 @@ euro_baseline_kernel(const EuroParams* __restrict__ opts, const int32_t* __restr
     out.status[o] = 0;
     if (out.bcount) out.bcount[o] = 0;
   }
+  __syncthreads();
+  }
 }
 
-cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, BatchOut out,
+cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, int grid, BatchOut out,
                              cudaStream_t stream) {
-  if (nwork <= 0) return cudaSuccess;
-  euro_fast_kernel<<<nwork, EURO_THREADS, 0, stream>>>(opts, order, nwork, out);
+  if (nwork <= 0 || grid <= 0) return cudaSuccess;
+  euro_fast_kernel<<<grid, EURO_THREADS, 0, stream>>>(opts, order, nwork, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, int nwork, double* ws,
-                                 int64_t ws_stride, BatchOut out, cudaStream_t stream) {
-  if (nwork <= 0) return cudaSuccess;
-  euro_baseline_kernel<<<nwork, EURO_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
+cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                 double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream) {
+  if (nwork <= 0 || grid <= 0) return cudaSuccess;
+  if (n_max + 1 <= sweep_max_cells()) return launch_euro_sweep(opts, order, nwork, n_max, grid, out, stream);
+  euro_baseline_kernel<<<grid, EURO_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
   return cudaGetLastError();
 }
 

@@ -29,7 +29,20 @@ struct BatchOut {
   double* snap = nullptr;
   int64_t snap_cap = 0;
   int64_t* snap_len = nullptr;
+  // device-planned launches (fl_price_batch_dev): when set, the work list is
+  // order[dlist[0] .. dlist[1]) (decided on the device, so the host launches
+  // with an upper bound and never reads the count back)
+  const int32_t* dlist = nullptr;
 };
+
+// Apply a device-side work list (BatchOut::dlist) at kernel entry.
+template <class Ptr>
+__device__ __forceinline__ void apply_dlist(const BatchOut& out, Ptr& order, int& nwork) {
+  if (out.dlist) {
+    order += out.dlist[0];
+    nwork = out.dlist[1] - out.dlist[0];
+  }
+}
 
 void init_twiddles(cudaStream_t stream);
 cudaError_t probe_fp64(double* tflops, cudaStream_t stream);
@@ -39,17 +52,26 @@ int put_fast_smem_bytes();
 int put_chains_per_cta();
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                             int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
-cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, double* ws,
-                                int64_t ws_stride, BatchOut out, cudaStream_t stream);
+cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream);
 int64_t put_trap_ws_doubles(int64_t f, int64_t W, int64_t h);
 cudaError_t launch_put_trapezoid(const PutParams& P, int64_t f, int64_t W, int64_t h, const double* seg,
                                  double* out, int64_t* meta, int32_t* counter, double* ws, int64_t ws_stride,
                                  unsigned long long* flops, cudaStream_t stream);
 
-cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, BatchOut out,
+cudaError_t launch_euro_fast(const EuroParams* opts, const int32_t* order, int nwork, int grid, BatchOut out,
                              cudaStream_t stream);
-cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, int nwork, double* ws,
-                                 int64_t ws_stride, BatchOut out, cudaStream_t stream);
+cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                 double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream);
+
+// register-resident O(T^2) sweeps (fl_sweep.cu); rows of at most sweep_max_cells()
+int64_t sweep_max_cells();
+cudaError_t launch_put_sweep(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                             BatchOut out, cudaStream_t stream);
+cudaError_t launch_call_sweep(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                              BatchOut out, cudaStream_t stream);
+cudaError_t launch_euro_sweep(const EuroParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                              BatchOut out, cudaStream_t stream);
 
 int linear_steps_smem_bytes();
 cudaError_t launch_linear_steps(const double* x, int64_t L, double* y, int64_t Lout, int h, double c0, double c1,
@@ -64,8 +86,8 @@ cudaError_t launch_call_trapezoid(const CallParams& P, int64_t i, int64_t j, int
                                   int64_t ws_stride, unsigned long long* flops, cudaStream_t stream);
 cudaError_t launch_call_fast(const CallParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
                              int64_t ws_stride, int grid, BatchOut out, cudaStream_t stream);
-cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, double* ws,
-                                 int64_t ws_stride, BatchOut out, cudaStream_t stream);
+cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                 double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream);
 
 // mixed American put / call batches (fl_american.cu): work item e >= 0 is put
 // option e, e < 0 call option -e-1

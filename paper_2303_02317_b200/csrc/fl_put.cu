@@ -662,6 +662,7 @@ template <bool ACCT>
 __global__ void __launch_bounds__(SCHED_THREADS, 1)
 put_fast_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                 int32_t* counter, double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
+  apply_dlist(out, order, nwork);
   const PutPricer<ACCT> pr{opts, order, out};
   sched_body(pr, nwork, counter, ws, ws_stride, out.flops, out.prof);
 }
@@ -716,8 +717,8 @@ __global__ void __launch_bounds__(CTA_THREADS)
 put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restrict__ order, int nwork,
                     double* __restrict__ ws, int64_t ws_stride, BatchOut out) {
   __shared__ int s_red[CTA_THREADS / 32];
-  const int w = blockIdx.x;
-  if (w >= nwork) return;
+  apply_dlist(out, order, nwork);
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
   const int o = order[w];
   const PutParams P = opts[o];
   const int64_t n = P.n;
@@ -769,6 +770,8 @@ put_baseline_kernel(const PutParams* __restrict__ opts, const int32_t* __restric
     out.status[o] = 0;
     if (out.bcount) out.bcount[o] = (int32_t)(n + 1);
   }
+  __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -778,16 +781,16 @@ int put_fast_smem_bytes() { return sched_smem_bytes(); }
 int put_chains_per_cta() { return NCHAIN; }
 
 static cudaError_t put_configure() {
-  static bool configured = false;
-  if (configured) return cudaSuccess;
-  const int smem = sched_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(put_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(put_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(put_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) configured = true;
-  return e;
+  static std::atomic<unsigned long long> configured{0};
+  return once_per_device(configured, [] {
+    const int smem = sched_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(put_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(put_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(put_trap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return e;
+  });
 }
 
 cudaError_t launch_put_fast(const PutParams* opts, const int32_t* order, int nwork, int32_t* counter, double* ws,
@@ -885,10 +888,14 @@ cudaError_t launch_put_march_rows(const PutParams& P, const int64_t* times, int 
   return cudaGetLastError();
 }
 
-cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, double* ws,
-                                int64_t ws_stride, BatchOut out, cudaStream_t stream) {
-  if (nwork <= 0) return cudaSuccess;
-  put_baseline_kernel<<<nwork, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
+// O(T^2) baseline: the register-resident sweep (fl_sweep.cu) when the row
+// fits its tile, else the global-memory march.  grid: CTAs (each loops over
+// work items; the global march needs ws_stride doubles per CTA).
+cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
+                                double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream) {
+  if (nwork <= 0 || grid <= 0) return cudaSuccess;
+  if (2 * n_max + 1 <= sweep_max_cells()) return launch_put_sweep(opts, order, nwork, n_max, grid, out, stream);
+  put_baseline_kernel<<<grid, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
   return cudaGetLastError();
 }
 

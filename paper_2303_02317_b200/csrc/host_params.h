@@ -17,6 +17,18 @@
 
 #include "fl_status.h"
 
+// The same derivation also runs on the device for the device-pointer entry
+// points (fl_price_batch_dev: caller-owned device buffers, no host round trip).
+// There the CUDA libm (exp/log within 1 ulp) and the compiler's FMA
+// contraction replace glibc's bits, so device-derived constants may differ
+// from the reference's in the last place; prices stay within the parity
+// tolerance and the host path stays bit-identical.
+#ifdef __CUDACC__
+#define FL_HD __host__ __device__
+#else
+#define FL_HD
+#endif
+
 namespace fl {
 
 enum : int32_t {
@@ -63,7 +75,7 @@ struct EuroParams {
 
 constexpr double DAYS_PER_YEAR = 365.0;
 
-inline int32_t validate_spec(const SpecIn& s) {
+FL_HD inline int32_t validate_spec(const SpecIn& s) {
   if (!(s.S > 0.0 && std::isfinite(s.S))) return FL_E_VALIDATION | FL_F_SPOT;
   if (!(s.K >= 0.0 && std::isfinite(s.K))) return FL_E_VALIDATION | FL_F_STRIKE;
   if (!(s.R >= 0.0 && std::isfinite(s.R))) return FL_E_VALIDATION | FL_F_RATE;
@@ -78,7 +90,7 @@ struct Binom {
   double dt, up, down, p, disc, wd, wu, lu;
 };
 
-inline int32_t derive_binomial(const SpecIn& s, Binom& b) {
+FL_HD inline int32_t derive_binomial(const SpecIn& s, Binom& b) {
   int32_t st = validate_spec(s);
   if (st) return st;
   b.dt = s.E / (DAYS_PER_YEAR * (double)s.T);
@@ -94,12 +106,12 @@ inline int32_t derive_binomial(const SpecIn& s, Binom& b) {
   return FL_OK;
 }
 
-inline double green_call(const SpecIn& s, const Binom& b, int64_t i, int64_t j) {
+FL_HD inline double green_call(const SpecIn& s, const Binom& b, int64_t i, int64_t j) {
   return s.S * std::exp((double)(2 * j - i) * b.lu) - s.K;
 }
 
 // american.py:260-295
-inline int64_t call_top_boundary(const SpecIn& s, const Binom& b) {
+FL_HD inline int64_t call_top_boundary(const SpecIn& s, const Binom& b) {
   const int64_t n = s.T;
   if (s.K <= 0.0) return -1;
   double g = std::floor(0.5 * (double)n + std::log(s.K / s.S) / (2.0 * b.lu));
@@ -112,7 +124,7 @@ inline int64_t call_top_boundary(const SpecIn& s, const Binom& b) {
 }
 
 // american.py:366-425, boundary part; returns status (ValueError on log domain)
-inline int32_t call_junction_boundary(const SpecIn& s, const Binom& b, int64_t top_b, int64_t& j_out) {
+FL_HD inline int32_t call_junction_boundary(const SpecIn& s, const Binom& b, int64_t top_b, int64_t& j_out) {
   const int64_t n = s.T;
   const int64_t i = n - 1;
   auto red = [&](int64_t j) {
@@ -144,7 +156,7 @@ inline int32_t call_junction_boundary(const SpecIn& s, const Binom& b, int64_t t
   return FL_OK;
 }
 
-inline int32_t prep_euro(const SpecIn& s, EuroParams& e) {
+FL_HD inline int32_t prep_euro(const SpecIn& s, EuroParams& e) {
   Binom b;
   int32_t st = derive_binomial(s, b);
   e.S = s.S; e.K = s.K; e.n = s.T; e.lu = b.lu;
@@ -158,7 +170,7 @@ inline int32_t prep_euro(const SpecIn& s, EuroParams& e) {
 }
 
 // american.py:428-470 dispatch
-inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroParams& e) {
+FL_HD inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroParams& e) {
   Binom b;
   c.S = s.S; c.K = s.K; c.n = s.T; c.cutoff = (int32_t)cutoff; c.price = 0.0;
   c.top_b = -1; c.junc_j = -1;
@@ -227,7 +239,7 @@ struct PutDisc {
 };
 
 // bsm.py:150-229
-inline int32_t discretize_put(const SpecIn& s, double lam, PutDisc& d) {
+FL_HD inline int32_t discretize_put(const SpecIn& s, double lam, PutDisc& d) {
   int32_t st = validate_spec(s);
   if (st) return st;
   const int64_t n = s.T;
@@ -257,7 +269,7 @@ inline int32_t discretize_put(const SpecIn& s, double lam, PutDisc& d) {
 }
 
 // bsm.py:585-625 dispatch
-inline int32_t prep_put(const SpecIn& s, double lam, int64_t cutoff, PutParams& p) {
+FL_HD inline int32_t prep_put(const SpecIn& s, double lam, int64_t cutoff, PutParams& p) {
   PutDisc d;
   p.S = s.S; p.K = s.K; p.n = s.T; p.cutoff = (int32_t)cutoff; p.price = 0.0;
   p.cd = p.cm = p.cu = p.ds = 0.0; p.ks = 0; p.slide = 0; p.pad = 0;

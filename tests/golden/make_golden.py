@@ -52,13 +52,114 @@ def run_ref(kind, spec, method="fast"):
         return math.nan, np.zeros(0, np.int64), np.zeros(0, np.int64), type(e).__name__, fld or ""
 
 
-def save(name, batch: Batch, method="fast"):
+# --- boundary margins -------------------------------------------------------
+# north_star allows a boundary index to differ from the reference's only "at
+# ties within tolerance".  To check that on the device without the reference,
+# the goldens carry, for every boundary record the reference produced with a
+# leaf strip, the reference's own  lin - exercise  at the 7 cells around its
+# boundary on that record's row (cells b-3 .. b+3, b = last exercise column for
+# the put, last continuation column for the call).  They are computed by
+# re-running the reference's strip sweep (unmodified numba kernel) for
+# height-1 rows on a copy and evaluating the last row with the kernel's own
+# expression and evaluation order (_accel.py:232 put, :148-149 call), so they
+# are the reference's bits.  Put margins are in units of K (the put grid is
+# normalised by the strike), call margins in currency units; NaN where the
+# record was not produced by a strip (payoff row, junction row, baseline
+# dispatch) -- those records get no slack.
+from fftlattice import _accel as _ref_accel  # noqa: E402
+from fftlattice import bsm as _ref_bsm  # noqa: E402
+
+NMARG = 7
+_MARG: dict = {}
+_orig_strip_advance = _ref_bsm._strip_advance
+_orig_binomial_sweep = _ref_accel.binomial_strip_sweep
+
+
+def _strip_advance_margins(ctx, time_index, boundary, seg, height):
+    kb, out = _orig_strip_advance(ctx, time_index, boundary, seg, height)
+    disc = ctx.disc
+    cd, cm, cu = disc.coef_down, disc.coef_mid, disc.coef_up
+    f = boundary
+    hi = f + seg.shape[0]
+    lo = f - 2 * height - 1
+    payoff = _ref_bsm._payoff_slice(disc, lo, hi)
+    arr = np.empty(hi - lo + 1, dtype=np.float64)
+    arr[: f - lo + 1] = payoff[: f - lo + 1]
+    arr[f - lo + 1:] = seg
+    if height > 1:
+        _ref_accel.bsm_strip_sweep(arr, payoff, lo, height - 1, cd, cm, cu)
+    m = np.full(NMARG, np.nan)
+    for d in range(-(NMARG // 2), NMARG // 2 + 1):
+        k = kb + d
+        if lo + height <= k <= hi - height:
+            left, cur, right = arr[k - 1 - lo], arr[k - lo], arr[k + 1 - lo]
+            lin = cm * cur + cu * right + cd * left
+            m[d + NMARG // 2] = lin - payoff[k - lo]
+    _MARG[time_index + height] = m
+    return kb, out
+
+
+def _binomial_sweep_margins(values, e2, lo, top_row, boundary, height, spot, strike, wd, wu, log_up):
+    buf = values.copy()
+    jr = int(_orig_binomial_sweep(values, e2, lo, top_row, boundary, height, spot, strike, wd, wu, log_up))
+    j1 = boundary
+    if height > 1:
+        j1 = int(_orig_binomial_sweep(buf, e2, lo, top_row, boundary, height - 1, spot, strike, wd, wu, log_up))
+    m = np.full(NMARG, np.nan)
+    parent = top_row - (height - 1)
+    child = parent - 1
+    if j1 >= lo:
+        top = j1 if j1 < child else child
+        base_child = spot * math.exp((2 * lo - child) * log_up)
+        base_parent = spot * math.exp((2 * lo - parent) * log_up)
+        for d in range(-(NMARG // 2), NMARG // 2 + 1):
+            c = jr + d
+            if lo <= c <= top:
+                vr = buf[c + 1 - lo] if c + 1 <= j1 else base_parent * e2[c + 1 - lo] - strike
+                lin = wd * buf[c - lo] + wu * vr
+                grn = base_child * e2[c - lo] - strike
+                m[d + NMARG // 2] = lin - grn
+    _MARG[top_row - height] = m
+    return jr
+
+
+_ref_bsm._strip_advance = _strip_advance_margins
+_ref_accel.binomial_strip_sweep = _binomial_sweep_margins
+
+
+def run_ref_marg(kind, spec, method="fast"):
+    """run_ref plus the per-record boundary margins (n_rec x NMARG)."""
+    _MARG.clear()
+    p, t, c, ek, ef = run_ref(kind, spec, method)
+    marg = np.full((len(t), NMARG), np.nan)
+    if kind != KIND_EURO and method == "fast":
+        for r, tm in enumerate(t.tolist()):
+            if tm in _MARG:
+                marg[r] = _MARG[tm]
+    return p, t, c, ek, ef, marg
+
+
+def _run_one(args):
+    kind, spec, method = args
+    return run_ref_marg(kind, spec, method)
+
+
+def save(name, batch: Batch, method="fast", procs=None):
+    """Price ``batch`` with the reference (``procs`` forked workers) and save."""
+    import multiprocessing as mp
+
     t0 = time.time()
-    prices, terr, tfld, offs, times, cols = [], [], [], [0], [], []
-    for i in range(len(batch)):
-        p, t, c, ek, ef = run_ref(int(batch.kind[i]), batch.spec(i), method)
+    prices, terr, tfld, offs, times, cols, margs = [], [], [], [0], [], [], []
+    jobs = [(int(batch.kind[i]), batch.spec(i), method) for i in range(len(batch))]
+    procs = procs or int(os.environ.get("GOLDEN_PROCS", os.cpu_count() or 1))
+    if procs > 1 and len(jobs) > 8:
+        with mp.get_context("fork").Pool(procs) as pool:
+            results = pool.map(_run_one, jobs, chunksize=1)
+    else:
+        results = [_run_one(j) for j in jobs]
+    for p, t, c, ek, ef, mg in results:
         prices.append(p); terr.append(ek); tfld.append(ef)
-        times.append(t); cols.append(c); offs.append(offs[-1] + len(t))
+        times.append(t); cols.append(c); offs.append(offs[-1] + len(t)); margs.append(mg)
     np.savez_compressed(
         os.path.join(HERE, f"{name}.npz"),
         kind=batch.kind, S=batch.S, K=batch.K, R=batch.R, Y=batch.Y, V=batch.V,
@@ -66,6 +167,7 @@ def save(name, batch: Batch, method="fast"):
         err_field=np.asarray(tfld), bnd_off=np.asarray(offs, np.int64),
         bnd_times=np.concatenate(times) if times else np.zeros(0, np.int64),
         bnd_cols=np.concatenate(cols) if cols else np.zeros(0, np.int64),
+        bnd_marg=np.concatenate(margs) if margs else np.zeros((0, NMARG)),
         method=np.asarray(method),
     )
     print(f"{name}: {len(batch)} options, {time.time() - t0:.1f}s", flush=True)
@@ -201,7 +303,9 @@ def ops_cases():
         for h in (h0, max(1, h0 // 3)):
             if len(st.segment) < 2 * h:
                 break
+            _MARG.clear()
             nxt = fl.solve_bsm_trapezoid(disc, st, h)
+            out[f"pt{k}_marg"] = _MARG.get(st.time_index + h, np.full(NMARG, np.nan))
             out[f"pt{k}_coef"] = np.array([disc.coef_down, disc.coef_mid, disc.coef_up, disc.d_s])
             out[f"pt{k}_f"] = np.asarray(st.boundary)
             out[f"pt{k}_t"] = np.asarray(st.time_index)
@@ -226,7 +330,9 @@ def ops_cases():
                 break
             h = min(j + 1, i - resid)
             prob = fl.TrapezoidProblem(i, j, h, fl.GridRow(i, 0, vals))
+            _MARG.clear()
             st = fl.solve_trapezoid(spec, prob, p)
+            out[f"ct{k}_marg"] = _MARG.get(i - h, np.full(NMARG, np.nan))
             out[f"ct{k}_spec"] = np.array([spec.spot, spec.strike, spec.rate, spec.dividend_yield,
                                            spec.volatility, spec.days_to_expiry, spec.steps], dtype=np.float64)
             out[f"ct{k}_i"] = np.asarray(i)
@@ -401,12 +507,11 @@ if __name__ == "__main__":
     if want("c3"):
         save("c3_fast", draw_config(3), "fast")
     if want("c6"):
-        save("c6_fast", draw_config(6, n=32), "fast")
+        save("c6_fast", draw_config(6, n=256), "fast")  # every timed headline option
     if want("c4"):
-        b = draw_config(4)
-        save("c4_fast", b.subset(np.r_[0:4, 64:68]), "fast")
+        save("c4_fast", draw_config(4), "fast")  # all 64 puts + 64 calls
     if want("c5"):
-        save("c5_fast", stratified_c5(), "fast")
+        save("c5_fast", stratified_c5(per=49), "fast")  # >= 1/64 of every (kind, T) stratum
     if want("ops"):
         ops_cases()
     if want("api"):

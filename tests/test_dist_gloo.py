@@ -35,6 +35,11 @@ def _worker(rank, world, port, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     b = draw_config(5, n=600)
     idx = lpt_shards(b.kind, b.T, world)[rank]
+    # the library's own plan (fl_shard_plan, used by fl_price_batch_multi)
+    # gives every rank the same shard
+    from paper_2303_02317_b200._native import shard_plan
+
+    assert np.array_equal(np.nonzero(shard_plan(b.kind, b.T, world) == rank)[0], idx)
     local = b.subset(idx)
     # stand-in for the per-option price: a function of the option alone
     price = local.S * 1e-3 + local.K + np.log2(local.T)

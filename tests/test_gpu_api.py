@@ -4,7 +4,7 @@ exported sub-operators) against golden vectors produced by the reference.
 Prices: |d| <= 1e-9 max(|ref|, K); rescaled put rows (values in [0, 1]) and
 call rows: |d| <= 1e-9 max(1, K); composed kernels: |d| <= 1e-12 max|W|
 (the reference's own FFT round-off is ~1e-16 max|W|); boundaries equal except
-a +-1 shift at a near-tie."""
+at a tie certified by the reference's own margins (conftest.boundary_check)."""
 
 from __future__ import annotations
 
@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, golden, price_close
+from conftest import GOLDEN, boundary_check, golden, price_close
 
 pytestmark = pytest.mark.gpu
 
@@ -69,9 +69,12 @@ def test_solve_bsm_trapezoid(ops):
         f, h = int(ops[f"pt{k}_f"]), int(ops[f"pt{k}_h"])
         kp, seg = _native.put_trapezoid(cd, cm, cu, ds, 128, f, ops[f"pt{k}_seg"], h)
         kp_ref, ref = int(ops[f"pt{k}_kp"]), ops[f"pt{k}_out"]
-        assert abs(kp - kp_ref) <= 1, (k, kp, kp_ref)
-        if kp == kp_ref:
-            assert _close_rows(seg, ref, 1.0), (k, np.max(np.abs(seg - ref)))
+        ok, _, why = boundary_check(2, 1.0, [0], [kp], [0], [kp_ref], ops[f"pt{k}_marg"][None, :])
+        assert ok, (k, why)
+        # rows cover columns kp+1 .. f+len-h: compare the columns both cover
+        d = kp - kp_ref
+        got, want = (seg[max(0, -d):], ref[max(0, d):])
+        assert _close_rows(got, want, 1.0), (k, np.max(np.abs(got - want)))
         # through the drop-in signature
         disc = fl.BsmDiscretization(0, 0.0, 0.0, 0.0, ds, 0, 0.4, cd, cm, cu)
         st = fl.PutRowState(int(ops[f"pt{k}_t"]), f, fl.GridRow(int(ops[f"pt{k}_t"]), f + 1, ops[f"pt{k}_seg"]))
@@ -104,9 +107,13 @@ def test_solve_trapezoid(ops):
         st = fl.solve_trapezoid(spec, prob)
         jp_ref, ref = int(ops[f"ct{k}_jp"]), ops[f"ct{k}_out"]
         assert st.time_index == i - h
-        assert abs(st.boundary - jp_ref) <= 1, (k, st.boundary, jp_ref)
-        if st.boundary == jp_ref:
-            assert _close_rows(st.segment.values, ref, max(1.0, K)), (k, np.max(np.abs(st.segment.values - ref)))
+        # first-green columns jp+1 (boundary_check's call convention)
+        ok, _, why = boundary_check(1, K, [0], [st.boundary + 1], [0], [jp_ref + 1], ops[f"ct{k}_marg"][None, :])
+        assert ok, (k, why)
+        # rows cover columns first_col .. jp: compare the columns both cover
+        m = min(st.boundary, jp_ref) + 1
+        got, want = st.segment.values[:m], ref[:m]
+        assert _close_rows(got, want, max(1.0, K)), (k, np.max(np.abs(got - want)))
 
 
 def test_single_spec_pricers_match_golden():

@@ -228,3 +228,65 @@ def test_model_frozen_constants():
     assert (d.omega, d.d_tau, d.d_s, d.k_star) == (2.4999999999999996, 1.9531250000000004e-05,
                                                   0.0069877124296868435, 0)
     assert (d.coef_down, d.coef_mid, d.coef_up) == (0.39790368627109396, 0.199951171875, 0.4020963137289061)
+
+
+def test_native_shard_plan_matches_python_lpt():
+    """fl_shard_plan (C++, behind fl_price_batch_multi) == shard.lpt_shards."""
+    from paper_2303_02317_b200._native import shard_plan
+    from paper_2303_02317_b200.shard import lpt_shards
+    from paper_2303_02317_b200.workloads import draw_config
+
+    b = draw_config(5, n=3000)
+    for k in (1, 2, 3, 4, 8):
+        owner = shard_plan(b.kind, b.T, k)
+        for r, idx in enumerate(lpt_shards(b.kind, b.T, k)):
+            assert np.array_equal(np.nonzero(owner == r)[0], idx), (k, r)
+
+
+def test_oracle_margins_match_reference_goldens():
+    """The oracle's boundary margins (tie evidence for boundary parity) are
+    bit-identical to the reference's own, recorded in the goldens."""
+    from conftest import golden
+    from oracle import port
+
+    for name in ("c3_fast", "c2_fast", "small_fast"):
+        g = golden(name)
+        for i in range(0, g.n, max(1, g.n // 12)):
+            if str(g.err_kind[i]) or g.kind[i] == 0:
+                continue
+            fn = port.put_fast if g.kind[i] == 2 else port.call_fast
+            _, t, c, m = fn(*g.args(i), margins=True)
+            tr, cr = g.boundary(i)
+            assert np.array_equal(t, tr) and np.array_equal(c, cr)
+            assert np.array_equal(m, g.margins(i), equal_nan=True), (name, i)
+
+
+def test_boundary_check_rules():
+    """conftest.boundary_check: equal records pass; a shift passes only over
+    cells the reference certifies as ties; later records are then free."""
+    from conftest import NMARG, boundary_check
+
+    t = np.array([0, 10, 20])
+    c = np.array([0, -5, -9])
+    marg = np.full((3, NMARG), 1e-3)
+    assert boundary_check(2, 100.0, t, c, t, c, marg)[0]
+    # put: device boundary one column right (cell -4 exercise on device) -> needs margin at d=+1
+    c2 = np.array([0, -4, -7])
+    assert not boundary_check(2, 100.0, t, c2, t, c, marg)[0]
+    marg[1, NMARG // 2 + 1] = 5e-10
+    ok, nt, _ = boundary_check(2, 100.0, t, c2, t, c, marg)
+    assert ok and nt == 1
+    # a shift of two needs both cells
+    c3 = np.array([0, -3, -9])
+    assert not boundary_check(2, 100.0, t, c3, t, c, marg)[0]
+    # no margin evidence (NaN) -> no slack
+    marg[1, :] = np.nan
+    assert not boundary_check(2, 100.0, t, c2, t, c, marg)[0]
+    # differing record times fail
+    assert not boundary_check(2, 100.0, np.array([0, 11, 20]), c, t, c, np.full((3, NMARG), 0.0))[0]
+    # call: margins in currency, tolerance 1e-9 K
+    mc = np.full((3, NMARG), 1e-3)
+    mc[1, NMARG // 2] = 5e-8  # |lin - green| at the reference's last continuation column
+    cc = np.array([5, 7, 9])
+    assert boundary_check(1, 100.0, t, np.array([5, 6, 9]), t, cc, mc)[0]
+    assert not boundary_check(1, 1.0, t, np.array([5, 6, 9]), t, cc, mc)[0]
