@@ -323,7 +323,7 @@ int upload(fl_batch* b, cudaStream_t stream) {
   for (int32_t o : b->o_euro_base) b->n_euro_base = std::max(b->n_euro_base, b->euro[o].n);
   // the global-memory fallback march needs a workspace row set per CTA; the
   // register-resident sweeps (fl_sweep.cu) need none
-  const int64_t cells_max = fl::sweep_max_cells();
+  const int64_t cells_max = fl::sweep_disabled() ? 0 : fl::sweep_max_cells();
   if (2 * b->n_put_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_put_base * 2 + 2);
   if (b->n_call_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_call_base + 2);
   if (b->n_euro_base + 1 > cells_max) nmax_base = std::max(nmax_base, b->n_euro_base + 2);

@@ -892,7 +892,7 @@ cudaError_t launch_call_grid(const CallParams& P, double* rows, uint8_t* masks, 
 cudaError_t launch_call_baseline(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                                  double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream) {
   if (nwork <= 0 || grid <= 0) return cudaSuccess;
-  if (n_max + 1 <= sweep_max_cells()) return launch_call_sweep(opts, order, nwork, n_max, grid, out, stream);
+  if (n_max + 1 <= sweep_max_cells() && !sweep_disabled()) return launch_call_sweep(opts, order, nwork, n_max, grid, out, stream);
   call_baseline_kernel<<<grid, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
   return cudaGetLastError();
 }

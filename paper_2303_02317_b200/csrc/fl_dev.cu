@@ -229,7 +229,9 @@ int dev_sizes(int64_t n, int64_t max_steps, int method, int64_t call_cutoff, int
                                           : max_steps;
   z.grid_base = (int)std::min<int64_t>(n, 4 * (int64_t)nsm);
   z.grid_euro = (int)std::min<int64_t>(n, 16 * (int64_t)nsm);
-  z.base_stride = (2 * z.base_steps + 1 > fl::sweep_max_cells()) ? 3 * (2 * z.base_steps + 2) + 16 : 0;
+  z.base_stride = (2 * z.base_steps + 1 > fl::sweep_max_cells() || fl::sweep_disabled())
+                      ? 3 * (2 * z.base_steps + 2) + 16
+                      : 0;
   size_t tmp = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs<unsigned long long, int32_t>(
       nullptr, tmp, (const unsigned long long*)nullptr, (unsigned long long*)nullptr, (const int32_t*)nullptr,

@@ -66,6 +66,7 @@ cudaError_t launch_euro_baseline(const EuroParams* opts, const int32_t* order, i
 
 // register-resident O(T^2) sweeps (fl_sweep.cu); rows of at most sweep_max_cells()
 int64_t sweep_max_cells();
+bool sweep_disabled();
 cudaError_t launch_put_sweep(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                              BatchOut out, cudaStream_t stream);
 cudaError_t launch_call_sweep(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,

@@ -24,6 +24,8 @@
 // reference (put exercise iff payoff >= lin, call continuation iff lin >=
 // exercise).  The exercise tables come from the device exp (<= 1 ulp from
 // numpy's), as in the round-1 kernels.
+#include <cstdlib>
+
 #include "fl_common.cuh"
 #include "fl_kernels.h"
 
@@ -235,6 +237,16 @@ inline int sweep_tile_for(int64_t cells) {
 }
 
 int64_t sweep_max_cells() { return kSweepMaxCells; }
+
+// FL_NO_SWEEP=1 (A/B tools only): route every baseline to the round-1
+// global-memory march
+bool sweep_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("FL_NO_SWEEP");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
 
 cudaError_t launch_put_sweep(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                              BatchOut out, cudaStream_t stream) {

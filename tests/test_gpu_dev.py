@@ -61,7 +61,9 @@ def test_dev_entry_matches_goldens(name):
     g = golden(name)
     idx = np.arange(g.n)
     k, S, K, R, Y, V, E, T = _tensors(g, idx)
-    price, status, bt, bc, bn = fl.price_batch_dev(k, S, K, R, Y, V, E, T, bnd_cap=128)
+    # fast records are short; options the reference dispatches to its baseline
+    # (T <= 2 * cutoff) record every row
+    price, status, bt, bc, bn = fl.price_batch_dev(k, S, K, R, Y, V, E, T, bnd_cap=300)
     torch.cuda.synchronize()
     _check(g, idx, price.cpu().numpy(), status.cpu().numpy(), bt.cpu().numpy(), bc.cpu().numpy(),
            bn.cpu().numpy())
