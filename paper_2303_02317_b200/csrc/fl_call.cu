@@ -17,17 +17,12 @@
 #include "fl_kernels.h"
 #include "fl_sched.cuh"
 #include "fl_strip.cuh"
+#include "fl_callstrip.cuh"
 #include "host_params.h"
 
 namespace fl {
 
 constexpr int CALL_LEAF = 32;
-#ifndef FL_CALL_UNROLL  // rows per unrolled step of the call leaf strip loop
-#define FL_CALL_UNROLL 2
-#endif
-#ifndef FL_CALL_LEAF_V2  // 2: call_leaf_v3 (shared e2 table, carried bases)
-#define FL_CALL_LEAF_V2 2
-#endif
 #ifndef FL_CALL_HS
 #define FL_CALL_HS 256
 #endif
@@ -61,137 +56,8 @@ __device__ __forceinline__ uint64_t call_ref_jump(int64_t L, int64_t M) {
   return 5ull * N * (uint64_t)lg + 3ull * N + 6ull;
 }
 
-// Leaf strip (binomial_strip_sweep with lo = j-h+1, height h <= 32) on the
-// chain warp: lane l holds column lo+l.  Reads in_org[lo..j], writes
-// out_org[lo..jp], returns jp.  Operation order as _accel.py:143-158
-// (unfused products and sums).
-__device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict__ in_org,
-                                  double* __restrict__ out_org, int64_t lo, int64_t top_row, int64_t j0,
-                                  int height, double* cells) {
-  const int lane = threadIdx.x & 31;
-  const int W = (int)(j0 - lo + 1);
-  const int64_t col = lo + lane;
-  double v = (lane < W) ? in_org[col] : 0.0;
-  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
-  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
-  // base(t) = S exp((2 lo - (top_row - t)) lu): lane t holds the parent base of step t
-  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
-  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
-  int64_t j = j0;
-  for (int s = 0; s < height; ++s) {
-    if (j < lo) break;
-    const int64_t child = top_row - s - 1;
-    const int64_t top = j < child ? j : child;
-    *cells += (double)(top - lo + 1);
-    const double bp = __shfl_sync(FULL, Bl, s);
-    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
-    const double right = __shfl_down_sync(FULL, v, 1);
-    int fg = INT32_MAX;
-    if (col <= top) {
-      const double vr = (col + 1 <= j) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);
-      const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
-      const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
-      if (lin >= grn) {
-        v = lin;
-      } else {
-        v = grn;
-        fg = lane;
-      }
-    }
-    fg = warp_min_i32(fg);
-    j = (fg == INT32_MAX) ? top : lo + fg - 1;
-  }
-  if (col <= j && lane < W) out_org[col] = v;
-  __syncwarp();
-  return j;
-}
-
-// call_leaf_warp without the per-row boundary reduction.  The call boundary
-// only moves left as rows descend (american.py:232-251 enforces it), so every
-// column right of the row's boundary is an exercise cell for the rest of the
-// strip: advancing all strip columns with the projected update
-// max(wd v + wu v', green) reproduces the analytic exercise values there
-// (lin < green strictly inside the exercise region), and the boundary is
-// needed only once, on the last row (first green by one warp min).  Cells
-// beyond the lattice edge (col > child) are never read by valid cells.  Same
-// operation order as _accel.py:143-158.
-__device__ int64_t call_leaf_v2(const CallParams& P, const double* __restrict__ in_org, double* __restrict__ out_org,
-                                int64_t lo, int64_t top_row, int64_t j0, int height, double* cells) {
-  const int lane = threadIdx.x & 31;
-  const int W = (int)(j0 - lo + 1);
-  const int64_t col = lo + lane;
-  double v = (lane < W) ? in_org[col] : 0.0;
-  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
-  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
-  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
-  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
-  bool green = false;
-  for (int s = 0; s < height; ++s) {
-    const double bp = __shfl_sync(FULL, Bl, s);
-    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
-    const double right = __shfl_down_sync(FULL, v, 1);
-    const double vr = (lane + 1 < W) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);  // right of j0: exercise
-    const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
-    const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
-    green = !(lin >= grn);
-    v = green ? grn : lin;
-  }
-  const int64_t child = top_row - height;  // last lattice column of the final row
-  const int64_t top = (j0 < child) ? j0 : child;
-  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
-  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
-  *cells += (double)W * height;
-  if (col <= jp && lane < W) out_org[col] = v;
-  __syncwarp();
-  return jp;
-}
-
-// call_leaf_v2 restructured for the warp's in-order issue: the e2 factors
-// come from a per-option shared table (same exp expressions as v2, computed
-// once per option instead of once per leaf), the parent base of row s+1 is
-// carried from row s (one broadcast shuffle per row), and every value that
-// does not depend on the row's neighbour exchange (the green value, the
-// out-of-strip right neighbour, wd v) is formed before the exchange lands.
-// Bit-identical to call_leaf_v2.
 constexpr int CALL_E2 = CHAIN_SCRATCH - 40;  // e2[k] = exp(2 k lu), k = 0..32, in the chain scratch
 static_assert(CALL_E2 >= CSUB_ASM2 + CALL_HS / 4 + 8, "e2 table above the call subtree scratch");
-__device__ int64_t call_leaf_v3(const CallParams& P, const double* __restrict__ in_org, double* __restrict__ out_org,
-                                int64_t lo, int64_t top_row, int64_t j0, int height, double* cells,
-                                const double* __restrict__ e2) {
-  const int lane = threadIdx.x & 31;
-  const int W = (int)(j0 - lo + 1);
-  const int64_t col = lo + lane;
-  double v = (lane < W) ? in_org[col] : 0.0;
-  const double e2_me = e2[lane], e2_nx = e2[lane + 1];
-  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
-  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
-  const bool edge = (lane + 1 >= W);  // right neighbour outside the strip: exercise value
-  double bp = __shfl_sync(FULL, Bl, 0);
-  bool green = false;
-  // unrolled by 2 only (instruction-cache footprint; C2 4.45 -> 4.30 ms, C5 630 -> 620 ms)
-  constexpr int kCallUnroll = FL_CALL_UNROLL;
-#pragma unroll kCallUnroll
-  for (int s = 0; s < height; ++s) {
-    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
-    const double right = __shfl_down_sync(FULL, v, 1);
-    const double ex_r = __dsub_rn(__dmul_rn(bp, e2_nx), P.K);
-    const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
-    const double a = __dmul_rn(P.wd, v);
-    const double vr = edge ? ex_r : right;
-    const double lin = __dadd_rn(a, __dmul_rn(P.wu, vr));
-    green = !(lin >= grn);
-    v = green ? grn : lin;
-    bp = bc;
-  }
-  const int64_t child = top_row - height;
-  const int64_t top = (j0 < child) ? j0 : child;
-  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
-  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
-  *cells += (double)W * height;
-  if (col <= jp && lane < W) out_org[col] = v;
-  __syncwarp();
-  return jp;
-}
 
 struct CallFrame {
   int64_t i, j, jm;
@@ -234,13 +100,7 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
                                              double* out_org, int64_t i, int64_t j, int h) {
   const long long t1 = clock64();
   double cells = 0.0;
-#if FL_CALL_LEAF_V2 == 2
   const int64_t jp = call_leaf_v3(P, in_org, out_org, j - h + 1, i, j, h, &cells, X.scratch + CALL_E2);
-#elif FL_CALL_LEAF_V2
-  const int64_t jp = call_leaf_v2(P, in_org, out_org, j - h + 1, i, j, h, &cells);
-#else
-  const int64_t jp = call_leaf_warp(P, in_org, out_org, j - h + 1, i, j, h, &cells);
-#endif
   if (X.acct) X.flops += 5ull * (uint64_t)cells;
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
@@ -279,7 +139,6 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   stk[0].i = i0; stk[0].j = j0; stk[0].h = h0; stk[0].in = s_in - lo0; stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
-#if FL_WALK_MERGE
   // one helper post site and one wait site (as put_subtree)
   while (sp > 0) {
     CallSubFrame& F = stk[sp - 1];
@@ -334,57 +193,6 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
     C.out = mid ? F.asmo : F.out;
     C.state = 0;
   }
-#else
-  while (sp > 0) {
-    CallSubFrame& F = stk[sp - 1];
-    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
-    const int ph = (sp >= 2) ? stk[sp - 2].h : ph0;
-    const int64_t lo = F.j - h + 1;
-    if (F.state == 0) {
-      call_ref_enter(X, h, ph);
-      if (h <= CALL_LEAF) {
-        ret = call_leaf(X, P, F.in, F.out, F.i, F.j, h);
-        --sp;
-        continue;
-      }
-      F.asmo = X.scratch + (sp == 1 ? CSUB_ASM0 : sp == 2 ? CSUB_ASM1 : CSUB_ASM2) - lo;
-      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
-      // mid (helper): cols lo .. j-h1 of row i-h1
-      F.tk = helper_post(*X.S, X.c, F.q, F.in + lo, F.asmo + lo, h2, wslot(*X.S, X.c, X.wst, sp, h1), h1 + 1, &F.tk0);
-      if (X.acct) X.flops += 2ull * (uint64_t)(h2 * (h1 + 1));
-      F.state = 1;
-      CallSubFrame& C = stk[sp++];
-      C.i = F.i; C.j = F.j; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
-    } else if (F.state == 1) {
-      const int64_t jm = ret;
-      if (jm < F.j - h1 || jm > F.j) { *err = FL_E_GEOMETRY | 1; return 0; }
-      F.jm = jm;
-      const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
-      twait += clock64() - tw;
-      const int64_t A = jm - lo + 1;  // assembled cols lo .. jm
-      call_ref_bottom(X, h, A);
-      F.tk = -1;
-      if (A > h2) {  // bottom (helper): cols lo .. jm-h2 of row i-h
-        F.tk = helper_post(*X.S, X.c, F.q, F.asmo + lo, F.out + lo, (int)(A - h2), wslot(*X.S, X.c, X.wst, sp, h2),
-                           h2 + 1, &F.tk0);
-        if (X.acct) X.flops += 2ull * (uint64_t)((A - h2) * (h2 + 1));
-      }
-      F.state = 2;
-      CallSubFrame& C = stk[sp++];
-      C.i = F.i - h1; C.j = jm; C.h = h2; C.in = F.asmo; C.out = F.out; C.state = 0;
-    } else {
-      const int64_t jp = ret;
-      if (jp < F.jm - h2 || jp > F.jm) { *err = FL_E_GEOMETRY | 2; return 0; }
-      if (F.tk >= 0) {
-        const long long tw = clock64();
-        helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
-        twait += clock64() - tw;
-      }
-      --sp;
-    }
-  }
-#endif
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_MID, twait);

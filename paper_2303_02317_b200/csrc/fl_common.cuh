@@ -39,26 +39,14 @@ __device__ __forceinline__ double2 tw_get(int m) { return __ldg(&fl_tw[m]); }
 // W_L^m = exp(-2 pi i m / L) for L a power of two <= TW_N.
 __device__ __forceinline__ double2 tw_l(int m, int log_l) { return tw_get(m << (TW_LOG - log_l)); }
 
-// Quarter-wave tables are stored bank-swizzled: entry i at position
-// twq_swz(i), the low three bits (the 16-byte bank group of a 128-byte row)
-// XORed with bits 3-5, 6-8 and 9-11.  FFT stages read W^(j << s) for
-// consecutive j, strides of 2^s entries that would all hit one bank group in
-// natural order; swizzled, any eight consecutive j of a stride 2^(3k) land on
-// eight bank groups.  A bijection on [0, TWQ).
-#ifndef FL_TW_SWZ
-#define FL_TW_SWZ 0  // measured neutral in the kernel (13.76 vs 13.92 ms; 1024: 49.9 vs 49.6 ms)
-#endif
-__host__ __device__ constexpr int twq_swz(int i) {
-  return FL_TW_SWZ ? (i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7)) : i;
-}
-// Global swizzled quarter-wave copy (kernels without a shared copy).
+// Global quarter-wave copy (kernels without a shared copy).
 __device__ double2 fl_twq[TWQ];
 
-// exp(-2 pi i m / TW_N), m in [0, TW_N), from a swizzled quarter-wave table
+// exp(-2 pi i m / TW_N), m in [0, TW_N), from a quarter-wave table
 // tq[0..TWQ) (shared memory or fl_twq): W^(m+TWQ) = -i W^m.
 __device__ __forceinline__ double2 twq(const double2* tq, int m) {
   // branch-free: lanes of a warp sit in different quadrants
-  const double2 b = tq[twq_swz(m & (TWQ - 1))];
+  const double2 b = tq[m & (TWQ - 1)];
   const int q = m >> (TW_LOG - 2);
   const double x = (q & 1) ? b.y : b.x;
   const double y = (q & 1) ? -b.x : b.y;

@@ -18,7 +18,7 @@ void init_twiddles(cudaStream_t stream) {
   }
   cudaMemcpyToSymbolAsync(fl_tw, h.data(), sizeof(double2) * TW_N, 0, cudaMemcpyHostToDevice, stream);
   std::vector<double2> q(TWQ);
-  for (int i = 0; i < TWQ; ++i) q[twq_swz(i)] = h[i];
+  for (int i = 0; i < TWQ; ++i) q[i] = h[i];
   cudaMemcpyToSymbolAsync(fl_twq, q.data(), sizeof(double2) * TWQ, 0, cudaMemcpyHostToDevice, stream);
   cudaStreamSynchronize(stream);
 }

@@ -38,18 +38,9 @@ namespace fl {
 #define FL_PUT_LEAF 64
 #endif
 constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
-#ifndef FL_STRIP_PIPE  // 1: leaf strips with the software-pipelined neighbour exchange
-#define FL_STRIP_PIPE 1
-#endif
 constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
-#ifndef FL_STRIP_SLIDE  // 1: sliding-frame leaf strips (put_strip_slide) for options with the exercise margin
-#define FL_STRIP_SLIDE 1
-#endif
-#ifndef FL_STRIP_GHOST  // 1: the sliding frame with a ghost lane of exercise cells (no selects after shuffles)
-#define FL_STRIP_GHOST 1
-#endif
-constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 31 - FL_STRIP_GHOST) / (32 - FL_STRIP_GHOST);  // cells per lane
-constexpr int PUT_SLIDE_H = ((32 - FL_STRIP_GHOST) * PUT_SLIDE_CPL - 2) / 2;  // tallest strip the frame holds
+constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 30) / 31;  // cells per lane (lane 0 is the ghost lane)
+constexpr int PUT_SLIDE_H = (31 * PUT_SLIDE_CPL - 2) / 2;      // tallest strip the frame holds
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
 #endif
@@ -151,18 +142,15 @@ struct PutChainCtx {
 // Reference cost of a recursion node of height h whose parent has height ph:
 // the reference strips it whole if h <= cutoff (and its parent did not), else
 // it issues the mid jump here and the bottom jump once km is known.
-#ifndef FL_ABL
-#define FL_ABL 0
-#endif
 template <bool ACCT = true>
 __device__ __forceinline__ void ref_node_enter(PutChainCtx& X, int h, int ph) {
-  if (FL_ABL || !ACCT || !X.acct) return;
+  if (!ACCT || !X.acct) return;
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(2 * (int64_t)h, 2 * (int64_t)((h + 1) / 2) + 1);
   else if (ph > X.ref_cut) X.ref_flops += ref_strip_flops(4 * (int64_t)h + 2, h);
 }
 template <bool ACCT = true>
 __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A) {
-  if (FL_ABL || !ACCT || !X.acct) return;
+  if (!ACCT || !X.acct) return;
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
 }
 
@@ -178,26 +166,13 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   const long long t1 = clock64();
   long long tm[2] = {0, 0};
   FL_TR(*X.S, X.c, EV_LEAF_B, height);
-#if FL_STRIP_SLIDE
   // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
   const int64_t kb =
       (SL == 1 || (SL < 0 && P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height))
-#if FL_STRIP_GHOST
           ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
                                               FL_PROFP(X.prof) ? tm : nullptr)
-#else
-          ? put_strip_slide<PUT_SLIDE_CPL, 1>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
-                                              FL_PROFP(X.prof) ? tm : nullptr)
-#endif
           : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
                                     FL_PROFP(X.prof) ? tm : nullptr);
-#elif FL_STRIP_PIPE
-  const int64_t kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                             FL_PROFP(X.prof) ? tm : nullptr);
-#else
-  const int64_t kb = put_strip_warp<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                             FL_PROFP(X.prof) ? tm : nullptr);
-#endif
   FL_TR(*X.S, X.c, EV_LEAF_E, height);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
@@ -205,7 +180,7 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
     prof_add(FL_PROFP(X.prof), PROF_STRIP_LOOP, tm[1]);
     prof_add(FL_PROFP(X.prof), PROF_LEAF_LOAD, tm[0] - t1);
   }
-  if (!FL_ABL && ACCT && X.acct) X.flops += ref_strip_flops(hi - lo + 1, height);
+  if (ACCT && X.acct) X.flops += ref_strip_flops(hi - lo + 1, height);
   FL_TR(*X.S, X.c, EV_MARK, 1);
   return kb;
 }
@@ -267,7 +242,6 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   stk[0].f = f0; stk[0].h = h0; stk[0].in = s_in - (f0 + 1); stk[0].out = out_org; stk[0].state = 0;
   int sp = 1;
   int64_t ret = 0;
-#if FL_WALK_MERGE
   // one helper post site and one wait site (the walk runs for every 256 rows:
   // its code footprint counts, see profiles/r01_experiments.md)
   while (sp > 0) {
@@ -315,7 +289,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     const long long tp = clock64();
     F.tk = helper_post(*X.S, X.c, F.q, xj, yj, Lj, wslot(*X.S, X.c, X.wst, sp, m), Mj, &F.tk0);
     tpost += clock64() - tp;
-    if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lj * Mj);
+    if (ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lj * Mj);
     F.state = mid ? 1 : 2;
     SubFrame& C = stk[sp++];
     C.f = mid ? F.f : km;
@@ -324,65 +298,6 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     C.out = mid ? F.asmo : F.out;
     C.state = 0;
   }
-#else
-  while (sp > 0) {
-    SubFrame& F = stk[sp - 1];
-    const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
-    const int ph = (sp >= 2) ? stk[sp - 2].h : ph0;
-    FL_TR(*X.S, X.c, EV_MARK, 3);
-    if (F.state == 0) {
-      ref_node_enter(X, h, ph);
-      FL_TR(*X.S, X.c, EV_MARK, 4);
-      if (h <= PUT_LEAF) {
-        const int64_t kb = put_leaf<ACCT, SL>(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
-        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
-        ret = kb;
-        --sp;
-        FL_TR(*X.S, X.c, EV_MARK, 2);
-        continue;
-      }
-      F.asmo = X.scratch + (sp == 1 ? SUB_ASM0 : sp == 2 ? SUB_ASM1 : SUB_ASM2) - (F.f - h1 + 1);
-      F.q = (sp == 1) ? 1 : 0;  // the subtree root's jumps have the most slack: background ring
-      // mid (helper): cols f+h1+1 .. f+2h-h1 of row t+h1, overlapping the first child
-      const int Lmid = 2 * (h - h1), Mmid = 2 * h1 + 1;
-      const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.in + F.f + 1, F.asmo + F.f + h1 + 1, Lmid, wslot(*X.S, X.c, X.wst, sp, h1), Mmid,
-                         &F.tk0);
-      tpost += clock64() - tp;
-      if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lmid * Mmid);
-      F.state = 1;
-      SubFrame& C = stk[sp++];
-      C.f = F.f; C.h = h1; C.in = F.in; C.out = F.asmo; C.state = 0;
-    } else if (F.state == 1) {
-      const int64_t km = ret;
-      if (km < F.f - h1 || km > F.f) { *err = FL_E_GEOMETRY | 2; return 0; }
-      F.km = km;
-      FL_TR(*X.S, X.c, EV_MARK, 5);
-      const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
-      twait += clock64() - tw;
-      // bottom (helper): cols km+h2+1 .. f+h of row t+h, from assembled cols km+1 .. f+2h-h1
-      const int64_t A = F.f + 2 * (int64_t)h - h1 - km;
-      ref_node_bottom<ACCT>(X, h, A);
-      const int Lbot = (int)(A - 2 * h2), Mbot = 2 * h2 + 1;
-      const long long tp = clock64();
-      F.tk = helper_post(*X.S, X.c, F.q, F.asmo + km + 1, F.out + km + h2 + 1, Lbot, wslot(*X.S, X.c, X.wst, sp, h2), Mbot,
-                         &F.tk0);
-      tpost += clock64() - tp;
-      if (!FL_ABL && ACCT && X.acct) X.flops += 2ull * (uint64_t)(Lbot * Mbot);
-      F.state = 2;
-      SubFrame& C = stk[sp++];
-      C.f = km; C.h = h2; C.in = F.asmo; C.out = F.out; C.state = 0;
-    } else {
-      const int64_t kp = ret;
-      if (kp < F.km - h2 || kp > F.km) { *err = FL_E_GEOMETRY | 3; return 0; }
-      const long long tw = clock64();
-      helper_wait_range(*X.S, X.c, F.q, F.tk0, F.tk);
-      twait += clock64() - tw;
-      --sp;
-    }
-  }
-#endif
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_STAGE, t2 - t1);
@@ -418,7 +333,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     FL_TR(*X.S, X.c, EV_NODE, h * 4 + F.state);
     if (F.state == 0) {
       if (h <= PUT_HS) {
-        ret = (FL_STRIP_SLIDE && P.slide && PUT_LEAF <= PUT_SLIDE_H)
+        ret = (P.slide && PUT_LEAF <= PUT_SLIDE_H)
                   ? put_subtree<ACCT, 1>(X, P, F.f, F.in_org, F.out_org, h, ph, err)
                   : put_subtree<ACCT, 0>(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;

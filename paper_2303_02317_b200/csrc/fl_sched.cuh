@@ -40,25 +40,6 @@ namespace fl {
 //                subtrees, fed through a request ring (no deps scan)
 // Groups execute one task at a time over 128 threads (named barriers 1, 2).
 // (Isolating the chains on SMSPs of their own was measured: no gain.)
-#ifndef FL_DEDUP  // 1: the chain's big, rarely-hot helpers are real calls (one copy in the kernel, fewer i-cache misses)
-#define FL_DEDUP 0  // measured: the calls add spills, 15.4 -> 17.4 ms
-#endif
-#if FL_DEDUP
-#define FL_COLD __noinline__
-#else
-#define FL_COLD
-#endif
-#ifndef FL_COLD_INIT  // 1: once-per-option setup / teardown helpers are real calls (out of the hot code)
-#define FL_COLD_INIT 0
-#endif
-#if FL_COLD_INIT || FL_DEDUP
-#define FL_COLD1 __noinline__
-#else
-#define FL_COLD1
-#endif
-#ifndef FL_WALK_MERGE  // 1: subtree walks with one helper-post and one helper-wait site (smaller hot loop)
-#define FL_WALK_MERGE 1
-#endif
 #ifndef FL_PROF  // 1: scheduler profile counters (FL_PROFILE=1 at run time); tool builds only --
 #define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
 #endif
@@ -72,32 +53,12 @@ constexpr int GROUP_WARPS = 4;
 constexpr int GROUP_THREADS = 32 * GROUP_WARPS;
 constexpr int BIG_WARPS = GROUP_WARPS;
 constexpr int BIG_THREADS = GROUP_THREADS;
-#ifndef FL_LAYOUT
-#define FL_LAYOUT 4
-#endif
 // layout 4 keeps two warp slots idle so the chains' SMSP holds nothing else
-constexpr int IDLE_WARPS = (FL_LAYOUT == 4 || FL_LAYOUT == 5) ? 2 : 0;
+constexpr int IDLE_WARPS = 2;
 constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP) + IDLE_WARPS;
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
 enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3, ROLE_IDLE = 4 };
 __device__ __forceinline__ int warp_role(int w, int* rank) {
-#if FL_LAYOUT == 5
-  // each chain on its own SMSP (2 / 3) with two medium-group warps; the big
-  // group and the helpers (two per chain) on SMSPs 0 / 1; warps 14, 15 idle
-  static_assert(NCHAIN == 2 && NHELP == 2 && SCHED_WARPS == 16, "layout 5 shape");
-  const int smsp = w & 3, slot = w >> 2;
-  if (smsp >= 2) {
-    if (slot == 0) { *rank = smsp - 2; return ROLE_CHAIN; }
-    if (slot == 3) { *rank = 0; return ROLE_IDLE; }
-    *rank = (slot - 1) * 2 + (smsp - 2);
-    return ROLE_MED;
-  }
-  if (slot < 2) { *rank = slot * 2 + smsp; return ROLE_BIG; }
-  // helpers: SMSP 0 serves chain 0, SMSP 1 chain 1
-  *rank = smsp * NHELP + (slot - 2);
-  return ROLE_HELPER;
-#endif
-#if FL_LAYOUT == 4
   // The chains' leaf strips exchange neighbours by shuffle every row, and a
   // shuffle waits behind every shared-memory access queued on its SMSP's MIO
   // path (measured, tools/strip_noise_bench.cu: 68 cycles/row alone, 148 with
@@ -118,46 +79,6 @@ __device__ __forceinline__ int warp_role(int w, int* rank) {
   constexpr int kRank[12] = {0, 1, 2, 3, 0, 1, 2, 3, 0, NHELP + 0, 1, NHELP + 1};
   *rank = kRank[slot];
   return kRole[slot];
-#endif
-#if FL_LAYOUT == 1
-  // SMSP-aware: SMSP 0 / 1 hold one chain each plus the OTHER chain's helpers
-  // (a chain and its own helpers never compete for one issue port), the FFT
-  // groups (steady issuers) live on SMSP 2 / 3
-  static_assert(NCHAIN == 2 && NHELP == 3 && SCHED_WARPS == 16, "layout 1 shape");
-  const int smsp = w & 3, slot = w >> 2;
-  if (smsp < 2) {
-    if (slot == 0) { *rank = smsp; return ROLE_CHAIN; }
-    *rank = (1 - smsp) * NHELP + (slot - 1);
-    return ROLE_HELPER;
-  }
-  if (slot < 2) { *rank = slot * 2 + (smsp - 2); return ROLE_BIG; }
-  *rank = (slot - 2) * 2 + (smsp - 2);
-  return ROLE_MED;
-#endif
-#if FL_LAYOUT == 2 || FL_LAYOUT == 3
-  // The SMSP issue arbiter serves the highest warp id first: the chains (the
-  // sequential critical path) take the top ids 14 / 15 (SMSP 2 / 3), so
-  // co-resident warps only get the issue slots a chain leaves free.  Each
-  // chain's helpers avoid its SMSP.  Layout 2: FFT groups lowest, helpers
-  // above them; layout 3: helpers lowest, FFT groups above them.
-  static_assert(NCHAIN == 2 && NHELP == 3 && SCHED_WARPS == 16, "layout 2/3 shape");
-  if (w >= 14) { *rank = w - 14; return ROLE_CHAIN; }
-#if FL_LAYOUT == 2
-  constexpr int HB = 8, BB = 0, MB = 4;
-#else
-  constexpr int HB = 0, BB = 6, MB = 10;
-#endif
-  if (w >= HB && w < HB + 6) {
-    // helper warps HB..HB+5 sit on SMSPs 0,1,2,3,0,1: the SMSP-2 warp serves
-    // chain 1, the SMSP-3 warp chain 0, the rest alternate
-    constexpr int kRank[6] = {0, 1, NHELP + 0, 2, NHELP + 1, NHELP + 2};
-    *rank = kRank[w - HB];
-    return ROLE_HELPER;
-  }
-  if (w >= BB && w < BB + 4) { *rank = w - BB; return ROLE_BIG; }
-  *rank = w - MB;
-  return ROLE_MED;
-#endif
   constexpr int C0 = 2 * GROUP_WARPS, H0 = C0 + NCHAIN;
   if (w >= H0) { *rank = w - H0; return ROLE_HELPER; }  // helper rank: chain = rank / NHELP
   if (w >= C0) { *rank = w - C0; return ROLE_CHAIN; }
@@ -196,20 +117,8 @@ constexpr int NRINGS = 3;
 #ifndef FL_SMALL_MW  // FFT jumps with a window <= FL_SMALL_MW go to the medium group
 #define FL_SMALL_MW 600
 #endif
-#ifndef FL_POST_FENCE  // 1: CTA fences around helper posts (0: in-order shared stores + compiler barrier)
-#define FL_POST_FENCE 1
-#endif
-#ifndef FL_CONV_PAIRS  // helper correlation: 1 two outputs / lane, 2 register-blocked 8 x 4, 3 blocked + weights in registers
-#define FL_CONV_PAIRS 2
-#endif
-#ifndef FL_STEAL  // 1: the big FFT group also takes small-ring tasks after its own rings (2: before RING_LOW)
-#define FL_STEAL 1
-#endif
 #ifndef FL_IDLE_NS  // longest back-off sleep of an idle worker poll
 #define FL_IDLE_NS 2048
-#endif
-#ifndef FL_HELPER_GAP  // ns a helper pauses after each background (subtree-root) chunk (0: none)
-#define FL_HELPER_GAP 0
 #endif
 #ifndef FL_HELPER_NS  // longest back-off sleep of an idle helper poll
 #define FL_HELPER_NS 512
@@ -223,14 +132,11 @@ constexpr int DIRECT_H = FL_DIRECT_H;  // direct-correlation TASKS for kernels u
 #endif
 constexpr int KT_H = FL_KT_H;
 static_assert(KT_H >= DIRECT_H, "direct tasks read the table");
-#ifndef FL_MED_WARPS  // 1: the medium group is four independent single-warp workers on RING_SMALL
-#define FL_MED_WARPS 0  // measured: 14.6 -> 16.6 ms (1-warp blocks of 1024 points: longer tasks, more blocks)
-#endif
 constexpr int BIG_LOGN = 13;                     // big-group FFT blocks <= 8192 real points
-constexpr int SMALL_LOGN = FL_MED_WARPS ? 10 : 12;  // small-ring FFT blocks <= 1024 (4096) real points
+constexpr int SMALL_LOGN = 12;  // small-ring FFT blocks <= 4096 real points
 constexpr int BIG_SLOTS = smem_complex_slots(1 << (BIG_LOGN - 1));
 constexpr int MED_WSLOTS = smem_complex_slots(1 << (SMALL_LOGN - 1));  // one small-ring worker's buffer
-constexpr int SMALL_SLOTS = FL_MED_WARPS ? 4 * MED_WSLOTS : MED_WSLOTS;  // the medium group's buffers
+constexpr int SMALL_SLOTS = MED_WSLOTS;  // the medium group's buffer
 constexpr int NDEP = 6;
 
 enum : int {
@@ -396,9 +302,7 @@ __device__ __forceinline__ int helper_post(SchedShared& S, int c, int q, const d
   const int lane = lane_id();
   // the slots' previous occupants (t - HQ) must be finished
   while (__any_sync(0xffffffffu, lane < n && m.done[(t0 + lane) % HQ] < t0 + lane - HQ)) __nanosleep(16);
-#if FL_POST_FENCE
   __threadfence_block();  // every lane's writes to x (shared) ...
-#endif
   if (lane < n) {
     HReq& r = m.q[(t0 + lane) % HQ];
     const int k0 = lane * HCHUNK;
@@ -406,11 +310,7 @@ __device__ __forceinline__ int helper_post(SchedShared& S, int c, int q, const d
   }
   __syncwarp();           // ... and the requests are written before lane 0 publishes
   if (lane == 0) {
-#if FL_POST_FENCE
     __threadfence_block();
-#else
-    asm volatile("" ::: "memory");
-#endif
     m.seq = tl;
   }
   __syncwarp();
@@ -434,7 +334,7 @@ __device__ __forceinline__ void warp_wait_done(const SchedShared& S, int id) {
 
 // The chain's unfinished tasks conflicting with the given ranges, in issue
 // order, into out[0..min(n,cap)); returns n.
-__device__ FL_COLD int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+__device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                               uintptr_t w0, uintptr_t w1, int* out, int cap, int* rawf = nullptr) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
@@ -468,7 +368,7 @@ __device__ FL_COLD int scan_conflicts(const SchedShared& S, int c, uintptr_t r0,
 
 // Chain c waits for its unfinished tasks that conflict with a region it is
 // about to read (r0/r1, r2/r3) and write (w0/w1).
-__device__ FL_COLD void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+__device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                                uintptr_t w0, uintptr_t w1) {
   int* ids = S.cw_ids[c];
   int* rawf = S.cw_raw[c];
@@ -511,7 +411,7 @@ __device__ FL_COLD void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uint
 
 // Issue a task from chain warp `c` (all 32 lanes call).  Returns its id.
 // rlo/rhi: read range; wlo/whi: write range.
-__device__ FL_COLD int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
+__device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
                      uintptr_t whi) {
   int* deps = S.cw_deps[c];
   int nd;
@@ -564,7 +464,7 @@ __device__ FL_COLD int issue(SchedShared& S, int c, int ring, const Task& t, uin
 }
 
 // Chain c waits for all of its issued tasks.
-__device__ FL_COLD1 void wait_all_own(SchedShared& S, int c) {
+__device__ void wait_all_own(SchedShared& S, int c) {
   const int np = S.npend[c];
   const int first = np > PEND_CAP ? np - PEND_CAP : 0;
   for (int i = first; i < np; ++i) warp_wait_done(S, S.pend[c][i % PEND_CAP].id);
@@ -595,7 +495,7 @@ __device__ __forceinline__ int wst_sz(int d) { return d == 1 ? WST_SZ1 : d == 2 
 constexpr int64_t KTABLE_DOUBLES = (int64_t)(KT_H + 2) * (KT_H + 2) * 2;
 
 // scratch: 2*(2*DIRECT_H+2) doubles of shared memory owned by the calling warp.
-__device__ FL_COLD1 void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
+__device__ void build_kernel_table(double* kc, const Stencil& st, double* scratch) {
   const int lane = lane_id();
   const int span = st.span;
   double* a = scratch;
@@ -895,31 +795,15 @@ __device__ __forceinline__ void conv_direct_reg(const double* __restrict__ x, do
 
 __device__ double warp_conv_direct(const double* __restrict__ x, double* __restrict__ y, int64_t Lout,
                                    const double* __restrict__ w, int M) {
-#if FL_CONV_PAIRS == 3
-  for (int64_t k0 = 0; k0 < Lout; k0 += 64)
-    conv_direct_reg(x + k0, y + k0, (Lout - k0 < 64) ? (int)(Lout - k0) : 64, w, M);
-  __syncwarp();
-  return 2.0 * (double)Lout * (double)M;
-#endif
-#if FL_CONV_PAIRS == 2
   for (int64_t k0 = 0; k0 < Lout; k0 += 64)
     conv_direct_blk(x + k0, y + k0, (Lout - k0 < 64) ? (int)(Lout - k0) : 64, w, M);
   __syncwarp();
   return 2.0 * (double)Lout * (double)M;
-#endif
-#if FL_CONV_PAIRS == 4
-  for (int64_t k0 = 0; k0 < Lout; k0 += 64)
-    conv_direct_blk_cf(x + k0, y + k0, (Lout - k0 < 64) ? (int)(Lout - k0) : 64, w, M);
-  __syncwarp();
-  return 2.0 * (double)Lout * (double)M;
-#endif
-#if FL_CONV_PAIRS
   if (Lout <= 64) {
     conv_direct_pairs(x, y, (int)Lout, w, M);
     __syncwarp();
     return 2.0 * (double)Lout * (double)M;
   }
-#endif
   int64_t k0 = 0;
   for (; Lout - k0 > 64; k0 += 128) conv_direct_pass<4>(x, y, k0, Lout, w, M);
   if (Lout - k0 > 32) conv_direct_pass<2>(x, y, k0, Lout, w, M);
@@ -959,7 +843,7 @@ __device__ __forceinline__ void warp_stage(double* dst, const double* src, int n
 
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
 // or an FFT task, on the small or big ring.
-__device__ FL_COLD void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
+__device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
                            int64_t Lout, int h, const double* kc, unsigned long long* prof, bool low = false) {
   if (Lout <= 0) return;
   Task t;
@@ -1026,7 +910,7 @@ __device__ __forceinline__ void publish_done(SchedShared& S, int ring, int idx) 
 // depth d-1 correlates with W_m of its children's heights m (depth d), two
 // consecutive values per depth.  Slots are reused while they cover the
 // subtree (consecutive subtrees mostly share heights).
-__device__ FL_COLD void stash_weights(SchedShared& S, int c, double* wst, const double* kc, int h0, int leaf, int span) {
+__device__ void stash_weights(SchedShared& S, int c, double* wst, const double* kc, int h0, int leaf, int span) {
   for (int d = 1; d <= 3; ++d) {
     const int pmax = (h0 + (1 << (d - 1)) - 1) >> (d - 1);  // tallest node at depth d-1
     if (pmax <= leaf) break;                                // depth d-1 is all leaves
@@ -1110,7 +994,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double2* bigbuf = tq + TWQ;              // big-group FFT buffer
   double2* medbuf = bigbuf + BIG_SLOTS;   // medium-group FFT buffer
   __shared__ int s_idx[2], s_ring[2];
-  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[twq_swz(i)] = fl_tw[i];
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
   sched_init(S);
   if (threadIdx.x == 0) S.prof = prof;
   __syncthreads();
@@ -1158,9 +1042,6 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
         prof_add(prof, PROF_HELP_CYC + q, clock64() - th);
         prof_add(prof, PROF_HELP_FMA, (unsigned long long)Lout * M);
       }
-#if FL_HELPER_GAP
-      if (q == 1) __nanosleep(FL_HELPER_GAP);  // background chunks: spread the shared-memory bursts
-#endif
     }
     if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
     return;
@@ -1218,62 +1099,11 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
       t.x = nullptr; t.y = nullptr; t.w = nullptr; t.L = t.Lout = 0;
       t.c0 = t.c1 = t.c2 = 0.0; t.h = 0; t.span = 0;
       t.i0 = t.i1 = t.i2 = 0; t.d0 = 0.0;
-      for (int k = 0; k < (FL_MED_WARPS ? GROUP_WARPS : 1); ++k) issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
+      issue(S, c, RING_SMALL, t, 0, 0, 0, 0);
       issue(S, c, RING_BIG, t, 0, 0, 0, 0);
     }
     return;
   }
-#if FL_MED_WARPS
-  if (role == ROLE_MED) {
-    // ---- small-ring worker: one warp per task (claims by CAS; the big group may
-    // steal too).  Every small-ring task runs with this one-warp plan whichever
-    // worker takes it, so its arithmetic does not depend on the schedule.
-    const Grp gw{lane_id(), 32, -1};
-    double2* wbuf = medbuf + rank * MED_WSLOTS;
-    double flops = 0.0;
-    for (;;) {
-      const long long t0 = clock64();
-      int idx = 0;
-      unsigned ns = 16;
-      for (;;) {
-        int got = 0, ii = 0;
-        if (lane_id() == 0) {
-          ii = *(volatile int*)&S.claim[RING_SMALL];
-          if (ii < *(volatile int*)&S.reserve[RING_SMALL]) {
-            const Task& sl = S.ring[RING_SMALL][ii % QCAP];
-            if (sl.seq == ii) {
-              __threadfence_block();
-              bool ready = true;
-              for (int d = 0; d < sl.ndep; ++d) ready = ready && task_done(S, sl.dep[d]);
-              if (ready && atomicCAS(&S.claim[RING_SMALL], ii, ii + 1) == ii) got = 1;
-            }
-          }
-        }
-        if (__shfl_sync(FULL, got, 0)) { idx = __shfl_sync(FULL, ii, 0); break; }
-        __nanosleep(ns);
-        ns = ns < FL_IDLE_NS ? 2 * ns : ns;
-      }
-      worker_wait_ready(S, RING_SMALL, idx);
-      const Task t = load_task(S.ring[RING_SMALL][idx % QCAP]);
-      const long long t1 = clock64();
-      if (lane_id() == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
-      if (t.kind == TK_EXIT) break;
-      const double fl = pr.exec(S, t, wbuf, MED_WSLOTS, SMALL_LOGN, tq, gw);
-      flops += fl > 0 ? fl : 0.0;
-      __syncwarp();
-      if (lane_id() == 0) {
-        publish_done(S, RING_SMALL, idx);
-        if (FL_PROFP(prof)) {
-          const int ps = (t.kind == TK_FFT) ? PROF_FFT_CYC : (t.kind == TK_DIRECT) ? PROF_DIR_CYC : PROF_OTHER_CYC;
-          prof_add(prof, ps, clock64() - t1);
-          prof_add(prof, ps + 1, 1);
-        }
-      }
-    }
-    if (lane_id() == 0 && flops_out) atomicAdd(flops_out, (unsigned long long)flops);
-    return;
-  }
-#endif
   // ---- FFT groups: one task at a time over 128 threads; each group is the
   // only consumer of its rings (the big group: RING_BIG, then RING_LOW; the
   // medium group: RING_SMALL), so claims need no atomics
@@ -1284,17 +1114,12 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   double2* buf = gi == 0 ? bigbuf : medbuf;
   const int slots = gi == 0 ? BIG_SLOTS : SMALL_SLOTS;
   const int logN = gi == 0 ? BIG_LOGN : SMALL_LOGN;
-  // claim order: the big group RING_BIG, RING_LOW (and with FL_STEAL the
-  // medium group's RING_SMALL: idle big-group time absorbs small-ring queueing);
+  // claim order: the big group RING_BIG, RING_LOW, then the medium group's
+  // RING_SMALL (idle big-group time absorbs small-ring queueing);
   // the medium group RING_SMALL only
   const int r_hi = gi == 0 ? RING_BIG : RING_SMALL;
-#if FL_STEAL == 2
-  const int r_2 = gi == 0 ? RING_SMALL : -1;
-  const int r_3 = gi == 0 ? RING_LOW : -1;
-#else
   const int r_2 = gi == 0 ? RING_LOW : -1;
-  const int r_3 = (gi == 0 && FL_STEAL) ? RING_SMALL : -1;
-#endif
+  const int r_3 = gi == 0 ? RING_SMALL : -1;
   constexpr int NCLAIM = 3;
   for (;;) {
     const long long t0 = clock64();
@@ -1320,7 +1145,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
             bool ready = true;
             for (int d = 0; d < sl.ndep; ++d) ready = ready && task_done(S, sl.dep[d]);
             if (!ready) continue;
-            if (rr == RING_SMALL && FL_STEAL) {  // two consumers: claim by CAS
+            if (rr == RING_SMALL) {  // two consumers: claim by CAS
               if (atomicCAS(&S.claim[rr], ii, ii + 1) == ii) { r = rr; i = ii; }
             } else {
               r = rr;
@@ -1346,14 +1171,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     // a stolen small-ring task runs with the medium group's block plan (same
     // arithmetic whichever group executes it)
     const bool stolen = (gi == 0 && tring == RING_SMALL);
-#if FL_MED_WARPS
-    // a stolen small-ring task runs on the group's first warp with the workers' one-warp plan
-    double fl = 0.0;
-    if (!stolen) fl = pr.exec(S, t, buf, slots, logN, tq, g);
-    else if (rank == 0) fl = pr.exec(S, t, buf, MED_WSLOTS, SMALL_LOGN, tq, Grp{lane_id(), 32, -1});
-#else
     const double fl = pr.exec(S, t, buf, stolen ? SMALL_SLOTS : slots, stolen ? SMALL_LOGN : logN, tq, g);
-#endif
     flops += fl > 0 ? fl : 0.0;
     gsync(g);
     if (g.t == 0) {

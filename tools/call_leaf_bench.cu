@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cmath>
 #include "fl_lib.cu"
+#include "strip_variants.cuh"
 using namespace fl;
 template <int MODE>
 __global__ void k(const CallParams P, const double* in, double* out, double* e2, long long* cyc, int reps, int height) {

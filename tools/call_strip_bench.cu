@@ -1,0 +1,119 @@
+// Call leaf strip: call_leaf_v3 (one neighbour exchange per row) vs
+// call_leaf_tiled<K> (one per K rows): identical outputs, cycles/row alone and
+// under the in-kernel kinds of co-resident load.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+#include "strip_variants.cuh"
+using namespace fl;
+
+struct Setup { CallParams P; long long lo, top, j0; int h; };
+
+template <int V>
+__device__ __forceinline__ long long strip(const CallParams& P, const double* in, double* out, long long lo,
+                                           long long top, long long j0, int h, const double* e2) {
+  double cells = 0;
+  if (V == 0) return call_leaf_v3(P, in, out, lo, top, j0, h, &cells, e2);
+  if (V == 2) return call_leaf_tiled<2>(P, in, out, lo, top, j0, h, &cells, e2);
+  return call_leaf_v3(P, in, out, lo, top, j0, h, &cells, e2);
+}
+
+template <int V, int NOISE>
+__global__ void __launch_bounds__(512, 1) k(Setup su, const double* in, long long* cyc, double* outg, int reps,
+                                           volatile int* stop) {
+  __shared__ double sin_[64], sout[64], sout2[64], se2[48], sn[2048];
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) { sin_[i] = in[i]; sout[i] = 0; sout2[i] = 0; }
+  for (int i = threadIdx.x; i < 48; i += blockDim.x) se2[i] = exp(2.0 * (double)i * su.P.lu);
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sn[i] = i;
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* inb = sin_ - su.lo;
+  if (w == 0) {
+    long long t0 = clock64();
+    long long acc = 0;
+    for (int r = 0; r < reps; ++r) acc += strip<V>(su.P, inb, sout - su.lo, su.lo, su.top, su.j0, su.h, se2);
+    long long t1 = clock64();
+    for (int i = lane; i < 64; i += 32) outg[i] = sout[i];
+    if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = acc; *stop = 1; }
+    return;
+  }
+  if (NOISE == 0) return;
+  if (NOISE == 1 && !(w == 1 || w == 2 || w == 3)) return;
+  if (NOISE == 2 && w != 4) return;
+  double x = lane;
+  int i = lane;
+  while (!*stop) {
+    if (NOISE == 1) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) { x += sn[(lane + j * 32 + i) & 2047]; i += 64; }
+    } else {
+      strip<V>(su.P, inb, sout2 - su.lo, su.lo, su.top, su.j0, su.h, se2);
+    }
+  }
+  if (x == 12345.0) cyc[2] = 1;
+}
+
+int main() {
+  // an American call lattice (american.py conventions), marched on the host to row i
+  const double S = 100, K = 90, R = 0.03, Y = 0.07, V = 0.25, E = 365;
+  const int T = 600;
+  const double dt = E / (365.0 * T), lu = V * sqrt(dt), up = exp(lu), down = 1 / up;
+  const double p = (exp((R - Y) * dt) - down) / (up - down), disc = exp(-R * dt);
+  const double wd = disc * (1 - p), wu = disc * p;
+  std::vector<double> v(T + 1);
+  for (int j = 0; j <= T; ++j) { double x = S * exp((2.0 * j - T) * lu) - K; v[j] = x > 0 ? x : 0; }
+  int i = T, jb = -1;
+  for (i = T - 1; i >= 300; --i) {
+    jb = -1;
+    double sc = S * exp((double)(T - i) * lu);
+    int fg = -1;
+    for (int j = 0; j <= i; ++j) {
+      double lin = wd * v[j] + wu * v[j + 1];
+      double grn = sc * exp((2.0 * j - T) * lu) - K;
+      if (lin >= grn) v[j] = lin; else { v[j] = grn; if (fg < 0) fg = j; }
+    }
+    jb = fg - 1;
+  }
+  const int row = 300;
+  Setup su;
+  su.P.S = S; su.P.K = K; su.P.wd = wd; su.P.wu = wu; su.P.lu = lu; su.P.n = T;
+  su.top = row; su.j0 = jb;
+  std::vector<double> in(64, 0.0);
+  double *d_in, *d_out; long long* c; int* stop;
+  cudaMalloc(&d_in, 8 * 64); cudaMalloc(&d_out, 8 * 64); cudaMalloc(&c, 32); cudaMalloc(&stop, 4);
+  const char* names[] = {"alone", "shared loads, other SMSPs", "2nd strip, same SMSP"};
+  for (int h : {32, 31, 17}) {
+    su.h = h;
+    su.lo = jb - h + 1;
+    for (int q = 0; q < h; ++q) in[q] = v[su.lo + q];
+    cudaMemcpy(d_in, in.data(), 8 * 64, cudaMemcpyHostToDevice);
+    std::vector<double> o[3];
+    long long kb[3];
+    for (int noise = 0; noise < 3; ++noise) {
+      double cy[3];
+      for (int var = 0; var < 3; ++var) {
+        for (int rep = 0; rep < 2; ++rep) {
+          cudaMemset(stop, 0, 4);
+          const int reps = rep ? 400 : 2;
+#define L(VV, NN) if (var == (VV == 0 ? 0 : VV == 2 ? 1 : 2) && noise == NN) k<VV, NN><<<1, 512>>>(su, d_in, c, d_out, reps, stop);
+          L(0, 0) L(0, 1) L(0, 2) L(2, 0) L(2, 1) L(2, 2) L(4, 0) L(4, 1) L(4, 2)
+          cudaDeviceSynchronize();
+        }
+        long long hh[2];
+        cudaMemcpy(hh, c, 16, cudaMemcpyDeviceToHost);
+        cy[var] = hh[0] / (400.0 * h);
+        if (noise == 0) {
+          kb[var] = hh[1] / 400;
+          o[var].resize(64);
+          cudaMemcpy(o[var].data(), d_out, 8 * 64, cudaMemcpyDeviceToHost);
+        }
+      }
+      printf("h=%d %-28s v3 %.1f  tiled2 %.1f  tiled4 %.1f cycles/row (%s)\n", h, names[noise], cy[0], cy[1], cy[2],
+             cudaGetErrorString(cudaGetLastError()));
+    }
+    bool same = kb[0] == kb[1] && kb[0] == kb[2];
+    for (int q = 0; q < 64; ++q) same = same && o[0][q] == o[1][q] && o[0][q] == o[2][q];
+    printf("h=%d outputs bit-identical: %s (jp %lld %lld %lld)\n", h, same ? "yes" : "NO", kb[0], kb[1], kb[2]);
+  }
+  return 0;
+}

@@ -1,7 +1,7 @@
 // Microbenchmark: put strip cycles/row while other warps hammer smem (mode 1) or DFMA (mode 2).
 #include <cstdio>
 #include "../paper_2303_02317_b200/csrc/fl_common.cuh"
-#include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+#include "strip_variants.cuh"
 #include "../paper_2303_02317_b200/csrc/fl_conv.cuh"
 
 using namespace fl;

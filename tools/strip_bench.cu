@@ -2,7 +2,7 @@
 #include <cstdio>
 #include <cmath>
 #include "../paper_2303_02317_b200/csrc/fl_common.cuh"
-#include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+#include "strip_variants.cuh"
 using namespace fl;
 template <int MODE>
 __global__ void k(double* in, double* out, double* pay, long long* cyc, int reps, int height) {

@@ -6,7 +6,7 @@
 #include <vector>
 
 #include "../paper_2303_02317_b200/csrc/fl_common.cuh"
-#include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+#include "strip_variants.cuh"
 using namespace fl;
 
 constexpr int NC = 1201, C0 = -600;  // columns C0 .. C0+NC-1

@@ -1,0 +1,602 @@
+// tools/strip_variants.cuh -- leaf-strip variants that were measured and NOT
+// kept in the product (fl_strip.cuh / fl_callstrip.cuh hold the production
+// strips).  Used by the A/B microbenchmarks in tools/ only; results in
+// profiles/r01_experiments.md and profiles/r02_experiments.md.
+//   put_strip_warp     the reference's full 4h+2 frame, one exchange per row
+//   put_strip_v2       3h+2 frame (columns that can still change)
+//   put_strip_slide    2h+2 sliding frame without the ghost lane
+//   put_strip_ghost2   ghost-lane frame, two rows per neighbour exchange
+//   put_strip_tiled    full frame, K rows per exchange (halo recompute)
+//   call_leaf_warp / call_leaf_v2 / call_leaf_tiled<K>   call strips
+#pragma once
+
+#include "../paper_2303_02317_b200/csrc/fl_callstrip.cuh"
+#include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+
+namespace fl {
+
+// Put strip over columns [lo, hi], `height` forward rows.  Cells <= f hold the
+// payoff, cells f+1..hi come from in_org[col].  Writes the continuation values
+// of cols kb+1 .. hi-height of the final row to out_org[col] and returns kb, the
+// largest exercise column of the final row within its valid range (NONE_SEEN
+// if none).  Every lane of the warp must call.
+template <int CPL>
+__device__ int64_t put_strip_warp(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                  const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
+                                  int height, double cd, double cm, double cu, long long* tm = nullptr) {
+  const int lane = threadIdx.x & 31;
+  double v[CPL], p[CPL];
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
+  }
+  unsigned green = 0;
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(v[0] + p[0] == 12345.678 ? 1 : 0); }
+  for (int s = 1; s <= height; ++s) {
+    const double left = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double right = __shfl_down_sync(FULL, v[0], 1);
+    double nv[CPL];
+    green = 0;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const double l = (c == 0) ? left : v[c - 1];
+      const double r = (c == CPL - 1) ? right : v[c + 1];
+      // the shuffled neighbour enters last: one DFMA between a shuffle and the
+      // next row's shuffle on the warp's critical path
+      const double lin = (c == CPL - 1) ? fma(cu, r, fma(cd, l, cm * v[c])) : fma(cd, l, fma(cu, r, cm * v[c]));
+      const bool red = lin > p[c];
+      nv[c] = red ? lin : p[c];
+      green |= (red ? 0u : 1u) << c;
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
+  // last green inside the final valid range [lo+height, hi-height]
+  const int64_t vlo = lo + height, vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col >= vlo && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = v[c];
+  }
+  return kb;
+}
+
+
+// put_strip_warp restricted to the columns that can still change.  The put
+// boundary drops by 0 or 1 column per row (bsm.py:420-427 enforces it: the
+// reference raises GeometryError otherwise), so at row s every column below
+// f-s is an exercise cell: its projected value is its payoff (deep in the
+// exercise region lin - payoff ~ -omega*dtau, far from any rounding tie).
+// The strip therefore only needs the frame [f-h-1, hi] (3h+2 columns instead
+// of 4h+2), with the payoff of column f-h-2 as the fixed left neighbour.
+// Same per-cell arithmetic and the same returned boundary / outputs as
+// put_strip_warp.  The green mask is formed on the final row only.
+template <int CPL>
+__device__ int64_t put_strip_v2(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                const double* __restrict__ pay_org, int64_t hi, int64_t f, int height, double cd,
+                                double cm, double cu, long long* tm = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t lo = f - height - 1;
+  double v[CPL], p[CPL];
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col <= hi) {
+      p[c] = pay_org[col];
+      v[c] = (col <= f) ? p[c] : in_org[col];
+    } else {
+      p[c] = 0.0;
+      v[c] = 0.0;
+    }
+  }
+  const double edge = pay_org[lo - 1];  // fixed left neighbour of the frame (an exercise cell)
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(v[0] + p[0] + edge == 12345.678 ? 1 : 0); }
+  unsigned green = 0;
+  for (int s = 1; s <= height; ++s) {
+    const double up = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double right = __shfl_down_sync(FULL, v[0], 1);
+    const double left = (lane == 0) ? edge : up;
+    double nv[CPL];
+    if (s < height) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double l = (c == 0) ? left : v[c - 1];
+        const double r = (c == CPL - 1) ? right : v[c + 1];
+        const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+        nv[c] = lin > p[c] ? lin : p[c];
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const double l = (c == 0) ? left : v[c - 1];
+        const double r = (c == CPL - 1) ? right : v[c + 1];
+        const double lin = fma(cd, l, fma(cu, r, cm * v[c]));
+        const bool red = lin > p[c];
+        nv[c] = red ? lin : p[c];
+        green |= (red ? 0u : 1u) << c;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
+  // last green inside the final valid range [f-h-1, hi-h]
+  const int64_t vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = v[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
+
+// Sliding-frame put strip.  Same contract as put_strip_warp (lo = f-2h-1,
+// hi = f+2h) but the frame follows the valid cone: at row s it holds only
+// the 2h+2 columns f-s-1 .. f+2h-s, cell j = column f-s-1+j.  Two facts make
+// that exact:
+//   * right side: the reference's valid range shrinks by one column per row
+//     (_accel.py:203-242: after s rows only [lo+s, hi-s] is valid), so
+//     columns right of f+2h-s never influence the final valid range;
+//   * left side: at row s every column < f-s is an exercise cell whose value
+//     is its payoff (the boundary drops by at most one column per row: a cell
+//     whose three parents are exercise cells gets lin = payoff - omega*dtau +
+//     O(dtau ds^2) < payoff; the host checks that margin per option,
+//     PutParams::slide, and options that fail it use put_strip_pipe).
+// In frame coordinates the stencil is left-shifted, new u[j] = F(u[j-2],
+// u[j-1], u[j]), so a lane needs two cells from its left neighbour and none
+// from its right: one shuffle direction, and the lane's last cell of the next
+// row depends on its own cells only.  The loop-carried path is one shuffle,
+// one DFMA and one max per row; each row costs 3 CPL FP64 ops + CPL maxes
+// instead of the 4h+2 frame's 5 x (3 + 1).  Lane 0's two left cells are the
+// payoffs of columns f-s-3, f-s-2.  Per-cell arithmetic is put_strip_warp's
+// interior order: fma(cd, left, fma(cu, right, cm * cur)), projected by max
+// (equal to the reference's lin > pay ? lin : pay), exercise iff !(lin > pay).
+// Requires 2h+2 <= 32*CPL.  pay_org must cover cols f-h-4 .. f+2h.
+template <int CPL, int PAYMODE = 0>
+__device__ int64_t put_strip_slide(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 2, "two left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = lane * CPL;
+  const bool l0 = lane == 0;
+  // row 0: cols f-1+j; cols <= f hold the payoff, f+1 .. f+2h the input segment
+  const double* pay0 = pay_org + (f - 1);
+  // cells past the frame (j >= W: idle lanes, the tail of the last lane) read
+  // the frame's last column; their values never reach a cell j < W
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];  // payoff of cell j at row 0 (col f-1+j)
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  // lane 0's left fills: at row s cells -2, -1 are cols f-s-3, f-s-2 (exercise
+  // cells: their payoff), loaded two rows ahead (one uniform load per row).
+  double fill1 = pay_org[f - 2], fill2 = pay_org[f - 3], fill3 = pay_org[f - 4];
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] + fill1 == 12345.678 ? 1 : 0); }
+  const double* pq = pay0 - 1;  // row s+1 payoff of cell j: pq[j - s]
+  unsigned green = 0;
+  for (int s = 0; s < height; ++s) {
+    const double fill4 = pay_org[f - s - 5];  // row s+2's cell -2 (never past col f-h-4)
+    double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    L2 = l0 ? fill2 : L2;
+    L1 = l0 ? fill1 : L1;
+    // payoffs of row s+1 (col f-s-2+j = col of cell j-1 at row s)
+    double np[CPL];
+    if (PAYMODE == 0) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) np[c] = pq[jx[c] - s];
+    } else {
+      const double pl = __shfl_up_sync(FULL, p[CPL - 1], 1);
+      np[0] = l0 ? fill1 : pl;
+#pragma unroll
+      for (int c = 1; c < CPL; ++c) np[c] = p[c - 1];
+    }
+    double nu[CPL];
+    // the lane's last cells first (local inputs), so the next row's shuffles issue early
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) {
+      const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+      nu[c] = lin > np[c] ? lin : np[c];
+    }
+    const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+    const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
+    nu[1] = lin1 > np[1] ? lin1 : np[1];
+    nu[0] = lin0 > np[0] ? lin0 : np[0];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      u[c] = nu[c];
+      p[c] = np[c];
+    }
+    fill1 = fill2;
+    fill2 = fill3;
+    fill3 = fill4;
+  }
+  // exercise flags of the final row: the reference's cell is exercise iff
+  // !(lin > pay), i.e. iff its projected value is exactly its payoff
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  // final row: cell j = col f-h-1+j, j < W is the reference's final valid range
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
+
+// put_strip_ghost advancing TWO rows per neighbour exchange.  The frame's
+// stencil is left-shifted (new u[j] from u[j-2..j]), so for two rows a lane
+// needs its left neighbour's last FOUR cells: it recomputes the neighbour's two
+// edge cells of the first row itself (a two-cell halo, bit-identical to the
+// neighbour's own: same inputs, same FMA order, same payoffs) and then its own
+// cells of both rows.  One shuffle round trip per two rows instead of two --
+// in the kernel a shuffle waits behind the SM's queued shared-memory traffic,
+// so the round trip, not the arithmetic, sets the row time.  The halo payoffs
+// are the next entries of the lane's own payoff stream (pay0[jx0 - r]), so the
+// loads per row are unchanged.  Lane 0's halo is computed from its own cells
+// (shfl_up from lane 0): lower inputs, true payoffs, so its cells stay exactly
+// their payoffs as in put_strip_ghost.  Results (rows, boundary, outputs) are
+// bit-identical to put_strip_ghost.  Requires CPL >= 4.
+template <int CPL>
+__device__ int64_t put_strip_ghost2(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                    const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                    double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 4, "four left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = (lane - 1) * CPL;
+  const double* pay0 = pay_org + (f - 1);
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] == 12345.678 ? 1 : 0); }
+  // payoff stream of the lane's first cell: P(r) = payoff of cell jx0 at row r
+  // = pq0[1 - r]; the halo cells jx0-1, jx0-2 at row r have P(r+1), P(r+2)
+  const double* pq0 = pay0 - 1 + jx[0];
+  double Pa = pq0[0];  // P(1)
+  int s = 0;
+#pragma unroll 1
+  for (; s + 2 <= height; s += 2) {
+    const double L4 = __shfl_up_sync(FULL, u[CPL - 4], 1);
+    const double L3 = __shfl_up_sync(FULL, u[CPL - 3], 1);
+    const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    const double Pb = pq0[-(s + 1)];  // P(s+2)
+    const double Pc = pq0[-(s + 2)];  // P(s+3)
+    // row s+1: the halo cells -2, -1, then the lane's own cells
+    const double hm2 = proj_max(fma(cd, L4, fma(cu, L2, cm * L3)), Pc);
+    const double hm1 = proj_max(fma(cd, L3, fma(cu, L1, cm * L2)), Pb);
+    double v[CPL];
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) v[c] = proj_max(fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1])), p[c - 1]);
+    v[1] = proj_max(fma(cd, L1, fma(cu, u[1], cm * u[0])), p[0]);
+    v[0] = proj_max(fma(cd, L2, fma(cu, u[0], cm * L1)), Pa);
+    // row s+2
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) u[c] = proj_max(fma(cd, v[c - 2], fma(cu, v[c], cm * v[c - 1])), p[c - 2]);
+    u[1] = proj_max(fma(cd, hm1, fma(cu, v[1], cm * v[0])), Pa);
+    u[0] = proj_max(fma(cd, hm2, fma(cu, v[0], cm * hm1)), Pb);
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) p[c] = p[c - 2];
+    p[1] = Pa;
+    p[0] = Pb;
+    Pa = Pc;
+  }
+  if (s < height) {  // odd height: one single-row step (put_strip_ghost's row)
+    const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    double nu[CPL];
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) nu[c] = proj_max(fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1])), p[c - 1]);
+    nu[1] = proj_max(fma(cd, L1, fma(cu, u[1], cm * u[0])), p[0]);
+    nu[0] = proj_max(fma(cd, L2, fma(cu, u[0], cm * L1)), Pa);
+#pragma unroll
+    for (int c = CPL - 1; c >= 1; --c) p[c] = p[c - 1];
+    p[0] = Pa;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) u[c] = nu[c];
+  }
+  unsigned green = 0;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c >= 0 && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
+
+// Time-tiled variant of put_strip_warp: lanes exchange K halo cells per side
+// once per K rows (instead of one cell per side per row) and advance K rows on
+// an extended register tile, recomputing the halo cone redundantly.  One
+// shuffle round trip per K rows takes the shuffle latency off the per-row
+// critical path.  Same arithmetic per valid cell as put_strip_warp (identical
+// results).  Requires K <= CPL.
+template <int CPL, int K>
+__device__ int64_t put_strip_tiled(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t lo, int64_t hi, int64_t f,
+                                   int height, double cd, double cm, double cu) {
+  static_assert(K <= CPL, "halo must come from the neighbouring lane");
+  constexpr int E = CPL + 2 * K;
+  const int lane = threadIdx.x & 31;
+  const int64_t c0 = lo + (int64_t)lane * CPL;
+  double e[E], p[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int64_t col = c0 - K + i;
+    p[i] = (col >= lo && col <= hi) ? pay_org[col] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    e[K + c] = (col <= hi) ? ((col <= f) ? p[K + c] : in_org[col]) : 0.0;
+  }
+  unsigned green = 0;
+  __syncwarp();
+  for (int s0 = 0; s0 < height; s0 += K) {
+    const int kk = (height - s0 < K) ? (height - s0) : K;
+    // halo exchange: K cells from each neighbour
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      e[i] = __shfl_up_sync(FULL, e[K + CPL - K + i], 1);
+      e[K + CPL + i] = __shfl_down_sync(FULL, e[K + i], 1);
+    }
+#pragma unroll
+    for (int s = 1; s <= K; ++s) {
+      if (s <= kk) {
+        const bool last = (s0 + s == height);
+        double left = e[s - 1];
+        green = 0;
+#pragma unroll
+        for (int i = s; i <= E - 1 - s; ++i) {
+          const double cur = e[i];
+          const double lin = fma(cd, left, fma(cu, e[i + 1], cm * cur));
+          left = cur;
+          const bool red = lin > p[i];
+          e[i] = red ? lin : p[i];
+          if (last && i >= K && i < K + CPL) green |= (red ? 0u : 1u) << (i - K);
+        }
+      }
+    }
+  }
+  // last green inside the final valid range [lo+height, hi-height]
+  const int64_t vlo = lo + height, vhi = hi - height;
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (((green >> c) & 1u) && col >= vlo && col <= vhi) best = (int)(col - lo);
+  }
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : lo + best;
+  const int64_t wlo = (best < 0) ? vhi + 1 : kb + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t col = c0 + c;
+    if (col >= wlo && col <= vhi) out_org[col] = e[K + c];
+  }
+  return kb;
+}
+
+
+
+// Leaf strip (binomial_strip_sweep with lo = j-h+1, height h <= 32) on the
+// chain warp: lane l holds column lo+l.  Reads in_org[lo..j], writes
+// out_org[lo..jp], returns jp.  Operation order as _accel.py:143-158
+// (unfused products and sums).
+__device__ int64_t call_leaf_warp(const CallParams& P, const double* __restrict__ in_org,
+                                  double* __restrict__ out_org, int64_t lo, int64_t top_row, int64_t j0,
+                                  int height, double* cells) {
+  const int lane = threadIdx.x & 31;
+  const int W = (int)(j0 - lo + 1);
+  const int64_t col = lo + lane;
+  double v = (lane < W) ? in_org[col] : 0.0;
+  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
+  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
+  // base(t) = S exp((2 lo - (top_row - t)) lu): lane t holds the parent base of step t
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
+  int64_t j = j0;
+  for (int s = 0; s < height; ++s) {
+    if (j < lo) break;
+    const int64_t child = top_row - s - 1;
+    const int64_t top = j < child ? j : child;
+    *cells += (double)(top - lo + 1);
+    const double bp = __shfl_sync(FULL, Bl, s);
+    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
+    const double right = __shfl_down_sync(FULL, v, 1);
+    int fg = INT32_MAX;
+    if (col <= top) {
+      const double vr = (col + 1 <= j) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);
+      const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
+      const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
+      if (lin >= grn) {
+        v = lin;
+      } else {
+        v = grn;
+        fg = lane;
+      }
+    }
+    fg = warp_min_i32(fg);
+    j = (fg == INT32_MAX) ? top : lo + fg - 1;
+  }
+  if (col <= j && lane < W) out_org[col] = v;
+  __syncwarp();
+  return j;
+}
+
+
+// call_leaf_warp without the per-row boundary reduction.  The call boundary
+// only moves left as rows descend (american.py:232-251 enforces it), so every
+// column right of the row's boundary is an exercise cell for the rest of the
+// strip: advancing all strip columns with the projected update
+// max(wd v + wu v', green) reproduces the analytic exercise values there
+// (lin < green strictly inside the exercise region), and the boundary is
+// needed only once, on the last row (first green by one warp min).  Cells
+// beyond the lattice edge (col > child) are never read by valid cells.  Same
+// operation order as _accel.py:143-158.
+__device__ int64_t call_leaf_v2(const CallParams& P, const double* __restrict__ in_org, double* __restrict__ out_org,
+                                int64_t lo, int64_t top_row, int64_t j0, int height, double* cells) {
+  const int lane = threadIdx.x & 31;
+  const int W = (int)(j0 - lo + 1);
+  const int64_t col = lo + lane;
+  double v = (lane < W) ? in_org[col] : 0.0;
+  const double e2_me = exp(2.0 * (double)lane * P.lu);        // e2[col - lo]
+  const double e2_nx = exp(2.0 * (double)(lane + 1) * P.lu);  // e2[col + 1 - lo]
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
+  bool green = false;
+  for (int s = 0; s < height; ++s) {
+    const double bp = __shfl_sync(FULL, Bl, s);
+    const double bc = (s + 1 < 32) ? __shfl_sync(FULL, Bl, s + 1) : B32;
+    const double right = __shfl_down_sync(FULL, v, 1);
+    const double vr = (lane + 1 < W) ? right : __dsub_rn(__dmul_rn(bp, e2_nx), P.K);  // right of j0: exercise
+    const double lin = __dadd_rn(__dmul_rn(P.wd, v), __dmul_rn(P.wu, vr));
+    const double grn = __dsub_rn(__dmul_rn(bc, e2_me), P.K);
+    green = !(lin >= grn);
+    v = green ? grn : lin;
+  }
+  const int64_t child = top_row - height;  // last lattice column of the final row
+  const int64_t top = (j0 < child) ? j0 : child;
+  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
+  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
+  *cells += (double)W * height;
+  if (col <= jp && lane < W) out_org[col] = v;
+  __syncwarp();
+  return jp;
+}
+
+
+// call_leaf_v3 advancing K rows per neighbour exchange: a lane holds its
+// column plus the K columns to its right (a K-cell halo fetched once per K
+// rows) and recomputes the halo's shrinking cone -- row r of a tile updates
+// cells 0 .. K-1-r -- so the shuffle round trip leaves the per-row critical
+// path.  The call strip has one cell per lane, so its row time is the
+// exchange's latency, not its arithmetic.  Each cell's arithmetic is
+// call_leaf_v3's (same operands, same order): bit-identical rows, boundary and
+// outputs.  e2 must cover indices up to 32 + K.
+template <int K>
+__device__ int64_t call_leaf_tiled(const CallParams& P, const double* __restrict__ in_org,
+                                   double* __restrict__ out_org, int64_t lo, int64_t top_row, int64_t j0, int height,
+                                   double* cells, const double* __restrict__ e2) {
+  const int lane = threadIdx.x & 31;
+  const int W = (int)(j0 - lo + 1);
+  const int64_t col = lo + lane;
+  double v = (lane < W) ? in_org[col] : 0.0;
+  double e2c[K + 1];
+#pragma unroll
+  for (int k = 0; k <= K; ++k) e2c[k] = e2[lane + k];
+  const double Bl = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - lane)) * P.lu));
+  const double B32 = __dmul_rn(P.S, exp((double)(2 * lo - (top_row - 32)) * P.lu));
+  bool green = false;
+#pragma unroll 1
+  for (int s0 = 0; s0 < height; s0 += K) {
+    double c[K + 1];
+    c[0] = v;
+#pragma unroll
+    for (int k = 1; k <= K; ++k) c[k] = __shfl_down_sync(FULL, v, k);
+    double b[K + 1];  // b[r]: the parent base of tile row r (child base b[r + 1])
+#pragma unroll
+    for (int r = 0; r <= K; ++r) b[r] = (s0 + r < 32) ? __shfl_sync(FULL, Bl, (s0 + r) & 31) : B32;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (s0 + r < height) {
+#pragma unroll
+        for (int k = 0; k < K - r; ++k) {
+          const bool edge = (lane + k + 1 >= W);  // right neighbour outside the strip: exercise value
+          const double ex_r = __dsub_rn(__dmul_rn(b[r], e2c[k + 1]), P.K);
+          const double grn = __dsub_rn(__dmul_rn(b[r + 1], e2c[k]), P.K);
+          const double a = __dmul_rn(P.wd, c[k]);
+          const double vr = edge ? ex_r : c[k + 1];
+          const double lin = __dadd_rn(a, __dmul_rn(P.wu, vr));
+          const bool g = !(lin >= grn);
+          c[k] = g ? grn : lin;
+          if (k == 0) green = g;
+        }
+      }
+    }
+    v = c[0];
+  }
+  const int64_t child = top_row - height;
+  const int64_t top = (j0 < child) ? j0 : child;
+  const int fg = warp_min_i32((green && lane < W && col <= top) ? lane : INT32_MAX);
+  const int64_t jp = (fg == INT32_MAX) ? top : lo + fg - 1;
+  *cells += (double)W * height;
+  if (col <= jp && lane < W) out_org[col] = v;
+  __syncwarp();
+  return jp;
+}
+
+
+}  // namespace fl
