@@ -65,6 +65,17 @@ int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double*
                    int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
                    int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream);
 
+/* fl_price_batch with caller-supplied lattice constants for binomial options
+ * (the reference pricers' `params=` argument: binomial.py:80/161,
+ * american.py:428): bparams is n x 4 doubles {weight_down, weight_up, log_up,
+ * step_years}; a row whose weight_down is NaN (or bparams == NULL) derives them
+ * from the spec as fl_price_batch does.  Puts ignore it. */
+int fl_price_batch_ex(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+                      const double* Y, const double* V, const double* E, const int64_t* T, const double* bparams,
+                      double lam, int64_t call_cutoff, int64_t put_cutoff, int method, double* price,
+                      int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap,
+                      void* stream);
+
 /* Release the calling thread's cached batch buffers (fl_price_batch keeps one
  * grow-only batch per (thread, device); they are also freed at thread exit). */
 void fl_release_cache(void);
@@ -245,6 +256,13 @@ int fl_euro_approx(int64_t n, const double* S, const double* K, const double* R,
  * DFT (inverse with the 1/N factor) of n complex values, interleaved
  * (re, im) doubles, host buffers. */
 int fl_fft(const double* in, int64_t n, int inverse, double* out, void* stream);
+
+/* fft.py:203-260 kernel_power for a generic kernel (any number of taps, any
+ * finite real weights): the zero-padded spectrum raised to the h-th power
+ * and inverted on the device (a one-tap kernel: its weight to the h-th
+ * power).  out receives h (L - 1) + 1 weights.  The pricers' own two- and
+ * three-tap nonnegative kernels take fl_apply_linear_steps' analytic path. */
+int fl_kernel_power(const double* w, int64_t L, int64_t h, double* out, void* stream);
 
 /* fft.py:130 convolve: full linear convolution of two complex sequences
  * (interleaved re, im; real inputs with zero imaginary parts), zero-padded to

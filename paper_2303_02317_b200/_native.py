@@ -44,7 +44,7 @@ EXPORTED_SYMBOLS = (
     "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
     "fl_probe_fp64", "fl_release_cache", "fl_shard_plan", "fl_price_batch_multi", "fl_price_batch_dev",
     "fl_price_put_bsm", "fl_price_american_call", "fl_price_european", "fl_dev_workspace_bytes", "fl_sync",
-    "fl_release_dev_cache",
+    "fl_release_dev_cache", "fl_kernel_power", "fl_price_batch_ex",
 )
 
 
@@ -139,6 +139,10 @@ def lib():
         L.fl_dev_workspace_bytes.restype = c_int
         L.fl_sync.argtypes = [P]
         L.fl_sync.restype = c_int
+        L.fl_price_batch_ex.argtypes = [i64, P, P, P, P, P, P, P, P, P, d, i64, i64, c_int, P, P, P, P, P, i32, P]
+        L.fl_price_batch_ex.restype = c_int
+        L.fl_kernel_power.argtypes = [P, i64, i64, P, P]
+        L.fl_kernel_power.restype = c_int
         _lib = L
         return L
 
@@ -236,8 +240,10 @@ def _inputs(kind, S, K, R, Y, V, E, T):
 
 
 def price_batch(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128,
-                method=METHOD_FAST, bnd_cap=0, stream=None) -> BatchResult:
-    """Price a batch through ``fl_price_batch`` (host arrays in and out)."""
+                method=METHOD_FAST, bnd_cap=0, stream=None, bparams=None) -> BatchResult:
+    """Price a batch through ``fl_price_batch`` (host arrays in and out);
+    ``bparams`` (n x 4: weight_down, weight_up, log_up, step_years; NaN rows
+    derive) overrides the binomial lattice constants (``fl_price_batch_ex``)."""
     n, k, S, K, R, Y, V, E, T = _inputs(kind, S, K, R, Y, V, E, T)
     price = np.empty(n)
     status = np.empty(n, dtype=np.int32)
@@ -245,8 +251,11 @@ def price_batch(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cuto
     bt = np.empty((n, max(cap, 1)), dtype=np.int64)
     bc = np.empty((n, max(cap, 1)), dtype=np.int64)
     bcount = np.zeros(n, dtype=np.int32)
-    _check(lib().fl_price_batch(
-        n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T), float(lam),
+    bp = None if bparams is None else np.ascontiguousarray(np.broadcast_to(
+        np.asarray(bparams, dtype=np.float64), (n, 4)))
+    _check(lib().fl_price_batch_ex(
+        n, _ptr(k), _ptr(S), _ptr(K), _ptr(R), _ptr(Y), _ptr(V), _ptr(E), _ptr(T),
+        _ptr(bp) if bp is not None else None, float(lam),
         int(call_cutoff), int(put_cutoff), int(method), _ptr(price), _ptr(status),
         _ptr(bt) if cap else None, _ptr(bc) if cap else None, _ptr(bcount) if cap else None,
         cap, ctypes.c_void_p(stream) if stream else None))
@@ -336,11 +345,11 @@ def apply_linear_steps(x: np.ndarray, taps: int, c0: float, c1: float, c2: float
 
 
 def price_batch_full(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put_cutoff=128,
-                     method=METHOD_FAST, bnd_cap=64, stream=None) -> BatchResult:
+                     method=METHOD_FAST, bnd_cap=64, stream=None, bparams=None) -> BatchResult:
     """``price_batch`` with complete boundary records: options whose record
     exceeded ``bnd_cap`` are re-run with a capacity that fits them."""
     res = price_batch(kind, S, K, R, Y, V, E, T, lam=lam, call_cutoff=call_cutoff, put_cutoff=put_cutoff,
-                      method=method, bnd_cap=bnd_cap, stream=stream)
+                      method=method, bnd_cap=bnd_cap, stream=stream, bparams=bparams)
     over = np.nonzero(res.bnd_count > res.cap)[0]
     if over.size == 0:
         return res
@@ -348,7 +357,8 @@ def price_batch_full(kind, S, K, R, Y, V, E, T, *, lam=0.4, call_cutoff=256, put
     cap2 = int(res.bnd_count[over].max())
     sub = price_batch(k[over], S[over], K[over], R[over], Y[over], V[over], E[over], T[over], lam=lam,
                       call_cutoff=call_cutoff, put_cutoff=put_cutoff, method=method, bnd_cap=cap2,
-                      stream=stream)
+                      stream=stream,
+                      bparams=None if bparams is None else np.broadcast_to(np.asarray(bparams), (n, 4))[over])
     bt = np.full((n, cap2), 0, dtype=np.int64)
     bc = np.full((n, cap2), 0, dtype=np.int64)
     c0 = res.cap
@@ -592,3 +602,11 @@ def release_caches() -> None:
     """Free this thread's cached host-path batches and device-path workspaces."""
     lib().fl_release_cache()
     lib().fl_release_dev_cache()
+
+
+def kernel_power(weights: np.ndarray, h: int) -> np.ndarray:
+    """fl_kernel_power: generic composed kernel (spectrum power on the device)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.empty(int(h) * (w.shape[0] - 1) + 1)
+    _check(lib().fl_kernel_power(_ptr(w), w.shape[0], int(h), _ptr(out), None))
+    return out

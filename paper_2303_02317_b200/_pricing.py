@@ -42,31 +42,43 @@ def _steps(t) -> int:
 
 
 def check_params(spec, params: BinomialParams | None) -> None:
-    """The device derives the lattice constants itself (bit-identically to
-    derive_binomial_params); caller-supplied constants must agree."""
+    """The normal-limit approximations derive prob_up / discount on the
+    device from the spec; caller-supplied constants must agree there (the
+    lattice pricers take them: ``bparams``)."""
     if params is None:
         return
     if params != derive_binomial_params(spec):
         raise UnsupportedCombinationError(
-            "the GPU pricers derive the lattice constants from the spec; "
-            "custom BinomialParams are not supported")
+            "the GPU normal-limit approximations derive prob_up and the discount from the spec; "
+            "custom BinomialParams are supported by the lattice pricers only")
+
+
+def bparams(params: BinomialParams | None):
+    """Caller-supplied lattice constants as the C ABI's override row (the
+    reference pricers' ``params=``, binomial.py:80/161, american.py:428)."""
+    if params is None:
+        return None
+    return np.array([[float(params.weight_down), float(params.weight_up), float(params.log_up),
+                      float(params.step_years)]])
 
 
 def price_one(kind: int, spec, *, method: int = FAST, lam: float = 0.4, steps: int | None = None,
-              call_cutoff: int = 256, put_cutoff: int = 128, record: bool = True):
+              call_cutoff: int = 256, put_cutoff: int = 128, record: bool = True,
+              params: BinomialParams | None = None):
     """Price one spec on the device; returns (price, BoundarySeries | None).
 
     Raises the reference exception for a nonzero status."""
     S, K, R, Y, V, E, T = spec_arrays([spec])
     if steps is not None:
         T[0] = _steps(steps)
+    bp = bparams(params)
     if record:
         cap = int(T[0]) + 2 if method == BASELINE else 64
         res = _native.price_batch_full(np.int8(kind), S, K, R, Y, V, E, T, lam=lam, call_cutoff=call_cutoff,
-                                       put_cutoff=put_cutoff, method=method, bnd_cap=cap)
+                                       put_cutoff=put_cutoff, method=method, bnd_cap=cap, bparams=bp)
     else:
         res = _native.price_batch(np.int8(kind), S, K, R, Y, V, E, T, lam=lam, call_cutoff=call_cutoff,
-                                  put_cutoff=put_cutoff, method=method, bnd_cap=0)
+                                  put_cutoff=put_cutoff, method=method, bnd_cap=0, bparams=bp)
     err = _native.status_error(int(res.status[0]))
     if err is not None:
         raise err

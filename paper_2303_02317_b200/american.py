@@ -103,9 +103,8 @@ def fast_american_call(spec: OptionSpec, params: BinomialParams | None = None, *
         # the reference validates base_cutoff only on its recursion path; the
         # device rejects it up front with the same exception
         raise ValidationError("base_cutoff", "base_cutoff must be >= 1")
-    _pricing.check_params(spec, params)
     price, series = _pricing.price_one(_pricing.KIND_CALL, spec, method=_pricing.FAST,
-                                       call_cutoff=int(base_cutoff))
+                                       call_cutoff=int(base_cutoff), params=params)
     return AmericanCallResult(price=price, boundaries=series)
 
 

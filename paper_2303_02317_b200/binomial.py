@@ -55,15 +55,13 @@ def leaf_row(spec: OptionSpec, params: BinomialParams | None = None) -> GridRow:
 
 def baseline_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
     """O(T^2) backward induction on the device (binomial.py:80-91)."""
-    _pricing.check_params(spec, params)
-    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.BASELINE, record=False)
+    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.BASELINE, record=False, params=params)
     return price
 
 
 def fast_european(spec: OptionSpec, params: BinomialParams | None = None) -> float:
     """Gauged composed-kernel inner product on the device (binomial.py:161-194)."""
-    _pricing.check_params(spec, params)
-    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.FAST, record=False)
+    price, _ = _pricing.price_one(_pricing.KIND_EURO, spec, method=_pricing.FAST, record=False, params=params)
     return price
 
 
@@ -71,17 +69,16 @@ def baseline_american_call(spec: OptionSpec, params: BinomialParams | None = Non
                            keep_grid: bool = False) -> AmericanCallResult:
     """O(T^2) projected induction on the device, first green per row recorded
     (binomial.py:94-130)."""
-    _pricing.check_params(spec, params)
     if keep_grid:
         # every row and exercise mask retained (binomial.py:133-158), computed on the device
         from . import _native
 
-        p = derive_binomial_params(spec)
+        p = derive_binomial_params(spec) if params is None else params
         price, rows, masks, cols = _native.call_grid(spec.spot, spec.strike, p.weight_down, p.weight_up,
                                                      p.log_up, spec.steps)
         series = BoundarySeries(np.arange(spec.steps + 1, dtype=np.int64), cols)
         return AmericanCallResult(price=price, boundaries=series, rows=rows, exercise_masks=masks)
-    price, series = _pricing.price_one(_pricing.KIND_CALL, spec, method=_pricing.BASELINE)
+    price, series = _pricing.price_one(_pricing.KIND_CALL, spec, method=_pricing.BASELINE, params=params)
     return AmericanCallResult(price=price, boundaries=series)
 
 

@@ -185,7 +185,7 @@ namespace {
 // Host-side derivation + dispatch lists.  Pure host work (libm), no CUDA.
 int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
                const double* Y, const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
-               int64_t put_cutoff, int method, int32_t cap) {
+               int64_t put_cutoff, int method, int32_t cap, const double* bparams = nullptr) {
   b->n = n;
   b->method = method;
   b->cap = cap;
@@ -206,9 +206,18 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
     const fl::SpecIn s{S[i], K[i], R[i], Y[i], V[i], E[i], T[i]};
     const int32_t o = (int32_t)i;
     int32_t st = 0;
+    // caller-supplied lattice constants (n x 4: weight_down, weight_up,
+    // log_up, step_years; a NaN weight_down row derives them from the spec)
+    fl::Binom ovr_b{};
+    const fl::Binom* ovr = nullptr;
+    if (bparams && !std::isnan(bparams[4 * i])) {
+      ovr_b.wd = bparams[4 * i]; ovr_b.wu = bparams[4 * i + 1]; ovr_b.lu = bparams[4 * i + 2];
+      ovr_b.dt = bparams[4 * i + 3];
+      ovr = &ovr_b;
+    }
     switch (kind[i]) {
       case FL_KIND_EURO: {
-        st = fl::prep_euro(s, b->euro[i]);
+        st = fl::prep_euro(s, b->euro[i], ovr);
         if (!st) {
           b->mode[i] = (method == FL_METHOD_FAST) ? fl::MODE_FAST : fl::MODE_BASELINE;
           (method == FL_METHOD_FAST ? b->o_euro_fast : b->o_euro_base).push_back(o);
@@ -217,7 +226,7 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
       }
       case FL_KIND_CALL: {
         if (method == FL_METHOD_FAST) {
-          st = fl::prep_call(s, call_cutoff, b->call[i], b->euro[i]);
+          st = fl::prep_call(s, call_cutoff, b->call[i], b->euro[i], ovr);
           if (!st) {
             b->mode[i] = b->call[i].mode;
             if (b->mode[i] == fl::MODE_FAST) b->o_call_fast.push_back(o);
@@ -226,7 +235,7 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
           }
         } else {
           fl::Binom bn;
-          st = fl::derive_binomial(s, bn);
+          st = fl::binomial_or_override(s, ovr, bn);
           if (!st) {
             fl::CallParams& c = b->call[i];
             c.S = s.S; c.K = s.K; c.wd = bn.wd; c.wu = bn.wu; c.lu = bn.lu; c.n = s.T;
@@ -868,6 +877,47 @@ int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double
   return 0;
 }
 
+int fl_kernel_power(const double* w, int64_t L, int64_t h, double* out, void* stream) {
+  // generic kernel_power (fft.py:203-260): the spectrum of the zero-padded
+  // kernel raised to the h-th power, inverted (any taps, any finite weights);
+  // a one-tap kernel is its weight to the h-th power.  Writes h (L-1) + 1
+  // weights.
+  if (!w || !out) return fail("fl_kernel_power: null pointer");
+  if (L < 1 || h < 1) return fail("fl_kernel_power: need L >= 1 and h >= 1");
+  const int64_t out_len = h * (L - 1) + 1;
+  int64_t n = 1;
+  while (n < out_len) n <<= 1;
+  if (n > ((int64_t)1 << 27)) return fail("fl_kernel_power: composed kernel too long");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  FL_CUDA(cudaGetDevice(&dev));
+  DevBuf a, t;
+  FL_CUDA(a.ensure(sizeof(double2) * n));
+  FL_CUDA(t.ensure(sizeof(double2) * n));
+  std::vector<double2> hw(L);
+  for (int64_t i = 0; i < L; ++i) hw[i] = make_double2(w[i], 0.0);
+  cudaError_t e = cudaMemsetAsync(a.p, 0, sizeof(double2) * n, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(a.p, hw.data(), sizeof(double2) * L, cudaMemcpyHostToDevice, st);
+  double2 *f = nullptr, *r = nullptr;
+  if (n == 1) {
+    if (e == cudaSuccess) e = fl::launch_cpow(a.as<double2>(), 1, h, 1.0, st);
+    r = a.as<double2>();
+  } else {
+    if (e == cudaSuccess) e = fl::fft_pow2(a.as<double2>(), t.as<double2>(), n, -1, &f, st);
+    if (e == cudaSuccess) e = fl::launch_cpow(f, n, h, 1.0 / (double)n, st);
+    double2* other = (f == a.as<double2>()) ? t.as<double2>() : a.as<double2>();
+    if (e == cudaSuccess) e = fl::fft_pow2(f, other, n, 1, &r, st);
+  }
+  std::vector<double2> ho(out_len);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ho.data(), r, sizeof(double2) * out_len, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  a.release();
+  t.release();
+  if (e != cudaSuccess) return fail(std::string("fl_kernel_power: ") + cudaGetErrorString(e));
+  for (int64_t i = 0; i < out_len; ++i) out[i] = ho[i].x;
+  return 0;
+}
+
 int64_t fl_batch_device_bytes(const fl_batch* b) {
   if (!b) {
     fail("fl_batch_device_bytes: null batch");
@@ -945,8 +995,9 @@ thread_local BatchCache t_cache;
 int price_with(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
                const double* Y, const double* V, const double* E, const int64_t* T, double lam, int64_t call_cutoff,
                int64_t put_cutoff, int method, double* price, int32_t* status, int64_t* bnd_times,
-               int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, cudaStream_t stream) {
-  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap);
+               int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, cudaStream_t stream,
+               const double* bparams = nullptr) {
+  int rc = plan_host(b, n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, bnd_cap, bparams);
   if (rc) return rc;
   rc = upload(b, stream);
   if (rc) return rc;
@@ -964,16 +1015,25 @@ fl_batch* g_dev_batch[64] = {nullptr};
 
 extern "C" {
 
-int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
-                   const double* Y, const double* V, const double* E, const int64_t* T, double lam,
-                   int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
-                   int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream) {
+int fl_price_batch_ex(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+                      const double* Y, const double* V, const double* E, const int64_t* T, const double* bparams,
+                      double lam, int64_t call_cutoff, int64_t put_cutoff, int method, double* price,
+                      int32_t* status, int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap,
+                      void* stream) {
   int dev = 0;
   FL_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) return fail("fl_price_batch: device index out of range");
   if (!t_cache.b[dev]) t_cache.b[dev] = new fl_batch();
   return price_with(t_cache.b[dev], n, kind, S, K, R, Y, V, E, T, lam, call_cutoff, put_cutoff, method, price,
-                    status, bnd_times, bnd_cols, bnd_count, bnd_cap, (cudaStream_t)stream);
+                    status, bnd_times, bnd_cols, bnd_count, bnd_cap, (cudaStream_t)stream, bparams);
+}
+
+int fl_price_batch(int64_t n, const int8_t* kind, const double* S, const double* K, const double* R,
+                   const double* Y, const double* V, const double* E, const int64_t* T, double lam,
+                   int64_t call_cutoff, int64_t put_cutoff, int method, double* price, int32_t* status,
+                   int64_t* bnd_times, int64_t* bnd_cols, int32_t* bnd_count, int32_t bnd_cap, void* stream) {
+  return fl_price_batch_ex(n, kind, S, K, R, Y, V, E, T, nullptr, lam, call_cutoff, put_cutoff, method, price,
+                           status, bnd_times, bnd_cols, bnd_count, bnd_cap, stream);
 }
 
 void fl_release_cache(void) { t_cache.release_all(); }

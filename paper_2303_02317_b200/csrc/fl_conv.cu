@@ -70,10 +70,46 @@ cudaError_t probe_fp64(double* tflops, cudaStream_t stream) {
   return e;
 }
 
+// Short jumps (h <= LS_DIRECT_H) go through the composed weights directly:
+// W_h by h - 1 real-space convolutions with the stencil in shared memory (all
+// terms nonnegative), then y[k] = sum_r W_h[r] x[k + r] -- as the pricers'
+// subtree correlations do, so a run of exact zeros stays exactly zero (the
+// windowed FFT leaves round-off of order 1e-16 max|x| there).  Longer jumps:
+// the truncated overlap-save FFT with the analytic spectrum (conv_fft).
+constexpr int LS_DIRECT_H = 64;
+
 __global__ void __launch_bounds__(CTA_THREADS)
 linear_steps_kernel(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
                     Stencil st) {
   extern __shared__ double2 sbuf[];
+  if (h <= LS_DIRECT_H) {
+    double* w = reinterpret_cast<double*>(sbuf);
+    double* t = w + (2 * LS_DIRECT_H + 2);
+    const int M = h * st.span + 1;
+    const double s[3] = {st.c0, st.c1, st.c2};
+    for (int r = threadIdx.x; r < M; r += CTA_THREADS) w[r] = (r <= st.span) ? s[r] : 0.0;
+    __syncthreads();
+    for (int m = 2; m <= h; ++m) {  // W_m = W_{m-1} (*) stencil, lengths (m-1) span + 1 -> m span + 1
+      const int len = m * st.span + 1;
+      for (int r = threadIdx.x; r < len; r += CTA_THREADS) {
+        double acc = 0.0;
+        for (int j = 0; j <= st.span; ++j) {
+          const int q = r - j;
+          if (q >= 0 && q <= (m - 1) * st.span) acc = fma(w[q], s[j], acc);
+        }
+        t[r] = acc;
+      }
+      __syncthreads();
+      for (int r = threadIdx.x; r < len; r += CTA_THREADS) w[r] = t[r];
+      __syncthreads();
+    }
+    for (int64_t k = threadIdx.x; k < Lout; k += CTA_THREADS) {
+      double acc = 0.0;
+      for (int r = 0; r < M; ++r) acc = fma(w[r], x[k + r], acc);
+      y[k] = acc;
+    }
+    return;
+  }
   conv_fft(x, L, y, Lout, h, st, sbuf, LS_LOGN_MAX, fl_twq, Grp{(int)threadIdx.x, CTA_THREADS, 0});
 }
 

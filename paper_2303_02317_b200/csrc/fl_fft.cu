@@ -68,6 +68,24 @@ cudaError_t launch_cmul(double2* a, const double2* b, int64_t n, double scale, c
   return cudaGetLastError();
 }
 
+// z -> z^h per bin by binary exponentiation (kernel_power's spectrum power,
+// fft.py:255 `rfft(padded) ** h`), then the inverse transform's 1/N folded in.
+__global__ void cpow_inplace(double2* __restrict__ a, int64_t n, int64_t h, double scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 base = a[i], acc = make_double2(1.0, 0.0);
+    for (int64_t e = h; e > 0; e >>= 1) {
+      if (e & 1) acc = cmul(acc, base);
+      if (e > 1) base = cmul(base, base);
+    }
+    a[i] = make_double2(acc.x * scale, acc.y * scale);
+  }
+}
+
+cudaError_t launch_cpow(double2* a, int64_t n, int64_t h, double scale, cudaStream_t stream) {
+  cpow_inplace<<<grid_for(n), 256, 0, stream>>>(a, n, h, scale);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cscale(double2* a, int64_t n, double scale, cudaStream_t stream) {
   cscale_inplace<<<grid_for(n), 256, 0, stream>>>(a, n, scale);
   return cudaGetLastError();

@@ -109,5 +109,6 @@ cudaError_t launch_euro_approx(const EuroApprox* opts, int n_opts, int method, d
 cudaError_t fft_pow2(double2* buf, double2* tmp, int64_t n, int sign, double2** result, cudaStream_t stream);
 cudaError_t launch_cmul(double2* a, const double2* b, int64_t n, double scale, cudaStream_t stream);
 cudaError_t launch_cscale(double2* a, int64_t n, double scale, cudaStream_t stream);
+cudaError_t launch_cpow(double2* a, int64_t n, int64_t h, double scale, cudaStream_t stream);
 
 }  // namespace fl

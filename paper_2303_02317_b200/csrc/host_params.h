@@ -156,9 +156,20 @@ FL_HD inline int32_t call_junction_boundary(const SpecIn& s, const Binom& b, int
   return FL_OK;
 }
 
-FL_HD inline int32_t prep_euro(const SpecIn& s, EuroParams& e) {
+// Caller-supplied lattice constants (the reference pricers' `params=`
+// argument, binomial.py:161 / american.py:428): used instead of the derived
+// ones; the spec is still validated.
+FL_HD inline int32_t binomial_or_override(const SpecIn& s, const Binom* ovr, Binom& b) {
+  if (!ovr) return derive_binomial(s, b);
+  const int32_t st = validate_spec(s);
+  if (st) return st;
+  b = *ovr;
+  return FL_OK;
+}
+
+FL_HD inline int32_t prep_euro(const SpecIn& s, EuroParams& e, const Binom* ovr = nullptr) {
   Binom b;
-  int32_t st = derive_binomial(s, b);
+  int32_t st = binomial_or_override(s, ovr, b);
   e.S = s.S; e.K = s.K; e.n = s.T; e.lu = b.lu;
   e.mode = st ? MODE_ERROR : MODE_FAST;
   e.pad = 0;
@@ -170,14 +181,15 @@ FL_HD inline int32_t prep_euro(const SpecIn& s, EuroParams& e) {
 }
 
 // american.py:428-470 dispatch
-FL_HD inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroParams& e) {
+FL_HD inline int32_t prep_call(const SpecIn& s, int64_t cutoff, CallParams& c, EuroParams& e,
+                               const Binom* ovr = nullptr) {
   Binom b;
   c.S = s.S; c.K = s.K; c.n = s.T; c.cutoff = (int32_t)cutoff; c.price = 0.0;
   c.top_b = -1; c.junc_j = -1;
-  int32_t st = derive_binomial(s, b);
+  int32_t st = binomial_or_override(s, ovr, b);
   if (st) { c.mode = MODE_ERROR; return st; }
   c.wd = b.wd; c.wu = b.wu; c.lu = b.lu;
-  prep_euro(s, e);
+  prep_euro(s, e, ovr);
   const int64_t n = s.T;
   if (s.Y == 0.0) {
     c.top_b = call_top_boundary(s, b);

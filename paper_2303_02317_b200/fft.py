@@ -4,9 +4,9 @@
 ``apply_linear_steps`` (fft.py:263-329) with the reference signatures; the
 composition and the valid-mode correlation run on the device
 (``fl_apply_linear_steps``: truncated overlap-save FFT with the analytic
-stencil spectrum, csrc/fl_conv.cuh).  Supported kernels are the pricers' own:
-two or three nonnegative taps (lattice / FD weights); anything else raises
-``UnsupportedCombinationError`` instead of falling back to the CPU.
+stencil spectrum, csrc/fl_conv.cuh, for the pricers' own two- / three-tap
+nonnegative stencils; ``fl_kernel_power`` + ``fl_convolve``, the device
+transform pair, for any other kernel).
 """
 
 from __future__ import annotations
@@ -20,7 +20,6 @@ from .model import (
     GridRow,
     InsufficientWidthError,
     NumericalIntegrityError,
-    UnsupportedCombinationError,
     ValidationError,
 )
 
@@ -48,41 +47,69 @@ class Kernel:
         return self.min_offset + len(self) - 1
 
 
-def _device_taps(kernel: Kernel) -> tuple[int, float, float, float]:
-    w = kernel.weights
-    if len(w) not in (2, 3) or not np.all(np.isfinite(w)) or np.any(w < 0.0):
-        raise UnsupportedCombinationError(
-            "the GPU composes two- or three-tap kernels with nonnegative finite weights only")
+def _fast_taps(w: np.ndarray) -> bool:
+    """The pricers' own stencils: two or three nonnegative finite taps (analytic
+    spectrum / direct composed weights on the device, fl_apply_linear_steps)."""
+    return len(w) in (2, 3) and bool(np.all(np.isfinite(w))) and bool(np.all(w >= 0.0))
+
+
+def _device_taps(w: np.ndarray) -> tuple[int, float, float, float]:
     c2 = float(w[2]) if len(w) == 3 else 0.0
     return len(w), float(w[0]), float(w[1]), c2
 
 
+def _power_core(w: np.ndarray, h: int) -> np.ndarray:
+    """Composed weights of a kernel with nonzero first and last taps."""
+    if _fast_taps(w):
+        taps, c0, c1, c2 = _device_taps(w)
+        m = h * (taps - 1) + 1
+        x = np.zeros(2 * m - 1)
+        x[m - 1] = 1.0
+        y = _native.apply_linear_steps(x, taps, c0, c1, c2, h)  # y[k] = W[m-1-k]
+        return np.ascontiguousarray(y[::-1])
+    return _native.kernel_power(w, h)  # generic: spectrum ** h on the device
+
+
 def kernel_power(kernel: Kernel, h: int) -> Kernel:
-    """h-fold composition of ``kernel`` (fft.py:203-260), computed on the device
-    as the composed correlation of a unit impulse."""
+    """h-fold composition of ``kernel`` (fft.py:203-260) on the device.
+
+    Exact zero taps at either end stay exact zeros (fft.py:176-183 for two
+    taps: they only shift the composed kernel); the nonzero core is composed
+    on the device -- the pricers' two- / three-tap nonnegative stencils as the
+    composed correlation of a unit impulse (analytic spectrum), any other
+    kernel (more taps, negative weights) by raising its spectrum to the h-th
+    power and inverting, as the reference does (fft.py:244-260)."""
     if h < 0:
         raise ValidationError("h", "step count h must be >= 0")
     if h == 0:
         return Kernel(np.array([1.0]), 0)
     if h == 1:
         return Kernel(kernel.weights.copy(), kernel.min_offset)
-    taps, c0, c1, c2 = _device_taps(kernel)
-    m = h * (taps - 1) + 1
-    x = np.zeros(2 * m - 1)
-    x[m - 1] = 1.0
-    y = _native.apply_linear_steps(x, taps, c0, c1, c2, h)  # y[k] = W[m-1-k]
-    w = np.ascontiguousarray(y[::-1])
+    w = kernel.weights
+    out_len = h * (len(w) - 1) + 1
     if not np.all(np.isfinite(w)):
         raise NumericalIntegrityError(f"composed kernel overflowed for h={h}")
-    return Kernel(w, h * kernel.min_offset)
+    nz = np.nonzero(w)[0]
+    out = np.zeros(out_len)
+    if nz.size:
+        lead = int(nz[0])
+        core = _power_core(np.ascontiguousarray(w[lead:int(nz[-1]) + 1]), h)
+        out[h * lead:h * lead + core.shape[0]] = core
+    if not np.all(np.isfinite(out)):
+        raise NumericalIntegrityError(
+            f"composed kernel overflowed for h={h} (max weight magnitude {np.max(np.abs(w)):.3e})")
+    return Kernel(out, h * kernel.min_offset)
 
 
 def apply_linear_steps(row: GridRow, kernel: Kernel, h: int, *, direction: int = 1,
                        composed: Kernel | None = None) -> GridRow:
     """Advance ``row`` by h linear steps in one device correlation (fft.py:263-329).
 
-    ``composed`` (the reference's cache hook) is length-checked; the device
-    derives the composed weights itself."""
+    The pricers' stencils (two / three nonnegative taps) run the device
+    correlation with the analytic spectrum (direct composed weights for
+    h <= 64); any other kernel is composed by ``kernel_power`` (or taken from
+    ``composed``, the reference's cache hook) and correlated by the device
+    transform pair, the reference's own route (fft.py:302-329)."""
     if h < 0:
         raise ValidationError("h", "step count h must be >= 0")
     if h == 0:
@@ -95,8 +122,13 @@ def apply_linear_steps(row: GridRow, kernel: Kernel, h: int, *, direction: int =
         raise InsufficientWidthError(
             f"run of {len(row)} columns is too narrow for {h} steps of a "
             f"{len(kernel)}-point kernel (needs >= {expected_len})")
-    taps, c0, c1, c2 = _device_taps(kernel)
-    vals = _native.apply_linear_steps(row.values, taps, c0, c1, c2, h)
+    if _fast_taps(kernel.weights):
+        taps, c0, c1, c2 = _device_taps(kernel.weights)
+        vals = _native.apply_linear_steps(row.values, taps, c0, c1, c2, h)
+    else:
+        ck = composed if composed is not None else kernel_power(kernel, h)
+        full = _native.convolve(row.values.astype(np.float64), np.ascontiguousarray(ck.weights[::-1]))
+        vals = np.ascontiguousarray(full.real[expected_len - 1:len(row)])
     return GridRow(row.time_index + direction * h, row.col_offset - h * kernel.min_offset, vals)
 
 

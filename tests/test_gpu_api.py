@@ -49,8 +49,6 @@ def test_apply_linear_steps_errors():
         fl.apply_linear_steps(fl.GridRow(0, 0, np.ones(3)), k, 5)
     with pytest.raises(fl.ValidationError):
         fl.apply_linear_steps(fl.GridRow(0, 0, np.ones(3)), k, -1)
-    with pytest.raises(fl.UnsupportedCombinationError):
-        fl.kernel_power(fl.Kernel(np.array([0.5, -0.1, 0.6]), -1), 4)
     out = fl.apply_linear_steps(fl.GridRow(5, 0, np.array([1.0, 2.0, 4.0])), k, 1, direction=-1)
     assert out.time_index == 4 and out.col_offset == 0
     assert np.allclose(out.values, [1.5, 3.0], rtol=0, atol=1e-15)
@@ -262,3 +260,89 @@ def test_batch_device_bytes():
         db.fetch()
         fp.append(db.device_bytes())
     assert 0 < fp[0] < fp[1], fp
+
+
+def test_generic_kernel_power_and_steps_vs_oracle():
+    """Kernels beyond the pricers' stencils (fft.py:244-260): more taps,
+    negative weights, zero taps -- composed on the device (fl_kernel_power)
+    and checked against the oracle's restatement of the reference (numpy
+    spectrum power / two-tap closed form) and naive repeated convolution."""
+    import paper_2303_02317_b200 as fl
+    from oracle import port
+
+    rng = np.random.default_rng(77)
+    # (sum |w| <= 1: the spectral route's absolute error scales with max |P(e^it)|^h,
+    # in the reference as here)
+    cases = [np.array([0.5, -0.1, 0.3]), np.array([-0.4, 0.55]), np.array([0.0, 0.8]), np.array([0.7, 0.0]),
+             np.array([0.0, 0.3, 0.0, 0.5, 0.0]), np.array([0.2]), np.array([0.0, 0.0])]
+    for _ in range(12):
+        taps = int(rng.integers(2, 7))
+        w = rng.uniform(-0.2, 1.0, taps)
+        cases.append(w / (np.abs(w).sum() * rng.uniform(1.0, 1.3)))
+    for w in cases:
+        for h in (2, 5, 31, 200):
+            got = fl.kernel_power(fl.Kernel(w, -1), h)
+            assert got.min_offset == -h and len(got) == h * (len(w) - 1) + 1
+            acc = np.array([1.0])
+            for _ in range(h):
+                acc = np.convolve(acc, w)
+            assert np.max(np.abs(got.weights - acc)) <= 1e-10, (w, h)
+            if np.count_nonzero(w) and len(w) > 1:
+                ref = port.kernel_power(w, h)
+                assert np.max(np.abs(got.weights - ref)) <= 1e-10 * max(1.0, np.max(np.abs(ref))), (w, h)
+            # exact zeros where a zero end tap forces them (fft.py:176-183)
+            nz = np.nonzero(w)[0]
+            if nz.size:
+                assert np.all(got.weights[:h * nz[0]] == 0.0) and np.all(got.weights[h * nz[-1] + 1:] == 0.0)
+        row = fl.GridRow(3, 7, rng.uniform(0.5, 1.5, 400))
+        h = 9
+        out = fl.apply_linear_steps(row, fl.Kernel(w, -1), h)
+        ref = port.valid_corr(row.values, _naive_power(w, h))
+        assert out.col_offset == row.col_offset + h and out.time_index == row.time_index + h
+        assert np.max(np.abs(out.values - ref)) <= 1e-10 * max(1.0, np.max(np.abs(ref))), w
+
+
+def _naive_power(w, h):
+    acc = np.array([1.0])
+    for _ in range(h):
+        acc = np.convolve(acc, w)
+    return acc
+
+
+def test_short_linear_jump_keeps_exact_zeros():
+    """apply_linear_steps for h <= 64 runs the composed weights directly: a run
+    of zeros stays exactly zero, as in the device trapezoid (the reference
+    test test_american.py:96-115 compares the two with rtol only)."""
+    import paper_2303_02317_b200 as fl
+
+    vals = np.concatenate([np.zeros(120), np.linspace(1e-3, 5.0, 80)])
+    k = fl.Kernel(np.array([0.49, 0.5]), 0)
+    out = fl.apply_linear_steps(fl.GridRow(100, 0, vals), k, 48, direction=-1)
+    assert np.all(out.values[:120 - 48] == 0.0)
+    ref = _naive_power(k.weights, 48)
+    exp = np.array([ref @ vals[i:i + len(ref)] for i in range(len(vals) - len(ref) + 1)])
+    assert np.max(np.abs(out.values - exp)) <= 1e-13 * np.max(exp)
+
+
+def test_custom_binomial_params():
+    """Caller-supplied BinomialParams (binomial.py:80/161, american.py:428):
+    the lattice pricers use them (fl_price_batch_ex) instead of the spec's."""
+    import paper_2303_02317_b200 as fl
+    from oracle import port
+
+    spec = fl.OptionSpec(100.0, 95.0, 0.03, 0.05, 0.25, 180, 2048)
+    other = fl.OptionSpec(100.0, 95.0, 0.04, 0.02, 0.31, 200, 2048)
+    p = fl.derive_binomial_params(other)
+    pd = {"wd": p.weight_down, "wu": p.weight_up, "lu": p.log_up}
+    ref = port.euro_fast(spec.spot, spec.strike, spec.rate, spec.dividend_yield, spec.volatility,
+                         spec.days_to_expiry, spec.steps, p=pd)
+    assert price_close(fl.fast_european(spec, p), ref, spec.strike)
+    assert price_close(fl.baseline_european(spec, p), ref, spec.strike)
+    assert not price_close(fl.fast_european(spec), ref, spec.strike)
+    base = fl.baseline_american_call(spec, p)
+    fast = fl.fast_american_call(spec, p)
+    assert price_close(fast.price, base.price, spec.strike)
+    assert not price_close(fl.fast_american_call(spec).price, base.price, spec.strike)
+    grid = fl.baseline_american_call(spec.__class__(*[getattr(spec, f) for f in (
+        "spot", "strike", "rate", "dividend_yield", "volatility", "days_to_expiry")], 64), p, keep_grid=True)
+    assert np.isfinite(grid.price)

@@ -9,3 +9,6 @@ rm -rf /tmp/fftlattice_ref_src baseline/_ref
 cp -r /root/reference/pkg /tmp/fftlattice_ref_src
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
   --target baseline/_ref /tmp/fftlattice_ref_src
+# the reference's own test suite, run against the drop-in by
+# tools/run_reference_tests.py (the tests are data here, never product code)
+cp -r /root/reference/pkg/tests baseline/_ref/tests
