@@ -474,6 +474,26 @@ def batch_case():
     print(f"batch: {len(rows)} rows, reference exit code {rc}")
 
 
+def bench_case():
+    """The reference's own bench CSV (cli.py:653-720) for every method at two
+    step counts: its price column is the golden for benchcsv.py."""
+    import argparse
+    import contextlib
+    import io
+
+    from fftlattice import cli
+
+    buf = io.StringIO()
+    ns = argparse.Namespace(method=",".join(cli._BENCH_METHODS), steps="300,1024", spot=100.0, strike=100.0,
+                            rate=0.05, dividend_yield=0.03, vol=0.2, days=365, lam=0.4, reps=1, csv=None,
+                            parallel=False)
+    with contextlib.redirect_stdout(buf):
+        rc = cli.cmd_bench(ns)
+    with open(os.path.join(HERE, "bench_ref.csv"), "w") as fh:
+        fh.write(buf.getvalue())
+    print(f"bench: reference exit code {rc}")
+
+
 def verify_case():
     """The reference's own verify output (cli.py:598-616) for a fixed seed."""
     import argparse
@@ -520,3 +540,5 @@ if __name__ == "__main__":
         batch_case()
     if want("verify"):
         verify_case()
+    if want("bench"):
+        bench_case()

@@ -10,7 +10,7 @@ import os
 
 import pytest
 
-from conftest import GOLDEN
+from conftest import GOLDEN, price_close
 
 
 def _lines(text):
@@ -73,3 +73,10 @@ def test_benchcsv_schema_and_prices():
     assert len(rows) == 1 + 2 * len(benchcsv.BENCH_METHODS)
     for r in rows[1:]:
         assert float(r[2]) > 0.0 and float(r[3]) == float(r[3]) and r[4] == "2"
+    # the price column against the reference's own bench CSV (cli.py:653-720,
+    # tests/golden/bench_ref.csv, same spec and steps): rows in the same order
+    with open(os.path.join(GOLDEN, "bench_ref.csv")) as fh:
+        ref = list(_csv.reader(fh))
+    assert [r[:2] for r in rows] == [r[:2] for r in ref]
+    for got, want in zip(rows[1:], ref[1:]):
+        assert price_close(float(got[3]), float(want[3]), 100.0), (got, want)
