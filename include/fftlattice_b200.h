@@ -273,6 +273,11 @@ int fl_convolve(const double* x, int64_t nx, const double* y, int64_t ny, double
  * roofline denominator bench.py reports against. */
 int fl_probe_fp64(double* tflops, void* stream);
 
+/* Measured fp64 exp and log throughput of the current device (evaluations per
+ * second): the European path's roofline counts each at its DFMA-equivalent
+ * cost. */
+int fl_probe_transcendentals(double* exp_per_s, double* log_per_s, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

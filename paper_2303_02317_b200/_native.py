@@ -44,7 +44,7 @@ EXPORTED_SYMBOLS = (
     "fl_call_grid", "fl_put_march_rows", "fl_put_fast_rows", "fl_fft", "fl_convolve", "fl_euro_approx",
     "fl_probe_fp64", "fl_release_cache", "fl_shard_plan", "fl_price_batch_multi", "fl_price_batch_dev",
     "fl_price_put_bsm", "fl_price_american_call", "fl_price_european", "fl_dev_workspace_bytes", "fl_sync",
-    "fl_release_dev_cache", "fl_kernel_power", "fl_price_batch_ex",
+    "fl_release_dev_cache", "fl_kernel_power", "fl_price_batch_ex", "fl_probe_transcendentals",
 )
 
 
@@ -117,6 +117,8 @@ def lib():
         L.fl_euro_approx.restype = c_int
         L.fl_probe_fp64.argtypes = [P, P]
         L.fl_probe_fp64.restype = c_int
+        L.fl_probe_transcendentals.argtypes = [P, P, P]
+        L.fl_probe_transcendentals.restype = c_int
         L.fl_release_cache.argtypes = []
         L.fl_release_cache.restype = None
         L.fl_release_dev_cache.argtypes = []
@@ -376,6 +378,13 @@ def probe_fp64_tflops(stream=None) -> float:
     t = ctypes.c_double(0.0)
     _check(lib().fl_probe_fp64(ctypes.byref(t), ctypes.c_void_p(stream) if stream else None))
     return t.value
+
+
+def probe_transcendentals(stream=None):
+    """(exp, log) fp64 evaluations per second on the current device."""
+    a, b = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(lib().fl_probe_transcendentals(ctypes.byref(a), ctypes.byref(b), ctypes.c_void_p(stream) if stream else None))
+    return a.value, b.value
 
 
 def put_trapezoid(cd: float, cm: float, cu: float, ds: float, base_cutoff: int, f: int, seg: np.ndarray, h: int):

@@ -966,6 +966,12 @@ int fl_probe_fp64(double* tflops, void* stream) {
   return 0;
 }
 
+int fl_probe_transcendentals(double* exp_per_s, double* log_per_s, void* stream) {
+  if (!exp_per_s || !log_per_s) return fail("fl_probe_transcendentals: null output");
+  FL_CUDA(fl::probe_transcendentals(exp_per_s, log_per_s, (cudaStream_t)stream));
+  return 0;
+}
+
 void fl_batch_free(fl_batch* b) {
   if (!b) return;
   b->release();

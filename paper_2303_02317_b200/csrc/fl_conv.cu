@@ -78,6 +78,70 @@ cudaError_t probe_fp64(double* tflops, cudaStream_t stream) {
 // the truncated overlap-save FFT with the analytic spectrum (conv_fft).
 constexpr int LS_DIRECT_H = 64;
 
+// fp64 exp / log throughput probes (8 independent chains per thread): the
+// European path is transcendental-bound; its roofline counts
+// each exp / log at its measured DFMA-equivalent cost.
+__global__ void __launch_bounds__(1024) exp_probe_kernel(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 0.1 + 1e-3 * k + threadIdx.x * 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = exp(-x[k]);  // converges to the fixed point 0.567
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) log_probe_kernel(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 3.0 + 1e-3 * k + threadIdx.x * 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = log(x[k]) + 2.5;  // fixed point near 3.5
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+cudaError_t probe_transcendentals(double* exp_per_s, double* log_per_s, cudaStream_t stream) {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = 2 * nsm, block = 1024, iters = 256;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(double) * grid * block);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int which = 0; which < 2; ++which) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(e0, stream);
+      if (which == 0) exp_probe_kernel<<<grid, block, 0, stream>>>(d, rep == 0 ? 8 : iters);
+      else log_probe_kernel<<<grid, block, 0, stream>>>(d, rep == 0 ? 8 : iters);
+      cudaEventRecord(e1, stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0) best = ms < best ? ms : best;
+    }
+    const double evals = 8.0 * iters * (double)grid * block;
+    (which == 0 ? *exp_per_s : *log_per_s) = evals / (best * 1e-3);
+  }
+  e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return e;
+}
+
 __global__ void __launch_bounds__(CTA_THREADS)
 linear_steps_kernel(const double* __restrict__ x, int64_t L, double* __restrict__ y, int64_t Lout, int h,
                     Stencil st) {

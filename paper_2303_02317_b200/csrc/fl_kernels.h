@@ -46,6 +46,7 @@ __device__ __forceinline__ void apply_dlist(const BatchOut& out, Ptr& order, int
 
 void init_twiddles(cudaStream_t stream);
 cudaError_t probe_fp64(double* tflops, cudaStream_t stream);
+cudaError_t probe_transcendentals(double* exp_per_s, double* log_per_s, cudaStream_t stream);
 
 int64_t put_ws_doubles(int64_t n_max, int64_t ks_pos_max);
 int put_fast_smem_bytes();
