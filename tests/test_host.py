@@ -200,8 +200,9 @@ def test_api_argument_checks_before_device():
         fl.kernel_power(k, -1)
     with pytest.raises(fl.InsufficientWidthError):
         fl.apply_linear_steps(fl.GridRow(0, 0, np.ones(3)), k, 5)
-    with pytest.raises(fl.UnsupportedCombinationError):
-        fl.kernel_power(fl.Kernel(np.array([0.2, 0.2, 0.2, 0.2]), 0), 3)
+    with pytest.raises(fl.NumericalIntegrityError):  # non-finite weights never reach the device
+        fl.kernel_power(fl.Kernel(np.array([0.2, np.inf, 0.2, 0.2]), 0), 3)
+    assert np.array_equal(fl.kernel_power(fl.Kernel(np.zeros(3), -1), 4).weights, np.zeros(9))  # all-zero kernel
     with pytest.raises(fl.ValidationError):
         fl.Kernel(np.array([]), 0)
     spec = fl.OptionSpec(100.0, 100.0, 0.05, 0.0, 0.2, 365, 1024)
