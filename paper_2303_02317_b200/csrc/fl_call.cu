@@ -22,7 +22,12 @@
 
 namespace fl {
 
-constexpr int CALL_LEAF = 32;
+#ifndef FL_CALL_LEAF
+#define FL_CALL_LEAF 128
+#endif
+constexpr int CALL_LEAF = FL_CALL_LEAF;  // leaf strip height (<= 64: call_leaf_v4<CALL_LEAF / 32>)
+static_assert(CALL_LEAF == 32 || CALL_LEAF == 64 || CALL_LEAF == 128 || CALL_LEAF == 256,
+              "leaf strips hold 32 * 2^k <= 256 columns");
 #ifndef FL_CALL_HS
 #define FL_CALL_HS 256
 #endif
@@ -33,6 +38,7 @@ constexpr int CSUB_IN = 0, CSUB_ASM0 = CALL_HS + 8, CSUB_ASM1 = CSUB_ASM0 + CALL
               CSUB_ASM2 = CSUB_ASM1 + CALL_HS / 2 + 8;
 static_assert(CSUB_ASM2 + CALL_HS / 4 + 8 <= CHAIN_SCRATCH, "call subtree scratch");
 static_assert(CALL_HS <= 8 * CALL_LEAF, "three asm levels cover a subtree");
+static_assert(CALL_LEAF <= CALL_HS, "leaves inside the shared-memory subtrees");
 static_assert(CALL_HS / 2 <= KT_H, "subtree correlations use the kernel table");
 
 enum : int { TK_CALL_INIT = TK_USER + 4, TK_CALL_RESID = TK_USER + 5 };
@@ -56,8 +62,10 @@ __device__ __forceinline__ uint64_t call_ref_jump(int64_t L, int64_t M) {
   return 5ull * N * (uint64_t)lg + 3ull * N + 6ull;
 }
 
-constexpr int CALL_E2 = CHAIN_SCRATCH - 40;  // e2[k] = exp(2 k lu), k = 0..32, in the chain scratch
-static_assert(CALL_E2 >= CSUB_ASM2 + CALL_HS / 4 + 8, "e2 table above the call subtree scratch");
+constexpr int CALL_TAB = CALL_LEAF + 8;
+constexpr int CALL_E2 = CHAIN_SCRATCH - CALL_TAB;  // e2[k] = exp(2 k lu), k = 0..CALL_LEAF, in the chain scratch
+constexpr int CALL_BT = CALL_E2 - CALL_TAB;        // a leaf's row bases (CALL_LEAF >= 128)
+static_assert(CALL_BT >= CSUB_ASM2 + CALL_HS / 4 + 8, "e2 / base tables above the call subtree scratch");
 
 struct CallFrame {
   int64_t i, j, jm;
@@ -100,7 +108,8 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
                                              double* out_org, int64_t i, int64_t j, int h) {
   const long long t1 = clock64();
   double cells = 0.0;
-  const int64_t jp = call_leaf_v3(P, in_org, out_org, j - h + 1, i, j, h, &cells, X.scratch + CALL_E2);
+  const int64_t jp = call_leaf_v4<CALL_LEAF / 32>(P, in_org, out_org, j - h + 1, i, j, h, &cells, X.scratch + CALL_E2,
+                                                  X.scratch + CALL_BT);
   if (X.acct) X.flops += 5ull * (uint64_t)cells;
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
@@ -281,7 +290,7 @@ __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams
   const Stencil st{P.wd, P.wu, 0.0, 1};
   build_kernel_table(kc, st, scratch);
   __syncwarp();
-  for (int k = lane_id(); k <= 32; k += 32) scratch[CALL_E2 + k] = exp(2.0 * (double)k * P.lu);  // call_leaf_v3
+  for (int k = lane_id(); k < CALL_TAB; k += 32) scratch[CALL_E2 + k] = exp(2.0 * (double)k * P.lu);  // call_leaf_v4
   __syncwarp();
   if (lane_id() < 4) S.wkey[c][lane_id()] = -1;  // new option: new weights
   __syncwarp();
