@@ -37,10 +37,15 @@ namespace fl {
 #ifndef FL_PUT_LEAF
 #define FL_PUT_LEAF 64
 #endif
-constexpr int PUT_LEAF = FL_PUT_LEAF;                  // leaf strip height
-constexpr int PUT_CPL = (4 * PUT_LEAF + 2 + 31) / 32;  // cells per lane in a leaf strip
+// leaf strip heights: the sliding 2h+2 frame (options with the exercise
+// margin, PutParams::slide) and the full 4h+2 frame (the others; CPL 9 at 64)
+constexpr int PUT_LEAF = FL_PUT_LEAF;
+constexpr int PUT_LEAF_FULL = PUT_LEAF < 64 ? PUT_LEAF : 64;
+constexpr int PUT_CPL = (4 * PUT_LEAF_FULL + 2 + 31) / 32;  // cells per lane in a full-frame leaf strip
 constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 30) / 31;  // cells per lane (lane 0 is the ghost lane)
 constexpr int PUT_SLIDE_H = (31 * PUT_SLIDE_CPL - 2) / 2;      // tallest strip the frame holds
+template <int SL>
+__host__ __device__ constexpr int put_leaf_h() { return SL == 1 ? PUT_LEAF : PUT_LEAF_FULL; }
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
 #endif
@@ -58,7 +63,7 @@ constexpr int SUB_ASM2 = SUB_ASM1 + PUT_HS + 8;
 constexpr int SUB_END = SUB_ASM2 + PUT_HS / 2 + 8;
 constexpr int SUB_DEPTH = 5;
 static_assert(SUB_END <= CHAIN_SCRATCH, "subtree scratch");
-static_assert(PUT_HS <= 8 * PUT_LEAF, "three asm levels cover a subtree");
+static_assert(PUT_HS <= 8 * PUT_LEAF_FULL, "three asm levels cover a subtree");
 static_assert(PUT_HS / 2 <= KT_H, "subtree correlations use the kernel table");
 static_assert(2 * (2 * KT_H + 2) <= CHAIN_SCRATCH, "kernel-table scratch");
 
@@ -221,14 +226,14 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   const bool early = X.pay_ready;
   if (early) {
     warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
-    if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
+    if (h0 > put_leaf_h<SL>()) stash_weights(*X.S, X.c, X.wst, X.kc, h0, put_leaf_h<SL>(), 2);
   }
   const double* pay_s = s_pay - plo;
   wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
                  U(out_org + f0 + h0 + 1));
   if (!early) {
     warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
-    if (h0 > PUT_LEAF) stash_weights(*X.S, X.c, X.wst, X.kc, h0, PUT_LEAF, 2);
+    if (h0 > put_leaf_h<SL>()) stash_weights(*X.S, X.c, X.wst, X.kc, h0, put_leaf_h<SL>(), 2);
     X.pay_ready = true;
   }
   const long long t1 = clock64();
@@ -249,7 +254,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     const int h = F.h, h1 = (h + 1) / 2, h2 = h - h1;
     if (F.state == 0) {
       ref_node_enter(X, h, (sp >= 2) ? stk[sp - 2].h : ph0);
-      if (h <= PUT_LEAF) {
+      if (h <= put_leaf_h<SL>()) {
         const int64_t kb = put_leaf<ACCT, SL>(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
         if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
         ret = kb;
