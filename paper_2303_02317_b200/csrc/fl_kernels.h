@@ -70,6 +70,8 @@ int64_t sweep_max_cells();
 bool sweep_disabled();
 cudaError_t launch_put_sweep(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                              BatchOut out, cudaStream_t stream);
+cudaError_t launch_put_sweep_cluster(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max,
+                                     BatchOut out, cudaStream_t stream);
 cudaError_t launch_call_sweep(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                               BatchOut out, cudaStream_t stream);
 cudaError_t launch_euro_sweep(const EuroParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,

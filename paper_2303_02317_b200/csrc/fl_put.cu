@@ -814,6 +814,11 @@ cudaError_t launch_put_march_rows(const PutParams& P, const int64_t* times, int 
 cudaError_t launch_put_baseline(const PutParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                                 double* ws, int64_t ws_stride, BatchOut out, cudaStream_t stream) {
   if (nwork <= 0 || grid <= 0) return cudaSuccess;
+  if (!out.dlist) {  // a few options (count known on the host): a cluster of SMs per option
+    const cudaError_t e = launch_put_sweep_cluster(opts, order, nwork, n_max, out, stream);
+    if (e != cudaErrorNotSupported) return e;
+    (void)cudaGetLastError();
+  }
   if (2 * n_max + 1 <= sweep_max_cells() && !sweep_disabled()) return launch_put_sweep(opts, order, nwork, n_max, grid, out, stream);
   put_baseline_kernel<<<grid, CTA_THREADS, 0, stream>>>(opts, order, nwork, ws, ws_stride, out);
   return cudaGetLastError();
