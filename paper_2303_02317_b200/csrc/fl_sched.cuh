@@ -180,6 +180,7 @@ struct SchedShared {
   int claim[NRINGS];
   Pend pend[NCHAIN][PEND_CAP];
   int npend[NCHAIN];
+  int plo[NCHAIN];  // every pending entry below plo[c] is known finished (scan start)
   double result[NCHAIN];   // per-chain results of blocking tasks
   double result2[NCHAIN];
   int64_t iresult[NCHAIN];
@@ -266,6 +267,7 @@ __device__ void sched_init(SchedShared& S) {
   }
   if (threadIdx.x < NCHAIN) {
     S.npend[threadIdx.x] = 0;
+    S.plo[threadIdx.x] = 0;
     for (int q = 0; q < 2; ++q) {
       Mailbox& m = S.mb[threadIdx.x][q];
       m.seq = 0;
@@ -334,21 +336,31 @@ __device__ __forceinline__ void warp_wait_done(const SchedShared& S, int id) {
 
 // The chain's unfinished tasks conflicting with the given ranges, in issue
 // order, into out[0..min(n,cap)); returns n.
-__device__ int scan_conflicts(const SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
+__device__ int scan_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1, uintptr_t r2, uintptr_t r3,
                               uintptr_t w0, uintptr_t w1, int* out, int cap, int* rawf = nullptr) {
   const int np = S.npend[c];
-  const int first = np > PEND_CAP ? np - PEND_CAP : 0;
+  int first = np > PEND_CAP ? np - PEND_CAP : 0;
+  if (S.plo[c] > first) first = S.plo[c];
   int n = 0;
+  bool prefix = true;  // entries below the first unfinished one need no more scans
   for (int base = first; base < np; base += 32) {  // warp-uniform trip count
     const int i = base + lane_id();
-    bool hit = false, raw = false;
+    bool hit = false, raw = false, live = false;
     int id = 0;
     if (i < np) {
       const Pend& p = S.pend[c][i % PEND_CAP];
       id = p.id;
+      live = !task_done(S, id);
       raw = overlap(p.wlo, p.whi, r0, r1) || overlap(p.wlo, p.whi, r2, r3);
       const bool war = overlap(p.rlo, p.rhi, w0, w1) || overlap(p.wlo, p.whi, w0, w1);
-      hit = (raw || war) && !task_done(S, id);
+      hit = (raw || war) && live;
+    }
+    if (prefix) {
+      const unsigned lv = __ballot_sync(FULL, live);
+      const int adv = lv ? __ffs(lv) - 1 : (np - base < 32 ? np - base : 32);
+      if (lane_id() == 0) S.plo[c] = base + adv;
+      __syncwarp();
+      prefix = (lv == 0);
     }
     unsigned m = __ballot_sync(FULL, hit);
     const unsigned rm = __ballot_sync(FULL, raw);
