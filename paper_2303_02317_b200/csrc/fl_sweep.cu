@@ -357,6 +357,147 @@ __global__ void __launch_bounds__(NT) call_sweep_kernel(const CallParams* __rest
 }
 
 // ---------------------------------------------------------------------------
+// call / European, one option over a CLUSTER of C CTAs, time-tiled as
+// put_sweep_cluster_kernel.  The backward induction reads only the right
+// neighbour (wd v[j] + wu v[j+1]), so CTA r owns columns [a, b) and holds a
+// K-column halo on its right only; every K rows each CTA publishes its first
+// K owned columns for its left neighbour.  First-exercise records combine by
+// atomicMin (the identity INT64_MAX, turned into NO_GREEN at the end).
+
+template <int NT, int CPT, bool PROJ, int K>
+__global__ void __launch_bounds__(NT) call_sweep_cluster_kernel(const CallParams* __restrict__ copts,
+                                                                const EuroParams* __restrict__ eopts,
+                                                                const int32_t* __restrict__ order, int nwork,
+                                                                BatchOut out) {
+  apply_dlist(out, order, nwork);
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+  const int cid = blockIdx.x / C, ncl = gridDim.x / C;
+  __shared__ double exL[2][K];  // my first K owned columns, by tile parity
+  __shared__ double eL[2][NT];
+  __shared__ double sscale[2];
+  __shared__ int wfg[2][K][NT / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool rec = PROJ && out.bt != nullptr && out.cap > 0;
+  constexpr int NONE = 0x7fffffff;
+  constexpr long long REC_ID = 0x7fffffffffffffffll;  // atomicMin identity
+  for (int w = cid; w < nwork; w += ncl) {
+    const int o = order[w];
+    double S0, K0, wd, wu, lu;
+    int n;
+    if (PROJ) {
+      const CallParams& P = copts[o];
+      S0 = P.S; K0 = P.K; wd = P.wd; wu = P.wu; lu = P.lu; n = (int)P.n;
+    } else {
+      const EuroParams& E = eopts[o];
+      S0 = E.S; K0 = E.K; wd = E.wd; wu = E.wu; lu = E.lu; n = (int)E.n;
+    }
+    const int Wc = n + 1;
+    const int chunk = (Wc + C - 1) / C;
+    const int a = r * chunk < Wc ? r * chunk : Wc, b = (r + 1) * chunk < Wc ? (r + 1) * chunk : Wc;
+    const int c0 = a + t * CPT;
+    double v[CPT], u2[CPT];
+    int fg = NONE;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int j = c0 + c;
+      u2[c] = exp(__dmul_rn(__dsub_rn(2.0 * (double)j, (double)n), lu));
+      const double leaf = __dsub_rn(__dmul_rn(S0, u2[c]), K0);
+      v[c] = (j <= n && leaf > 0.0) ? leaf : 0.0;
+      if (PROJ && j < b && j <= n && leaf > 0.0 && fg == NONE) fg = j;
+    }
+    if (rec) {
+      for (int row = r + C * t; row <= n && row < out.cap; row += C * NT) {
+        out.bt[(int64_t)o * out.cap + row] = row;
+        out.bc[(int64_t)o * out.cap + row] = REC_ID;
+      }
+    }
+    if (PROJ && t == 0 && n >= 1) sscale[(n - 1) & 1] = __dmul_rn(S0, exp((double)1 * lu));
+    cl.sync();  // records initialised
+    if (rec) {  // the leaf row (step 0)
+      fg = warp_min_i32(fg);
+      if (lane == 0 && fg != NONE && n < out.cap)
+        atomicMin(reinterpret_cast<long long*>(out.bc + (int64_t)o * out.cap + n), (long long)fg);
+    }
+    auto flush_tile = [&](int i0, int qq) {  // rows i0, i0-1, .. of a finished tile
+      const int row = i0 - t;
+      if (rec && t < K && row >= 0 && row < out.cap) {
+        int m = NONE;
+        for (int wi = 0; wi < NT / 32; ++wi) m = wfg[qq][t][wi] < m ? wfg[qq][t][wi] : m;
+        if (m != NONE) atomicMin(reinterpret_cast<long long*>(out.bc + (int64_t)o * out.cap + row), (long long)m);
+      }
+    };
+    int tile = 0;
+    for (int i0 = n - 1; i0 >= 0; i0 -= K, ++tile) {
+      const int q = tile & 1;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int j = c0 + c;
+        if (j >= a && j < a + K) exL[q][j - a] = v[c];
+      }
+      cl.sync();
+      if (tile > 0) flush_tile(i0 + K, q ^ 1);
+      const double* nb = r + 1 < C ? cl.map_shared_rank(&exL[q][0], r + 1) : nullptr;  // right neighbour's first K
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int j = c0 + c;
+        if (nb && j >= b && j < b + K) v[c] = nb[j - b];
+      }
+      const int i1 = (i0 - K + 1 > 0) ? i0 - K + 1 : 0;
+      for (int i = i0; i >= i1; --i) {
+        const int bb = i & 1;
+        eL[bb][t] = v[0];
+        __syncthreads();
+        double scale = 0.0;
+        if (PROJ) {
+          scale = sscale[bb];
+          if (t == 0 && i >= 1) sscale[bb ^ 1] = __dmul_rn(S0, exp((double)(n - i + 1) * lu));
+        }
+        fg = NONE;
+        if (c0 <= i) {
+          const double right_edge = (t < NT - 1) ? eL[bb][t + 1] : 0.0;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            const int j = c0 + c;
+            const double right = (c + 1 < CPT) ? v[c + 1] : right_edge;
+            const bool in = j <= i;
+            const double lin = __dadd_rn(__dmul_rn(wd, v[c]), __dmul_rn(wu, right));
+            if (PROJ) {
+              const double grn = __dsub_rn(__dmul_rn(scale, u2[c]), K0);
+              const bool red = lin >= grn;
+              v[c] = in ? (red ? lin : grn) : v[c];
+              fg = (in && !red && fg == NONE && j < b) ? j : fg;
+            } else {
+              v[c] = in ? lin : v[c];
+            }
+          }
+        }
+        if (rec) {
+          fg = warp_min_i32(fg);
+          if (lane == 0) wfg[q][i0 - i][warp] = fg;
+        }
+      }
+    }
+    __syncthreads();
+    if (tile > 0) flush_tile(n - 1 - (tile - 1) * K, (tile - 1) & 1);
+    cl.sync();  // every record combined: the untouched identities are NO_GREEN
+    if (rec) {
+      for (int row = r + C * t; row <= n && row < out.cap; row += C * NT) {
+        long long* pc = reinterpret_cast<long long*>(out.bc + (int64_t)o * out.cap + row);
+        if (*pc == REC_ID) *pc = SWEEP_NO_REC;
+      }
+    }
+    if (r == 0 && t == 0) {
+      out.price[o] = v[0];
+      out.status[o] = 0;
+      if (out.bcount) out.bcount[o] = PROJ ? n + 1 : 0;
+    }
+    __syncthreads();
+  }
+  cl.sync();
+}
+
+// ---------------------------------------------------------------------------
 // launchers: the smallest tile that holds the batch's widest row
 
 struct SweepTile {
@@ -460,13 +601,56 @@ static cudaError_t launch_call_sweep_t(const CallParams* copts, const EuroParams
   return cudaGetLastError();
 }
 
+template <int NT, int CPT, bool PROJ>
+static cudaError_t launch_call_cluster_t(const CallParams* copts, const EuroParams* eopts, const int32_t* order,
+                                         int nwork, int C, BatchOut out, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(C * nwork), 1, 1);
+  cfg.blockDim = dim3(NT, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, call_sweep_cluster_kernel<NT, CPT, PROJ, SWEEP_K>, copts, eopts, order, nwork, out);
+}
+
+// a few call / European options: a cluster of SMs per option (cudaErrorNotSupported otherwise)
+template <bool PROJ>
+static cudaError_t launch_call_sweep_cluster(const CallParams* copts, const EuroParams* eopts, const int32_t* order,
+                                             int nwork, int64_t n_max, BatchOut out, cudaStream_t stream) {
+  if (out.dlist || sweep_disabled()) return cudaErrorNotSupported;
+  int dev = 0, nsm = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  const int64_t W = n_max + 1;
+  int C = 8;
+  while (C > 1 && (C * nwork > nsm || (W + C - 1) / C < 2 * SWEEP_K)) C >>= 1;
+  if (C < 2) return cudaErrorNotSupported;
+  const int64_t ext = (W + C - 1) / C + SWEEP_K;
+  if (ext <= 128 * 2) return launch_call_cluster_t<128, 2, PROJ>(copts, eopts, order, nwork, C, out, stream);
+  if (ext <= 256 * 4) return launch_call_cluster_t<256, 4, PROJ>(copts, eopts, order, nwork, C, out, stream);
+  if (ext <= 256 * 8) return launch_call_cluster_t<256, 8, PROJ>(copts, eopts, order, nwork, C, out, stream);
+  if (ext <= 512 * 8) return launch_call_cluster_t<512, 8, PROJ>(copts, eopts, order, nwork, C, out, stream);
+  return cudaErrorNotSupported;
+}
+
 cudaError_t launch_call_sweep(const CallParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                               BatchOut out, cudaStream_t stream) {
+  const cudaError_t e = launch_call_sweep_cluster<true>(opts, nullptr, order, nwork, n_max, out, stream);
+  if (e != cudaErrorNotSupported) return e;
   return launch_call_sweep_t<true>(opts, nullptr, order, nwork, n_max, grid, out, stream);
 }
 
 cudaError_t launch_euro_sweep(const EuroParams* opts, const int32_t* order, int nwork, int64_t n_max, int grid,
                               BatchOut out, cudaStream_t stream) {
+  const cudaError_t e = launch_call_sweep_cluster<false>(nullptr, opts, order, nwork, n_max, out, stream);
+  if (e != cudaErrorNotSupported) return e;
   return launch_call_sweep_t<false>(nullptr, opts, order, nwork, n_max, grid, out, stream);
 }
 

@@ -97,3 +97,35 @@ def test_multi_device_entry_matches_single():
     p, st = fl.price_batch_multi(*f, devices=[0])
     assert np.array_equal(st, ref.status)
     assert p.tobytes() == ref.price.tobytes()
+
+
+@pytest.mark.parametrize("kind,T", [(2, 4096), (2, 777), (1, 4096), (1, 1500), (0, 3000)])
+def test_sweep_cluster_vs_per_cta(kind, T):
+    """O(T^2) baselines: one option alone runs on a cluster of SMs
+    (put_sweep_cluster_kernel / call_sweep_cluster_kernel, DSMEM halos);
+    the same option inside a 160-option batch runs on one CTA.  Price and
+    every boundary record must agree to the bit."""
+    from paper_2303_02317_b200 import _native
+
+    n = 160
+    rng = np.random.default_rng(kind * 100 + T)
+    S = np.full(n, 100.0) if kind == 2 else rng.uniform(80, 120, n)
+    K = np.full(n, 100.0)
+    R = np.full(n, 0.05)
+    Y = np.full(n, 0.0 if kind == 2 else 0.03)
+    V = rng.uniform(0.2, 0.4, n)
+    E = np.full(n, 365.0)
+    ks, Ts = np.full(n, kind, np.int8), np.full(n, T, np.int64)
+
+    def run(sel):
+        return _native.price_batch_full(ks[sel], S[sel], K[sel], R[sel], Y[sel], V[sel], E[sel], Ts[sel],
+                                        lam=0.4, method=_native.METHOD_BASELINE, bnd_cap=T + 2)
+
+    batch = run(np.arange(n))
+    assert np.all(batch.status == 0)
+    for i in (0, 77):
+        one = run(np.array([i]))
+        assert one.status[0] == 0
+        assert _same(batch, i, one, 0), (kind, T, i)
+        if kind == 1:
+            assert len(one.boundary(0)[0]) == T + 1
