@@ -8,6 +8,8 @@
 //   put_strip_ghost2   ghost-lane frame, two rows per neighbour exchange
 //   put_strip_tiled    full frame, K rows per exchange (halo recompute)
 //   call_leaf_warp / call_leaf_v2 / call_leaf_tiled<K>   call strips
+//   put_strip_ghost_rot<CPL, ROT>  the production ghost strip with a rotating
+//                      payoff file (ROT & 1) and / or integer-pipe compares (ROT & 2)
 #pragma once
 
 #include "../paper_2303_02317_b200/csrc/fl_callstrip.cuh"
@@ -598,5 +600,140 @@ __device__ int64_t call_leaf_tiled(const CallParams& P, const double* __restrict
   return jp;
 }
 
+
+// ---------------------------------------------------------------------------
+// put_strip_ghost variants (tools/strip_rot_bench.cu, profiles/r02_experiments.md)
+
+// The same projection with the comparison on the integer pipe.  For lin >= +0
+// (non-negative weights times non-negative values) the IEEE bit patterns of
+// lin and pay order as signed 64-bit integers exactly as the doubles do
+// (a negative payoff has the sign bit set and compares below every lin),
+// except lin = +0 against pay = -0 (equal values; the payoff table never
+// holds -0).  Two ISETP replace one DSETP, which would occupy the FP64 pipe
+// that the strip's DMUL / DFMA already saturate when two chains share an SMSP.
+__device__ __forceinline__ double proj_max_i(double lin, double pay) {
+  return __double_as_longlong(lin) > __double_as_longlong(pay) ? lin : pay;
+}
+template <int ICMP>
+__device__ __forceinline__ double proj_sel(double lin, double pay) {
+  if constexpr (ICMP) return proj_max_i(lin, pay);
+  return proj_max(lin, pay);
+}
+
+
+// One row of put_strip_ghost at compile-time phase T of a rotating payoff file
+// (see FL_STRIP_ROT below); np0 is the new row's cell-0 payoff.
+template <int CPL, int T, int ICMP>
+__device__ __forceinline__ void ghost_rot_row(double (&u)[CPL], double (&P)[CPL], double np0, double cd, double cm,
+                                              double cu) {
+  const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+  const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+  double lin[CPL];
+#pragma unroll
+  for (int c = CPL - 1; c >= 2; --c) lin[c] = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+  lin[1] = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+  lin[0] = fma(cd, L2, fma(cu, u[0], cm * L1));
+  P[(CPL - 1 - T) % CPL] = np0;  // the leaving cell's slot becomes the new cell 0
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) u[c] = proj_sel<ICMP>(lin[c], P[(c - T - 1 + 2 * CPL) % CPL]);
+}
+
+template <int CPL, int ICMP, int T = 0>
+__device__ __forceinline__ void ghost_rot_group(double (&u)[CPL], double (&P)[CPL], double& np0, const double* pq0,
+                                                int s0, double cd, double cm, double cu) {
+  if constexpr (T < CPL) {
+    const double cur = np0;
+    np0 = pq0[-(s0 + T + 1)];
+    ghost_rot_row<CPL, T, ICMP>(u, P, cur, cd, cm, cu);
+    ghost_rot_group<CPL, ICMP, T + 1>(u, P, np0, pq0, s0, cd, cm, cu);
+  }
+}
+
+template <int CPL, int ROT, int PAYLDS = 0>
+__device__ int64_t put_strip_ghost_rot(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 2, "two left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = (lane - 1) * CPL;  // lane 0: cells -CPL .. -1
+  // cells past the frame (idle lanes, the tail of the last lane) read the
+  // frame's last column; their values never reach a cell j < W
+  const double* pay0 = pay_org + (f - 1);
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] == 12345.678 ? 1 : 0); }
+  // row s+1 payoff of cell j: col f-s-2+j = pay0[j - 1 - s]
+  const double* pq0 = pay0 - 1 + jx[0];
+  double np0 = pq0[0];
+  unsigned green = 0;
+  int s0 = 0;
+  if constexpr ((ROT & 1) != 0) {
+  // rows in groups of CPL with the payoffs in a rotating register file: at
+  // phase t cell c's payoff is P[(c - t) mod CPL], so the one-cell shift per
+  // row costs no register moves (the new cell-0 payoff takes the slot of the
+  // cell that leaves); after a whole group P is in cell order again
+    for (; s0 + CPL <= height; s0 += CPL) ghost_rot_group<CPL, (ROT >> 1) & 1>(u, p, np0, pq0, s0, cd, cm, cu);
+  }
+  // unrolled by 2 only: in the kernel the strip shares the SM's instruction
+  // cache with every other role, and a longer body measured slower there
+  // (4 -> 14.2, 5 -> 14.8, 10 -> 15.8 ms; 2 -> 14.0 ms) although faster alone
+#pragma unroll 2
+  for (int s = s0; s < height; ++s) {
+    const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    double np[CPL];
+    if (PAYLDS) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) np[c] = pay0[jx[c] - 1 - s];
+    } else {
+      np[0] = np0;
+#pragma unroll
+      for (int c = 1; c < CPL; ++c) np[c] = p[c - 1];
+      np0 = pq0[-(s + 1)];  // next row's first-cell payoff
+    }
+    double nu[CPL];
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) {
+      const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+      nu[c] = proj_sel<(ROT >> 1) & 1>(lin, np[c]);
+    }
+    const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+    const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
+    nu[1] = proj_sel<(ROT >> 1) & 1>(lin1, np[1]);
+    nu[0] = proj_sel<(ROT >> 1) & 1>(lin0, np[0]);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      u[c] = nu[c];
+      p[c] = np[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c >= 0 && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
 
 }  // namespace fl
