@@ -19,7 +19,7 @@ struct AmericanPricer {
     const int e = order[w];
     if (e >= 0) {
       double ref = 0.0;
-      put_chain_option<ACCT>(S, c, put[e], e, arena, scratch, out, flops, &ref);
+      put_chain_option_retry<ACCT>(S, c, put[e], e, arena, scratch, out, flops, &ref);
       if (lane_id() == 0 && out.flops) atomicAdd(out.flops + 1, (unsigned long long)ref);
     } else {
       const int o = -e - 1;

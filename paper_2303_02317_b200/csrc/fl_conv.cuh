@@ -181,39 +181,20 @@ __device__ __forceinline__ void dit_stage(double2* buf, int logC, int logS, cons
   gsync(g);
 }
 
-// Stage plan of a C = 2^logC transform over a group of gn threads: per DIF
-// stage (largest span first) the radix log, the largest radix that still
-// gives every thread of the group a butterfly (C/R >= gn), else the largest
-// radix that fits.  Small blocks on a 4-warp group thus run radix-4/8 stages
-// with every thread busy instead of radix-16 stages on a quarter of them.
-#ifndef FL_FFT_PLAN  // 0: radix-16 stages + one remainder stage (round-1 schedule)
-#define FL_FFT_PLAN 0  // measured: every-thread-busy radix 4/8 stages are slower (N = 1024 task 9.9k -> 13.2k cycles)
-#endif
+// Stage plan of a C = 2^logC transform: radix-16 stages from the largest span
+// down, then one remainder stage of radix 2^last (last = last_radix_log).
+// Computed from logC in registers (a stage array in local memory cost a local
+// load per stage and four per spectrum bin pair).  (Measured alternative:
+// radix 4/8 stages keeping every group thread busy -- slower, N = 1024 task
+// 9.9k -> 13.2k cycles, profiles/r01_experiments.md.)
 struct FftPlan {
-  int n;
-  int lr[16];
+  int n16;   // radix-16 stages
+  int last;  // log2 radix of the remainder stage (1..4)
 };
-__device__ __forceinline__ FftPlan fft_plan(int logC, int gn) {
+__device__ __forceinline__ FftPlan fft_plan(int logC, int /*gn*/) {
   FftPlan p;
-  p.n = 0;
-  int rem = logC;
-#if FL_FFT_PLAN
-  while (rem > 0) {
-    int l = 0;
-    for (int c = 4; c >= 1 && !l; --c)
-      if (c <= rem && (1 << (logC - c)) >= gn) l = c;
-    if (!l) l = rem < 4 ? rem : 4;
-    p.lr[p.n++] = l;
-    rem -= l;
-  }
-#else
-  const int last = last_radix_log(logC);
-  while (rem > last) {
-    p.lr[p.n++] = 4;
-    rem -= 4;
-  }
-  p.lr[p.n++] = last;
-#endif
+  p.last = last_radix_log(logC);
+  p.n16 = (logC - p.last) >> 2;
   return p;
 }
 
@@ -230,34 +211,35 @@ __device__ __forceinline__ void fft_stage(double2* buf, int lr, int logC, int lo
 // Forward: natural order in, X[k] at slot P(k) out.
 __device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
   int logS = logC;
-  for (int s = 0; s < pl.n; ++s) {
-    fft_stage<true>(buf, pl.lr[s], logC, logS, tq, g);
-    logS -= pl.lr[s];
+#pragma unroll 1
+  for (int s = 0; s < pl.n16; ++s) {
+    dif_stage<16>(buf, logC, logS, tq, g);
+    logS -= 4;
   }
+  fft_stage<true>(buf, pl.last, logC, logS, tq, g);
 }
 
 // Inverse (unnormalised, x C): slot P(k) in, natural order out.
 __device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
-  int logS = 0;
-  for (int s = pl.n - 1; s >= 0; --s) {
-    logS += pl.lr[s];
-    fft_stage<false>(buf, pl.lr[s], logC, logS, tq, g);
+  int logS = pl.last;
+  fft_stage<false>(buf, pl.last, logC, logS, tq, g);
+#pragma unroll 1
+  for (int s = 0; s < pl.n16; ++s) {
+    logS += 4;
+    dit_stage<16>(buf, logC, logS, tq, g);
   }
 }
 
-// Slot holding frequency k after fft_dif: the mixed-radix digits of k (first
-// stage's radix least significant) written most-significant-first into the
-// slot index.
+// Slot holding frequency k after fft_dif: the base-16 digits of k (the first
+// stage's digit least significant) in reverse order, then the remainder
+// digit: slot = nibble_reverse(k mod 16^n16) << last | k >> 4 n16.
 __device__ __forceinline__ int slot_of(int k, int logC, const FftPlan& pl) {
-  int p = 0;
-  int logS = logC;
-#pragma unroll 1
-  for (int s = 0; s < pl.n; ++s) {
-    logS -= pl.lr[s];
-    p |= (k & ((1 << pl.lr[s]) - 1)) << logS;
-    k >>= pl.lr[s];
-  }
-  return p;
+  const int lo = 4 * pl.n16;
+  unsigned x = __brev((unsigned)k & ((1u << lo) - 1u));  // bit-reversed, nibbles internally reversed
+  x = ((x & 0x33333333u) << 2) | ((x >> 2) & 0x33333333u);
+  x = ((x & 0x55555555u) << 1) | ((x >> 1) & 0x55555555u);
+  x = lo ? (x >> (32 - lo)) : 0u;
+  return (int)((x << pl.last) | ((unsigned)k >> lo));
 }
 
 // ---------------------------------------------------------------------------

@@ -159,11 +159,18 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
 }
 
+#ifndef FL_FIXED_STRIP
+#define FL_FIXED_STRIP 1
+#endif
+// Internal status (never reported): a fixed-frame leaf saw the exercise region
+// reach its left margin; the option is priced again on the full frame.
+constexpr int32_t FL_RETRY_FULL = 0x7f01;
+
 // Leaf strip on the chain warp.  in_org / out_org / pay_org may address shared memory.
-// SL: 1 the sliding frame (the caller guarantees P.slide, height <= PUT_SLIDE_H
-// and hi == f + 2 height), 0 the full frame, -1 decided here.  The subtree
-// walk is instantiated per strip kind so the hot walk carries one strip only
-// (instruction-cache footprint).
+// SL: 1 the sliding / fixed frame (the caller guarantees P.slide, height <=
+// PUT_SLIDE_H and hi == f + 2 height), 0 the full frame, -1 decided here.  The
+// subtree walk is instantiated per strip kind so the hot walk carries one strip
+// only (instruction-cache footprint).
 template <bool ACCT = true, int SL = -1>
 __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, const double* in_org,
                                             double* out_org, const double* pay_org, int64_t lo, int64_t hi,
@@ -172,12 +179,27 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   long long tm[2] = {0, 0};
   FL_TR(*X.S, X.c, EV_LEAF_B, height);
   // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
-  const int64_t kb =
-      (SL == 1 || (SL < 0 && P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height))
-          ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
-                                              FL_PROFP(X.prof) ? tm : nullptr)
-          : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                    FL_PROFP(X.prof) ? tm : nullptr);
+  const bool slide = SL == 1 || (SL < 0 && P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height);
+  int64_t kb;
+#if FL_FIXED_STRIP
+  if (slide) {
+    kb = put_strip_fixed<PUT_SLIDE_CPL>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
+                                        FL_PROFP(X.prof) ? tm : nullptr);
+    // the exercise region reached the frame's left margin: inside a subtree
+    // (SL 1) the caller re-prices the option on the full frame; elsewhere the
+    // full frame runs here
+    if (SL != 1 && kb == FIXED_MISS)
+      kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu);
+  } else {
+    kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
+                                 FL_PROFP(X.prof) ? tm : nullptr);
+  }
+#else
+  kb = slide ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
+                                                 FL_PROFP(X.prof) ? tm : nullptr)
+             : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
+                                       FL_PROFP(X.prof) ? tm : nullptr);
+#endif
   FL_TR(*X.S, X.c, EV_LEAF_E, height);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
@@ -256,7 +278,10 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
       ref_node_enter(X, h, (sp >= 2) ? stk[sp - 2].h : ph0);
       if (h <= put_leaf_h<SL>()) {
         const int64_t kb = put_leaf<ACCT, SL>(X, P, F.in, F.out, pay_s, F.f - 2 * h - 1, F.f + 2 * h, F.f, h);
-        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) { *err = FL_E_GEOMETRY | 1; return 0; }
+        if (kb == NONE_SEEN || kb < F.f - h || kb > F.f) {
+          *err = (SL == 1 && kb == FIXED_MISS) ? FL_RETRY_FULL : FL_E_GEOMETRY | 1;
+          return 0;
+        }
         ret = kb;
         --sp;
         continue;
@@ -432,8 +457,10 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
 }
 
 // fast_put_bsm's stage loop (bsm.py:626-676) for option o on chain warp c.
+// Returns the status; FL_RETRY_FULL leaves no output (the caller re-prices the
+// option with P.slide = 0).
 template <bool ACCT>
-__device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
+__device__ int32_t put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
                                  double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
   const long long t_opt = clock64();
   const int64_t n = P.n, ks = P.ks;
@@ -501,6 +528,11 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
     nxt_org = t;
   }
   wait_all_own(S, c);  // the next option reuses this arena
+  if (err == FL_RETRY_FULL) {
+    if (out.snap && lane_id() == 0) out.snap_len[o] = 0;
+    __syncwarp();
+    return err;
+  }
   if (lane_id() == 0) {
     out.price[o] = err ? 0.0 : price;
     out.status[o] = err;
@@ -509,6 +541,16 @@ __device__ void put_chain_option(SchedShared& S, int c, const PutParams& P, int 
   }
   *chain_flops += (double)X.flops;
   *ref_flops += (double)X.ref_flops;
+  return err;
+}
+
+// put_chain_option with the full-frame re-run (at most one).
+template <bool ACCT>
+__device__ void put_chain_option_retry(SchedShared& S, int c, const PutParams& P0, int o, double* arena,
+                                       double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
+  PutParams P = P0;
+  while (put_chain_option<ACCT>(S, c, P, o, arena, scratch, out, chain_flops, ref_flops) == FL_RETRY_FULL)
+    P.slide = 0;
 }
 
 // Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
@@ -569,7 +611,7 @@ struct PutPricer {
   __device__ void chain(SchedShared& S, int c, int w, double* arena, double* scratch, double* flops) const {
     double ref = 0.0;
     const int o = order[w];
-    put_chain_option<ACCT>(S, c, opts[o], o, arena, scratch, out, flops, &ref);
+    put_chain_option_retry<ACCT>(S, c, opts[o], o, arena, scratch, out, flops, &ref);
     if (lane_id() == 0 && out.flops) atomicAdd(out.flops + 1, (unsigned long long)ref);
   }
   __device__ double exec(SchedShared& S, const Task& t, double2* sbuf, int slots, int logN, const double2* tq,
@@ -606,8 +648,16 @@ struct PutTrapPricer {
     double* cur_org = arena - Lo.colbase;
     double* nxt_org = arena + Lo.span - Lo.colbase;
     int32_t err = 0;
-    const int64_t kp = put_stage(X, P, f, W, h, cur_org, nxt_org, &err);
+    PutParams Q = P;
+    int64_t kp = put_stage(X, Q, f, W, h, cur_org, nxt_org, &err);
     wait_all_own(S, c);
+    if (err == FL_RETRY_FULL) {  // a fixed-frame leaf lost its margin: full frame
+      Q.slide = 0;
+      err = 0;
+      X = put_chain_setup(S, c, Q, Lo, 2 * h, arena, scratch, nullptr, seg, f + 1, W);
+      kp = put_stage(X, Q, f, W, h, cur_org, nxt_org, &err);
+      wait_all_own(S, c);
+    }
     const int64_t len = err ? 0 : (f + W - h) - kp;
     for (int64_t i = lane_id(); i < len; i += 32) out[i] = nxt_org[kp + 1 + i];
     if (lane_id() == 0) {

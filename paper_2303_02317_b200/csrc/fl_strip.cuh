@@ -217,4 +217,99 @@ __device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __
   return kb;
 }
 
+constexpr int64_t FIXED_MISS = NONE_SEEN - 1;  // put_strip_fixed: left edge not exercise, nothing written
+
+// Fixed-column put strip with a ghost lane (production leaf).  Same contract as
+// put_strip_ghost, but the frame does not slide: lanes 1..31 hold the columns
+// base .. f+2h (cell j = column base + j, CPL consecutive cells per lane,
+// base = f - M with M = min(31 CPL - 2h - 1, 2h) exercise columns left of f;
+// 2h + 2 <= 31 CPL),
+// so a cell keeps its payoff in a register for the whole strip: no payoff
+// shift and no payoff load per row (the sliding frame spends ~10 register
+// moves and a shared load per row on them -- in the kernel two chain warps
+// share one SMSP and the strip is issue-bound, ncu source view round 3).
+// Per row a lane exchanges one cell with each neighbour (two shuffle
+// directions, the same four 32-bit shuffles as the sliding frame).
+//   * right side: as in the sliding frame, garbage enters at column f+2h+1 and
+//     moves left one column per row, never reaching the valid range
+//     [f-h-1, f+h] of the last row (_accel.py:203-242);
+//   * left side: every column < base is an exercise cell at every row as long
+//     as column base is (a cell whose three parents are exercise cells stays
+//     exercise, PutParams::slide margin, see put_strip_ghost).  Lane 0 is the
+//     ghost lane (cols base-CPL .. base-1, values exactly their payoffs, its
+//     shuffled-in left inputs come from its own lower-payoff cells).  Column
+//     base is checked on every row; if it ever turns continuation the strip
+//     writes nothing and returns FIXED_MISS (the caller reruns the full frame).
+// Per-cell arithmetic is put_strip_ghost's (bit-identical results).
+// pay_org must cover cols f-2h-1 .. f+2h (the reference strip's frame).
+template <int CPL>
+__device__ int64_t put_strip_fixed(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int h = height;
+  // margin: what the frame's 31 CPL cells leave, at most 2h (column base-1
+  // stays inside the reference frame [f-2h-1, f+2h])
+  const int Mx = 31 * CPL - 2 * h - 1;
+  const int M = Mx < 2 * h ? Mx : 2 * h;
+  const int64_t base = f - M;
+  const int W = M + 2 * h + 1;      // frame cells base .. f+2h
+  const int j0 = (lane - 1) * CPL;  // lane 0: cells -CPL .. -1
+  double v[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = (j0 + c < W) ? j0 + c : W - 1;
+    int64_t col = base + j;
+    // ghost cells left of the reference frame read its first column: a lower
+    // payoff only lowers the ghost lane's lin, and the ghost cell next to the
+    // frame (column base-1 >= f-2h-1) is exact
+    col = col < f - 2 * h - 1 ? f - 2 * h - 1 : col;
+    p[c] = pay_org[col];
+    v[c] = (col <= f) ? p[c] : in_org[col];
+  }
+  __syncwarp();
+  long long ta = 0;
+  if (tm) { ta = clock64() + (long long)(v[0] + p[0] == 12345.678 ? 1 : 0); }
+  bool cont0 = false;  // lane 1: column base turned continuation on some row
+#pragma unroll 2
+  for (int s = 0; s < h; ++s) {
+    const double L = __shfl_up_sync(FULL, v[CPL - 1], 1);
+    const double R = __shfl_down_sync(FULL, v[0], 1);
+    double nv[CPL];
+    {
+      const double lin = fma(cd, L, fma(cu, v[1], cm * v[0]));
+      cont0 |= lin > p[0];
+      nv[0] = proj_max(lin, p[0]);
+    }
+#pragma unroll
+    for (int c = 1; c < CPL - 1; ++c) {
+      const double lin = fma(cd, v[c - 1], fma(cu, v[c + 1], cm * v[c]));
+      nv[c] = proj_max(lin, p[c]);
+    }
+    {
+      const double lin = fma(cd, v[CPL - 2], fma(cu, R, cm * v[CPL - 1]));
+      nv[CPL - 1] = proj_max(lin, p[CPL - 1]);
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = nv[c];
+  }
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(v[0] == 12345.678 ? 1 : 0) - ta; }
+  if (__shfl_sync(FULL, cont0 ? 1 : 0, 1)) return FIXED_MISS;
+  // last exercise column of the final row within the valid range (cols <= f+h)
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (v[c] == p[c] && j0 + c >= 0 && j0 + c <= M + h) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j <= M + h) out_org[base + j] = v[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
 }  // namespace fl

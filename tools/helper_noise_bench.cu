@@ -1,0 +1,211 @@
+// Leaf strip (production put_strip_fixed<5>, h = 64, warp 3 = SMSP 3) against
+// the co-resident work the kernel actually runs next to it: the helper warps'
+// shared-memory correlations (conv_direct_blk, the subtree's mid / bottom
+// jumps), FP64 FMA streams on the other SMSPs, and spin polls of shared flags.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/bin/helper_noise_bench tools/helper_noise_bench.cu
+#include <cstdio>
+#include <vector>
+#include <cmath>
+#include "../paper_2303_02317_b200/csrc/fl_sched.cuh"
+#include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+using namespace fl;
+constexpr int NC = 1201, C0 = -600;
+constexpr double CD = 0.39790368627109396, CM = 0.199951171875, CU = 0.4020963137289061;
+constexpr int HM = 129, HL = 64;  // helper correlation: 129 taps (h = 64), 64 outputs
+constexpr int HX = HL + HM + 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(512, 1) k(const double* in, const double* pay, long long* cyc, int reps, int height,
+                                           long long f, volatile int* stop, long long* hcount) {
+  __shared__ double spay[NC], sin_[NC], sout[NC];
+  __shared__ double hx[4][HX], hw[4][HM + 8], hy[4][HL + 8];
+  __shared__ volatile int flag[32];
+  for (int i = threadIdx.x; i < NC; i += blockDim.x) { spay[i] = pay[i]; sin_[i] = in[i]; }
+  for (int i = threadIdx.x; i < 4 * HX; i += blockDim.x) (&hx[0][0])[i] = 1.0 / (i + 1);
+  for (int i = threadIdx.x; i < 4 * (HM + 8); i += blockDim.x) (&hw[0][0])[i] = 0.01 * (i % 7);
+  if (threadIdx.x < 32) flag[threadIdx.x] = 0;
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == 3) {
+    long long t0 = clock64();
+    int64_t acc = 0;
+    for (int r = 0; r < reps; ++r) acc += put_strip_fixed<5>(sin_ - C0, sout - C0, spay - C0, f, height, CD, CM, CU);
+    long long t1 = clock64();
+    if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = acc; *stop = 1; }
+    return;
+  }
+  // noise roles
+  int nh = 0;      // helper correlations on warps 0..nh-1 (SMSPs 0, 1, 2, 0)
+  int nfma = 0;    // FP64 FMA streams on warps 4..
+  int npoll = 0;   // pollers
+  int kind = 0;
+  if (MODE == 1) nh = 2;
+  if (MODE == 2) nh = 4;
+  if (MODE == 3) nfma = 9;
+  if (MODE == 4) { nh = 2; kind = 1; }
+  if (MODE == 5) npoll = 6;
+  if (MODE == 6) { nh = 2; nfma = 6; }
+  const int wid = (w < 3) ? w : (w == 4 ? 3 : -1);  // helpers: warps 0, 1, 2, 4
+  long long done = 0;
+  if (wid >= 0 && wid < nh) {
+    while (!*stop) {
+      if (kind == 0) conv_direct_blk(hx[wid], hy[wid], HL, hw[wid], HM);
+      else conv_direct_blk_cf(hx[wid], hy[wid], HL, hw[wid], HM);
+      __syncwarp();
+      ++done;
+    }
+    if (lane == 0) atomicAdd((unsigned long long*)hcount, (unsigned long long)done);
+    return;
+  }
+  const bool fma_w = (w >= 5 && (w & 3) != 3 && w - 5 < nfma + 2);
+  if (nfma && fma_w) {
+    double x = lane, a = 0.999;
+    while (!*stop) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) x = fma(x, a, 1e-3);
+    }
+    if (x == 12345.0) cyc[2] = 1;
+    return;
+  }
+  if (npoll && w >= 5 && (w & 3) != 3 && w - 5 < npoll + 2) {
+    while (!*stop) {
+      if (__shfl_sync(FULL, flag[w & 31], 0) == 7) cyc[3] = 1;
+      __nanosleep(64);
+    }
+  }
+}
+
+
+// FFT-group noise: groups of 4 warps (named barriers 1, 2) run conv_fft on
+// global x (the medium group's task shape: Lout 512, h 256), the strip as before.
+template <int NG, int LOGN, int BIG = 0>
+__global__ void __launch_bounds__(512, 1) kf(const double* in, const double* pay, long long* cyc, int reps,
+                                            long long f, volatile int* stop, long long* hcount, const double* gx,
+                                            double* gy) {
+  extern __shared__ double2 sd[];
+  double2* tq = sd;
+  double* spay = (double*)(sd + TWQ);
+  double* sin_ = spay + NC;
+  double* sout = sin_ + NC;
+  double2* gbuf = (double2*)(sout + NC + 9);  // 16-byte aligned (3 NC + 9 even)
+  for (int i = threadIdx.x; i < TWQ; i += blockDim.x) tq[i] = fl_tw[i];
+  for (int i = threadIdx.x; i < NC; i += blockDim.x) { spay[i] = pay[i]; sin_[i] = in[i]; }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == 3) {
+    long long t0 = clock64();
+    int64_t acc = 0;
+    for (int r = 0; r < reps; ++r) acc += put_strip_fixed<5>(sin_ - C0, sout - C0, spay - C0, f, 64, CD, CM, CU);
+    long long t1 = clock64();
+    if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = acc; *stop = 1; }
+    return;
+  }
+  // groups: {0,1,2,4} and {5,6,8,9}
+  const int gw[2][4] = {{0, 1, 2, 4}, {5, 6, 8, 9}};
+  int grp = -1, gi = 0;
+  for (int q = 0; q < NG; ++q)
+    for (int j = 0; j < 4; ++j)
+      if (gw[q][j] == w) { grp = q; gi = j; }
+  if (grp < 0) return;
+  const int slots = smem_complex_slots(1 << (LOGN - 1));
+  double2* buf = gbuf + grp * slots;
+  Grp g{gi * 32 + lane, 128, 1 + grp};
+  Stencil st{CD, CM, CU, 2};
+  long long done = 0;
+  const int64_t Lout = 512, hh = 256, L = Lout + 2 * hh;
+  // a fixed task count that outlasts the strip (no stop polling inside a group)
+  for (int it = 0; it < 160; ++it) {
+    const int64_t off = BIG ? ((int64_t)(it * 2 + grp) * 1048576) % (1 << 25) : grp * 4096;
+    conv_fft(gx + off, L, gy + off, Lout, (int)hh, st, buf, LOGN, tq, g);
+    gsync(g);
+    if (g.t == 0 && !*stop) ++done;
+  }
+  if (g.t == 0) atomicAdd((unsigned long long*)hcount, (unsigned long long)done);
+}
+
+int main() {
+  std::vector<double> pay(NC), a(NC), b(NC);
+  const double DS = 0.0069877124296868435;
+  for (int i = 0; i < NC; ++i) { pay[i] = 1.0 - exp((double)(C0 + i) * DS); a[i] = pay[i] > 0 ? pay[i] : 0.0; }
+  long long f = 0;
+  for (int s = 1; s <= 300; ++s) {
+    long long lg = -100000;
+    for (int i = s; i < NC - s; ++i) {
+      double lin = CD * a[i - 1] + CU * a[i + 1] + CM * a[i];
+      bool red = lin > pay[i];
+      b[i] = red ? lin : pay[i];
+      if (!red) lg = C0 + i;
+    }
+    std::swap(a, b);
+    f = lg;
+  }
+  double *d_in, *d_pay; long long *c, *hc; int* stop;
+  cudaMalloc(&d_in, 8 * NC); cudaMalloc(&d_pay, 8 * NC); cudaMalloc(&c, 32); cudaMalloc(&stop, 4); cudaMalloc(&hc, 8);
+  cudaMemcpy(d_in, a.data(), 8 * NC, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_pay, pay.data(), 8 * NC, cudaMemcpyHostToDevice);
+  const char* names[] = {"alone", "2 helpers conv_direct_blk", "4 helpers conv_direct_blk", "9 FP64 FMA warps",
+                         "2 helpers conv_direct_blk_cf", "6 shared-flag pollers", "2 helpers + 6 FMA warps"};
+  for (int mode = 0; mode < 7; ++mode) {
+    double res = 0, rate = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(stop, 0, 4);
+      cudaMemset(hc, 0, 8);
+      const int reps = rep == 0 ? 2 : 300;
+      switch (mode) {
+        case 0: k<0><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 1: k<1><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 2: k<2><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 3: k<3><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 4: k<4><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 5: k<5><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 6: k<6><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+      }
+      cudaDeviceSynchronize();
+      long long hh[2], hcv;
+      cudaMemcpy(hh, c, 16, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&hcv, hc, 8, cudaMemcpyDeviceToHost);
+      res = hh[0] / (double(reps) * 64);
+      rate = hcv * (double)HL * HM / (double)hh[0];  // helper FMAs per strip cycle
+    }
+    printf("%-30s strip %6.1f cycles/row   helper %.2f FMA/cycle  %s\n", names[mode], res, rate,
+           cudaGetErrorString(cudaGetLastError()));
+  }
+  // FFT groups
+  {
+    std::vector<double2> hv(TW_N);
+    for (int m = 0; m < TW_N; ++m) {
+      long double an = 6.283185307179586476925286766559L * m / TW_N;
+      hv[m] = make_double2((double)cosl(an), -(double)sinl(an));
+    }
+    cudaMemcpyToSymbol(fl_tw, hv.data(), sizeof(double2) * TW_N);
+    double *gx, *gy;
+    cudaMalloc(&gx, 8 << 25); cudaMalloc(&gy, 8 << 25);
+    std::vector<double> xv(1 << 25);
+    for (int i = 0; i < (1 << 25); ++i) xv[i] = 1.0 / (1 + i % 97);
+    cudaMemcpy(gx, xv.data(), 8 << 25, cudaMemcpyHostToDevice);
+    auto runf = [&](auto kern, int ng, int logn, const char* nm) {
+      const int smem = TWQ * 16 + 3 * NC * 8 + 64 + 2 * smem_complex_slots(1 << (logn - 1)) * 16;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      double res = 0, rate = 0;
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(stop, 0, 4); cudaMemset(hc, 0, 8);
+        const int reps = rep == 0 ? 2 : 300;
+        kern<<<1, 512, smem>>>(d_in, d_pay, c, reps, f, stop, hc, gx, gy);
+        cudaDeviceSynchronize();
+        long long hh[2], hcv;
+        cudaMemcpy(hh, c, 16, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&hcv, hc, 8, cudaMemcpyDeviceToHost);
+        res = hh[0] / (double(reps) * 64);
+        rate = hh[0] / (double)(hcv > 0 ? hcv : 1) * ng;
+      }
+      printf("%-30s strip %6.1f cycles/row   %.0f cycles per FFT task per group  %s\n", nm, res, rate,
+             cudaGetErrorString(cudaGetLastError()));
+    };
+    runf(kf<0, 12>, 1, 12, "no FFT group (dyn smem)");
+    runf(kf<1, 12>, 1, 12, "1 FFT group (4096-pt)");
+    runf(kf<2, 12>, 2, 12, "2 FFT groups (4096-pt)");
+    runf(kf<2, 11>, 2, 11, "2 FFT groups (2048-pt)");
+    runf(kf<2, 12, 1>, 2, 12, "2 FFT groups, HBM-resident x/y");
+  }
+  return 0;
+}

@@ -37,8 +37,8 @@ print("issue per task: scan %.0f stall %.0f slot %.0f (tasks/option %.0f)" % (
 print("fused per node: stage %.0f wait %.0f post %.0f leaf %.0f rest %.0f (of %.0f)" % (
     d(P["F_STAGE"], P["FUSE_N"]), d(P["F_MID"], P["FUSE_N"]), d(P["F_BOT"], P["FUSE_N"]), d(P["STRIP_CYC"], P["FUSE_N"]),
     d(P["FUSE_CYC"] - P["F_STAGE"] - P["F_MID"] - P["F_BOT"] - P["STRIP_CYC"], P["FUSE_N"]), d(P["FUSE_CYC"], P["FUSE_N"])))
-print("strip: loop %.1f cyc/row, load %.0f cyc/leaf (leaves/option %.0f)" % (
-    d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"] / 28.0), P["STRIP_ROWS"] / 28.0 / nopt))
+print("strip: whole leaf %.1f cyc/row, row loop %.1f cyc/row, prologue %.1f cyc/row (per row of strip)" % (
+    d(P["STRIP_CYC"], P["STRIP_ROWS"]), d(P["STRIP_LOOP"], P["STRIP_ROWS"]), d(P["LEAF_LOAD"], P["STRIP_ROWS"])))
 print("conflict waits per option: RAW small %.3g big %.3g, WAR small %.3g big %.3g (n=%.0f)" % (
     P["W_RAW_S"] / nopt, P["W_RAW_B"] / nopt, P["W_WAR_S"] / nopt, P["W_WAR_B"] / nopt, P["W_N"] / nopt))
 print("helpers: urgent %.3g cyc, background %.3g cyc per option; %.3g FMA per option (%.2f FMA/cycle)" % (
