@@ -124,10 +124,6 @@ __device__ __forceinline__ void tw_powers(double2 w1, double2 (&w)[R]) {
   for (int q = 2; q < R; ++q) w[q] = cmul(w[q / 2], w[q - q / 2]);
 }
 
-__device__ __forceinline__ int last_radix_log(int logC) {
-  const int r = logC & 3;
-  return r ? r : 4;
-}
 
 // DIF stage of radix R on spans of S = 2^logS points.
 template <int R>
@@ -182,29 +178,31 @@ __device__ __forceinline__ void dit_stage(double2* buf, int logC, int logS, cons
 }
 
 // Stage plan of a C = 2^logC transform: radix-16 stages from the largest span
-// down, then one remainder stage of radix 2^last (last = last_radix_log).
+// down, then (if 4 does not divide logC) one remainder stage of radix 2^last.
 // Computed from logC in registers (a stage array in local memory cost a local
 // load per stage and four per spectrum bin pair).  (Measured alternative:
 // radix 4/8 stages keeping every group thread busy -- slower, N = 1024 task
 // 9.9k -> 13.2k cycles, profiles/r01_experiments.md.)
 struct FftPlan {
   int n16;   // radix-16 stages
-  int last;  // log2 radix of the remainder stage (1..4)
+  int last;  // log2 radix of the remainder stage (0: none, else 1..3)
 };
 __device__ __forceinline__ FftPlan fft_plan(int logC, int /*gn*/) {
   FftPlan p;
-  p.last = last_radix_log(logC);
-  p.n16 = (logC - p.last) >> 2;
+  p.last = logC & 3;
+  p.n16 = logC >> 2;
   return p;
 }
 
+// remainder stage: radix 2, 4 or 8 (the radix-16 stage has one call site per
+// direction: the instruction footprint counts)
 template <bool DIF>
-__device__ __forceinline__ void fft_stage(double2* buf, int lr, int logC, int logS, const double2* tq, const Grp& g) {
+__device__ __forceinline__ void fft_stage_rem(double2* buf, int lr, int logC, int logS, const double2* tq,
+                                              const Grp& g) {
   switch (lr) {
     case 1: DIF ? dif_stage<2>(buf, logC, logS, tq, g) : dit_stage<2>(buf, logC, logS, tq, g); break;
     case 2: DIF ? dif_stage<4>(buf, logC, logS, tq, g) : dit_stage<4>(buf, logC, logS, tq, g); break;
-    case 3: DIF ? dif_stage<8>(buf, logC, logS, tq, g) : dit_stage<8>(buf, logC, logS, tq, g); break;
-    default: DIF ? dif_stage<16>(buf, logC, logS, tq, g) : dit_stage<16>(buf, logC, logS, tq, g); break;
+    default: DIF ? dif_stage<8>(buf, logC, logS, tq, g) : dit_stage<8>(buf, logC, logS, tq, g); break;
   }
 }
 
@@ -216,13 +214,13 @@ __device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* t
     dif_stage<16>(buf, logC, logS, tq, g);
     logS -= 4;
   }
-  fft_stage<true>(buf, pl.last, logC, logS, tq, g);
+  if (pl.last) fft_stage_rem<true>(buf, pl.last, logC, logS, tq, g);
 }
 
 // Inverse (unnormalised, x C): slot P(k) in, natural order out.
 __device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
   int logS = pl.last;
-  fft_stage<false>(buf, pl.last, logC, logS, tq, g);
+  if (pl.last) fft_stage_rem<false>(buf, pl.last, logC, logS, tq, g);
 #pragma unroll 1
   for (int s = 0; s < pl.n16; ++s) {
     logS += 4;

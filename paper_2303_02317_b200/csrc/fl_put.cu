@@ -142,6 +142,7 @@ struct PutChainCtx {
   uint64_t ref_flops;  // reference-algorithmic flops (lane-uniform)
   unsigned long long* prof;
   bool pay_ready = false;  // the option's payoff table is written (see put_subtree)
+  bool full = false;       // price on the full frame only (re-run after a fixed-frame miss)
 };
 
 // Reference cost of a recursion node of height h whose parent has height ph:
@@ -179,7 +180,8 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   long long tm[2] = {0, 0};
   FL_TR(*X.S, X.c, EV_LEAF_B, height);
   // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
-  const bool slide = SL == 1 || (SL < 0 && P.slide && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height);
+  const bool slide =
+      SL == 1 || (SL < 0 && P.slide && !X.full && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height);
   int64_t kb;
 #if FL_FIXED_STRIP
   if (slide) {
@@ -363,7 +365,7 @@ __device__ int64_t put_solve_q(PutChainCtx& X, const PutParams& P, int64_t f0, d
     FL_TR(*X.S, X.c, EV_NODE, h * 4 + F.state);
     if (F.state == 0) {
       if (h <= PUT_HS) {
-        ret = (P.slide && PUT_LEAF <= PUT_SLIDE_H)
+        ret = (P.slide && !X.full && PUT_LEAF <= PUT_SLIDE_H)
                   ? put_subtree<ACCT, 1>(X, P, F.f, F.in_org, F.out_org, h, ph, err)
                   : put_subtree<ACCT, 0>(X, P, F.f, F.in_org, F.out_org, h, ph, err);
         if (*err) return 0;
@@ -458,14 +460,16 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
 
 // fast_put_bsm's stage loop (bsm.py:626-676) for option o on chain warp c.
 // Returns the status; FL_RETRY_FULL leaves no output (the caller re-prices the
-// option with P.slide = 0).
+// option with full = true: full-frame leaves only).
 template <bool ACCT>
 __device__ int32_t put_chain_option(SchedShared& S, int c, const PutParams& P, int o, double* arena,
-                                 double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
+                                    double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops,
+                                    bool full = false) {
   const long long t_opt = clock64();
   const int64_t n = P.n, ks = P.ks;
   const PutLayout Lo = put_layout(n, ks);
   PutChainCtx X = put_chain_setup(S, c, P, Lo, n, arena, scratch, out.prof, nullptr, 0, 0, out.acct != 0);
+  X.full = full;
   double* cur_org = arena - Lo.colbase;
   double* nxt_org = arena + Lo.span - Lo.colbase;
   int32_t err = 0, cnt = 0;
@@ -546,11 +550,11 @@ __device__ int32_t put_chain_option(SchedShared& S, int c, const PutParams& P, i
 
 // put_chain_option with the full-frame re-run (at most one).
 template <bool ACCT>
-__device__ void put_chain_option_retry(SchedShared& S, int c, const PutParams& P0, int o, double* arena,
+__device__ void put_chain_option_retry(SchedShared& S, int c, const PutParams& P, int o, double* arena,
                                        double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
-  PutParams P = P0;
-  while (put_chain_option<ACCT>(S, c, P, o, arena, scratch, out, chain_flops, ref_flops) == FL_RETRY_FULL)
-    P.slide = 0;
+  bool full = false;
+  while (put_chain_option<ACCT>(S, c, P, o, arena, scratch, out, chain_flops, ref_flops, full) == FL_RETRY_FULL)
+    full = true;
 }
 
 // Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
@@ -648,14 +652,13 @@ struct PutTrapPricer {
     double* cur_org = arena - Lo.colbase;
     double* nxt_org = arena + Lo.span - Lo.colbase;
     int32_t err = 0;
-    PutParams Q = P;
-    int64_t kp = put_stage(X, Q, f, W, h, cur_org, nxt_org, &err);
+    int64_t kp = put_stage(X, P, f, W, h, cur_org, nxt_org, &err);
     wait_all_own(S, c);
     if (err == FL_RETRY_FULL) {  // a fixed-frame leaf lost its margin: full frame
-      Q.slide = 0;
       err = 0;
-      X = put_chain_setup(S, c, Q, Lo, 2 * h, arena, scratch, nullptr, seg, f + 1, W);
-      kp = put_stage(X, Q, f, W, h, cur_org, nxt_org, &err);
+      X = put_chain_setup(S, c, P, Lo, 2 * h, arena, scratch, nullptr, seg, f + 1, W);
+      X.full = true;
+      kp = put_stage(X, P, f, W, h, cur_org, nxt_org, &err);
       wait_all_own(S, c);
     }
     const int64_t len = err ? 0 : (f + W - h) - kp;

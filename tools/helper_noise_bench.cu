@@ -14,6 +14,13 @@ constexpr double CD = 0.39790368627109396, CM = 0.199951171875, CU = 0.402096313
 constexpr int HM = 129, HL = 64;  // helper correlation: 129 taps (h = 64), 64 outputs
 constexpr int HX = HL + HM + 8;
 
+template <int K>
+__device__ __noinline__ double bigcode(double x, double a) {
+#pragma unroll
+  for (int i = 0; i < K * 64; ++i) x = fma(x, a, (double)(i & 7) * 1e-3);
+  return x;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) k(const double* in, const double* pay, long long* cyc, int reps, int height,
                                            long long f, volatile int* stop, long long* hcount) {
@@ -67,6 +74,12 @@ __global__ void __launch_bounds__(512, 1) k(const double* in, const double* pay,
     if (x == 12345.0) cyc[2] = 1;
     return;
   }
+  if (MODE >= 7 && w >= 4 && (w & 3) != 3) {
+    double x = lane, a = 0.999;
+    while (!*stop) x = (MODE == 7) ? bigcode<64>(x, a) : (MODE == 8 ? bigcode<8>(x, a) : bigcode<128>(x, a));
+    if (x == 12345.0) cyc[2] = 1;
+    return;
+  }
   if (npoll && w >= 5 && (w & 3) != 3 && w - 5 < npoll + 2) {
     while (!*stop) {
       if (__shfl_sync(FULL, flag[w & 31], 0) == 7) cyc[3] = 1;
@@ -78,10 +91,10 @@ __global__ void __launch_bounds__(512, 1) k(const double* in, const double* pay,
 
 // FFT-group noise: groups of 4 warps (named barriers 1, 2) run conv_fft on
 // global x (the medium group's task shape: Lout 512, h 256), the strip as before.
-template <int NG, int LOGN, int BIG = 0>
+template <int NG, int LOGN, int BIG = 0, int NHLP = 0>
 __global__ void __launch_bounds__(512, 1) kf(const double* in, const double* pay, long long* cyc, int reps,
                                             long long f, volatile int* stop, long long* hcount, const double* gx,
-                                            double* gy) {
+                                            double* gy, int height = 64) {
   extern __shared__ double2 sd[];
   double2* tq = sd;
   double* spay = (double*)(sd + TWQ);
@@ -95,12 +108,21 @@ __global__ void __launch_bounds__(512, 1) kf(const double* in, const double* pay
   if (w == 3) {
     long long t0 = clock64();
     int64_t acc = 0;
-    for (int r = 0; r < reps; ++r) acc += put_strip_fixed<5>(sin_ - C0, sout - C0, spay - C0, f, 64, CD, CM, CU);
+    for (int r = 0; r < reps; ++r) acc += put_strip_fixed<5>(sin_ - C0, sout - C0, spay - C0, f, height, CD, CM, CU);
     long long t1 = clock64();
     if (lane == 0) { cyc[0] = t1 - t0; cyc[1] = acc; *stop = 1; }
     return;
   }
-  // groups: {0,1,2,4} and {5,6,8,9}
+  if (NHLP && (w == 10 || w == 12)) {  // helper warps (kernel layout: 10, 12, 13, 14)
+    __shared__ double hx2[2][HX], hw2[2][HM + 8], hy2[2][HL + 8];
+    const int q = (w == 10) ? 0 : 1;
+    for (int i = lane; i < HX; i += 32) hx2[q][i] = 1.0 / (i + 1);
+    for (int i = lane; i < HM + 8; i += 32) hw2[q][i] = 0.01 * (i % 7);
+    __syncwarp();
+    while (!*stop) { conv_direct_blk(hx2[q], hy2[q], HL, hw2[q], HM); __syncwarp(); }
+    return;
+  }
+  // groups: {0,1,2,4} and {5,6,8,9} (the kernel's big / medium group warps)
   const int gw[2][4] = {{0, 1, 2, 4}, {5, 6, 8, 9}};
   int grp = -1, gi = 0;
   for (int q = 0; q < NG; ++q)
@@ -144,8 +166,9 @@ int main() {
   cudaMemcpy(d_in, a.data(), 8 * NC, cudaMemcpyHostToDevice);
   cudaMemcpy(d_pay, pay.data(), 8 * NC, cudaMemcpyHostToDevice);
   const char* names[] = {"alone", "2 helpers conv_direct_blk", "4 helpers conv_direct_blk", "9 FP64 FMA warps",
-                         "2 helpers conv_direct_blk_cf", "6 shared-flag pollers", "2 helpers + 6 FMA warps"};
-  for (int mode = 0; mode < 7; ++mode) {
+                         "2 helpers conv_direct_blk_cf", "6 shared-flag pollers", "2 helpers + 6 FMA warps",
+                         "9 warps 64 KB code (other SMSPs)", "9 warps 8 KB code", "9 warps 128 KB code"};
+  for (int mode = 0; mode < 10; ++mode) {
     double res = 0, rate = 0;
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(stop, 0, 4);
@@ -159,6 +182,9 @@ int main() {
         case 4: k<4><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
         case 5: k<5><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
         case 6: k<6><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 7: k<7><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 8: k<8><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
+        case 9: k<9><<<1, 512>>>(d_in, d_pay, c, reps, 64, f, stop, hc); break;
       }
       cudaDeviceSynchronize();
       long long hh[2], hcv;
@@ -183,14 +209,14 @@ int main() {
     std::vector<double> xv(1 << 25);
     for (int i = 0; i < (1 << 25); ++i) xv[i] = 1.0 / (1 + i % 97);
     cudaMemcpy(gx, xv.data(), 8 << 25, cudaMemcpyHostToDevice);
-    auto runf = [&](auto kern, int ng, int logn, const char* nm) {
+    auto runf = [&](auto kern, int ng, int logn, const char* nm, int hgt = 64) {
       const int smem = TWQ * 16 + 3 * NC * 8 + 64 + 2 * smem_complex_slots(1 << (logn - 1)) * 16;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       double res = 0, rate = 0;
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(stop, 0, 4); cudaMemset(hc, 0, 8);
         const int reps = rep == 0 ? 2 : 300;
-        kern<<<1, 512, smem>>>(d_in, d_pay, c, reps, f, stop, hc, gx, gy);
+        kern<<<1, 512, smem>>>(d_in, d_pay, c, reps, f, stop, hc, gx, gy, hgt);
         cudaDeviceSynchronize();
         long long hh[2], hcv;
         cudaMemcpy(hh, c, 16, cudaMemcpyDeviceToHost);
@@ -206,6 +232,10 @@ int main() {
     runf(kf<2, 12>, 2, 12, "2 FFT groups (4096-pt)");
     runf(kf<2, 11>, 2, 11, "2 FFT groups (2048-pt)");
     runf(kf<2, 12, 1>, 2, 12, "2 FFT groups, HBM-resident x/y");
+    runf(kf<0, 12, 0, 0>, 1, 12, "runtime h: alone", 64);
+    runf(kf<2, 12, 0, 0>, 2, 12, "runtime h: 2 FFT groups", 64);
+    runf(kf<0, 12, 0, 1>, 1, 12, "runtime h: 2 helpers", 64);
+    runf(kf<2, 12, 0, 1>, 2, 12, "runtime h: 2 FFT groups + 2 helpers", 64);
   }
   return 0;
 }
