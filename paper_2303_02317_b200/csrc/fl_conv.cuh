@@ -38,6 +38,9 @@ namespace fl {
 
 constexpr int CTA_THREADS = 256;
 
+#ifndef FL_ASYNC_LOAD  // 1: conv_fft stages its block with cp.async (no register staging)
+#define FL_ASYNC_LOAD 1
+#endif
 #ifndef FL_SPEC_SKIP  // 1: bin pairs whose spectrum values are both cut skip the split / multiply / re-pack
 #define FL_SPEC_SKIP 1
 #endif
@@ -332,6 +335,21 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
     const int64_t s0 = k0 + pl.rlo;
+#if FL_ASYNC_LOAD
+    // asynchronous 8-byte copies global -> shared (zero-filled past L): every
+    // load of the block is in flight at once and none holds a register (the
+    // register-staged pass waited one L2 round trip per 4 elements per thread)
+    for (int n = g.t; n < C; n += g.n) {
+      const int64_t i0 = s0 + 2 * (int64_t)n;
+      double* d = reinterpret_cast<double*>(buf + pidx(n));
+      const unsigned da = (unsigned)__cvta_generic_to_shared(d);
+      const int sa = (i0 < L) ? 8 : 0, sb = (i0 + 1 < L) ? 8 : 0;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da), "l"(x + (sa ? i0 : 0)), "r"(sa) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da + 8), "l"(x + (sb ? i0 + 1 : 0)), "r"(sb)
+                   : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#else
 #pragma unroll 4
     for (int n = g.t; n < C; n += g.n) {
       const int64_t i0 = s0 + 2 * (int64_t)n;
@@ -339,6 +357,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       const double b = (i0 + 1 < L) ? x[i0 + 1] : 0.0;
       buf[pidx(n)] = make_double2(a, b);
     }
+#endif
     gsync(g);
     fft_dif(buf, logC, tq, g, fp);
     // -- split to the real spectrum, multiply, re-pack for the inverse (/C)
