@@ -141,7 +141,8 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
   wait_conflicts(*X.S, X.c, U(in_org + lo0), U(in_org + j0 + 1), 0, 0, U(out_org + lo0), U(out_org + j0 + 1));
   const long long t1 = clock64();
   double* s_in = X.scratch + CSUB_IN;
-  warp_stage(s_in, in_org + lo0, h0);
+  warp_stage_async(s_in, in_org + lo0, h0);
+  warp_stage_wait();  // weights and input row
   long long twait = 0;
   static_assert(sizeof(CallSubFrame) * 5 <= FRAME_SOLVE_OFF - FRAME_SUB_OFF, "subtree frames");
   CallSubFrame* stk = chain_frames<CallSubFrame>(X.scratch, FRAME_SUB_OFF);

@@ -248,21 +248,22 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
   // composed weights depend on nothing in flight: stage them first, so their
   // load latency overlaps the wait for the jump writing this subtree's input
   const bool early = X.pay_ready;
-  if (early) {
-    warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+  if (early) {  // asynchronous copies, waited for after the input row's
+    warp_stage_async(s_pay, X.pay_org + plo, 4 * h0 + 2);
     if (h0 > put_leaf_h<SL>()) stash_weights(*X.S, X.c, X.wst, X.kc, h0, put_leaf_h<SL>(), 2);
   }
   const double* pay_s = s_pay - plo;
   wait_conflicts(*X.S, X.c, U(in_org + f0 + 1), U(in_org + f0 + 2 * h0 + 1), 0, 0, U(out_org + f0 - h0),
                  U(out_org + f0 + h0 + 1));
   if (!early) {
-    warp_stage_nb<17>(s_pay, X.pay_org + plo, 4 * h0 + 2, 4 * h0 + 2);
+    warp_stage_async(s_pay, X.pay_org + plo, 4 * h0 + 2);
     if (h0 > put_leaf_h<SL>()) stash_weights(*X.S, X.c, X.wst, X.kc, h0, put_leaf_h<SL>(), 2);
     X.pay_ready = true;
   }
   const long long t1 = clock64();
   FL_TR(*X.S, X.c, EV_STG_B, 0);
-  warp_stage(s_in, in_org + f0 + 1, 2 * h0);  // (batched loads: one round trip each)
+  warp_stage_async(s_in, in_org + f0 + 1, 2 * h0);
+  warp_stage_wait();  // payoff, weights and input row: one round trip
   const long long t2 = clock64();
   FL_TR(*X.S, X.c, EV_STG_E, 0);
   long long twait = 0, tpost = 0;

@@ -853,6 +853,23 @@ __device__ __forceinline__ void warp_stage(double* dst, const double* src, int n
   warp_stage_nb<8>(dst, src, n, n_total);
 }
 
+// Asynchronous warp_stage: 8-byte cp.async copies global -> shared (zero-fill
+// from n to n_total), no register staging and every copy in flight at once.
+// The data may be read only after warp_stage_wait().
+__device__ __forceinline__ void warp_stage_async(double* dst, const double* src, int n, int n_total = -1) {
+  if (n_total < n) n_total = n;
+  for (int i = lane_id(); i < n_total; i += 32) {
+    const unsigned da = (unsigned)__cvta_generic_to_shared(dst + i);
+    const int sz = (i < n) ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(da), "l"(src + (sz ? i : 0)), "r"(sz)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void warp_stage_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+}
+
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
 // or an FFT task, on the small or big ring.
 __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
@@ -918,7 +935,8 @@ __device__ __forceinline__ void publish_done(SchedShared& S, int ring, int idx) 
 }
 
 // Make the composed weights of every correlation of a shared-memory subtree
-// rooted at height h0 resident in the chain's stash: each internal node at
+// rooted at height h0 resident in the chain's stash (asynchronous copies: the
+// caller's warp_stage_wait() precedes any use): each internal node at
 // depth d-1 correlates with W_m of its children's heights m (depth d), two
 // consecutive values per depth.  Slots are reused while they cover the
 // subtree (consecutive subtrees mostly share heights).
@@ -932,7 +950,7 @@ __device__ void stash_weights(SchedShared& S, int c, double* wst, const double* 
     for (int j = 0; j < 2; ++j) {
       const int m = lo + j;
       if (m > KT_H) break;
-      warp_stage_nb<9>(wst + wst_off(d) + j * wst_sz(d), kc + (int64_t)m * m, m * span + 1, m * span + 1);
+      warp_stage_async(wst + wst_off(d) + j * wst_sz(d), kc + (int64_t)m * m, m * span + 1);
     }
     if (lane_id() == 0) S.wkey[c][d] = lo;
     __syncwarp();
