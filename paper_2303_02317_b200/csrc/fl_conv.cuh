@@ -38,6 +38,9 @@ namespace fl {
 
 constexpr int CTA_THREADS = 256;
 
+#ifndef FL_FFT_T  // phase timing hook (tools/fft_task_bench.cu)
+#define FL_FFT_T(k)
+#endif
 #ifndef FL_ASYNC_LOAD  // 1: conv_fft stages its block with cp.async (no register staging)
 #define FL_ASYNC_LOAD 1
 #endif
@@ -333,6 +336,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
   const FftPlan fp = fft_plan(logC, g.n);
 
   for (int64_t k0 = 0; k0 < Lout; k0 += pl.P) {
+    FL_FFT_T(4);
     // -- load packed pairs z[n] = x[s+2n] + i x[s+2n+1]
     const int64_t s0 = k0 + pl.rlo;
 #if FL_ASYNC_LOAD
@@ -359,7 +363,9 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
     }
 #endif
     gsync(g);
+    FL_FFT_T(0);
     fft_dif(buf, logC, tq, g, fp);
+    FL_FFT_T(1);
     // -- split to the real spectrum, multiply, re-pack for the inverse (/C)
     // W_N^k and the window phase W_N^(k rlo) advance by fixed steps per iteration
     // (one table lookup each instead of conflicted strided lookups per bin)
@@ -415,7 +421,9 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       ph = cmul(ph, phstep);
     }
     gsync(g);
+    FL_FFT_T(2);
     fft_dit(buf, logC, tq, g, fp);
+    FL_FFT_T(3);
     // -- store valid outputs: y[2n] = Re, y[2n+1] = Im
     const int64_t lim = (Lout - k0 < pl.P) ? (Lout - k0) : pl.P;
 #pragma unroll 4
@@ -426,6 +434,7 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
       if (j + 1 < lim) y[k0 + j + 1] = v.y;
     }
     gsync(g);
+    FL_FFT_T(5);
   }
   return (double)nblk * (10.0 * (double)C * (double)logC + 16.0 * (double)C);
 }

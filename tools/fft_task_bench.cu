@@ -7,6 +7,16 @@
 #include <cstdio>
 #include <vector>
 
+// phase timing: per group (g.bar), cycles from the previous mark; marks 4 (block
+// start), 0 (loaded), 1 (forward), 2 (spectrum), 3 (inverse), 5 (stored)
+__device__ long long fl_tlast[4];
+__device__ long long fl_tacc[4][8];
+#define FL_FFT_T(k)                                                    \
+  if (g.t == 0) {                                                      \
+    const long long _t = clock64();                                    \
+    if ((k) != 4) fl_tacc[g.bar & 3][k] += _t - fl_tlast[g.bar & 3];   \
+    fl_tlast[g.bar & 3] = _t;                                          \
+  }
 #include "../paper_2303_02317_b200/csrc/fl_common.cuh"
 #include "../paper_2303_02317_b200/csrc/fl_conv.cuh"
 using namespace fl;
@@ -83,6 +93,14 @@ int main() {
       for (int i = 0; i < q.ngrp; ++i) mx = fmax(mx, (double)hc[2 * i]);
       printf("Lout %5lld h %5d logNmax %2d  %3d thr x %d grp: %8.0f cycles/task, %8.0f cycles per task per SM-set  %s\n",
              (long long)k.Lout, k.h, k.logN, q.gsz, q.ngrp, mx / 20.0, mx / 20.0 / q.ngrp, cudaGetErrorString(e));
+      long long ta[4][8];
+      cudaMemcpyFromSymbol(ta, fl_tacc, sizeof(ta));
+      cudaMemset(c, 0, 8);
+      const long long zero[32] = {0};
+      cudaMemcpyToSymbol(fl_tacc, zero, sizeof(zero));
+      const double nt = 22.0;  // tasks timed (2 + 20 reps)
+      printf("      group 1 per task: load %6.0f  forward %6.0f  spectrum %6.0f  inverse %6.0f  store %6.0f\n",
+             ta[1][0] / nt, ta[1][1] / nt, ta[1][2] / nt, ta[1][3] / nt, ta[1][5] / nt);
     }
   }
   return 0;
