@@ -933,7 +933,8 @@ int64_t fl_batch_device_bytes(const fl_batch* b) {
 
 int fl_batch_profile(fl_batch* b, uint64_t* counters56, void* stream) {
   if (!b) return fail("fl_batch_profile: null batch");
-  if (!FL_PROF) return fail("fl_batch_profile: library built without profile counters (build with FL_NVCC_FLAGS=-DFL_PROF=1)");
+  if (!FL_PROF && !FL_STRIP_CLOCK)
+    return fail("fl_batch_profile: library built without profile counters (build with FL_NVCC_FLAGS=-DFL_PROF=1)");
   FL_CUDA(cudaMemcpyAsync(counters56, b->d_stats.as<unsigned long long>() + 8, 56 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

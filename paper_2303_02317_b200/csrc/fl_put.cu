@@ -163,6 +163,15 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
 #ifndef FL_FIXED_STRIP
 #define FL_FIXED_STRIP 1
 #endif
+#ifndef FL_STRIP_CLOCK  // tool builds: a few clock64 intervals of the chain only (tools/strip_clock.py)
+#define FL_STRIP_CLOCK 0
+#endif
+#if FL_STRIP_CLOCK
+#define LCLK_ADD(p, slot, v) \
+  do { if ((p) && lane_id() == 0) atomicAdd((p) + (slot), (unsigned long long)(v)); } while (0)
+#else
+#define LCLK_ADD(p, slot, v) do { } while (0)
+#endif
 // Internal status (never reported): a fixed-frame leaf saw the exercise region
 // reach its left margin; the option is priced again on the full frame.
 constexpr int32_t FL_RETRY_FULL = 0x7f01;
@@ -185,8 +194,16 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   int64_t kb;
 #if FL_FIXED_STRIP
   if (slide) {
+#if FL_STRIP_CLOCK  // tool builds: the strip loop's cycles alone, nothing else profiled
+    kb = put_strip_fixed<PUT_SLIDE_CPL>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu, X.prof ? tm : nullptr);
+    if (X.prof && lane_id() == 0) {
+      atomicAdd(X.prof + PROF_STRIP_LOOP, (unsigned long long)tm[1]);
+      atomicAdd(X.prof + PROF_STRIP_N, (unsigned long long)height);
+    }
+#else
     kb = put_strip_fixed<PUT_SLIDE_CPL>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
                                         FL_PROFP(X.prof) ? tm : nullptr);
+#endif
     // the exercise region reached the frame's left margin: inside a subtree
     // (SL 1) the caller re-prices the option on the full frame; elsewhere the
     // full frame runs here
@@ -203,6 +220,7 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
                                        FL_PROFP(X.prof) ? tm : nullptr);
 #endif
   FL_TR(*X.S, X.c, EV_LEAF_E, height);
+  LCLK_ADD(X.prof, PROF_STRIP_CYC, clock64() - t1);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
     prof_add(FL_PROFP(X.prof), PROF_STRIP_N, height);
@@ -331,6 +349,12 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
     C.out = mid ? F.asmo : F.out;
     C.state = 0;
   }
+  LCLK_ADD(X.prof, PROF_WAIT_CYC, t1 - t0);
+  LCLK_ADD(X.prof, PROF_F_STAGE, t2 - t1);
+  LCLK_ADD(X.prof, PROF_F_MID, twait);
+  LCLK_ADD(X.prof, PROF_F_BOT, tpost);
+  LCLK_ADD(X.prof, PROF_FUSE_CYC, clock64() - t1);
+  LCLK_ADD(X.prof, PROF_FUSE_N, 1);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_STAGE, t2 - t1);
@@ -544,6 +568,7 @@ __device__ int32_t put_chain_option(SchedShared& S, int c, const PutParams& P, i
     if (out.bcount) out.bcount[o] = err ? 0 : cnt;
     prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
+  LCLK_ADD(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   *chain_flops += (double)X.flops;
   *ref_flops += (double)X.ref_flops;
   return err;
