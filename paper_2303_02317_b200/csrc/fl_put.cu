@@ -163,9 +163,6 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
 #ifndef FL_FIXED_STRIP
 #define FL_FIXED_STRIP 1
 #endif
-#ifndef FL_STRIP_CLOCK  // tool builds: a few clock64 intervals of the chain only (tools/strip_clock.py)
-#define FL_STRIP_CLOCK 0
-#endif
 #if FL_STRIP_CLOCK
 #define LCLK_ADD(p, slot, v) \
   do { if ((p) && lane_id() == 0) atomicAdd((p) + (slot), (unsigned long long)(v)); } while (0)

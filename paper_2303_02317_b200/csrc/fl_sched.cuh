@@ -44,6 +44,9 @@ namespace fl {
 #define FL_PROF 0  // the counting code enlarges the kernel and costs instruction-cache misses
 #endif
 #define FL_PROFP(p) (FL_PROF ? (p) : nullptr)
+#ifndef FL_STRIP_CLOCK  // tool builds: a few clock64 intervals only (tools/strip_clock.py)
+#define FL_STRIP_CLOCK 0
+#endif
 #ifndef FL_NHELP
 #define FL_NHELP 2
 #endif
@@ -462,6 +465,9 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
     s.c0 = t.c0; s.c1 = t.c1; s.c2 = t.c2; s.h = t.h; s.span = t.span; s.kind = t.kind; s.chain = c;
     s.i0 = t.i0; s.i1 = t.i1; s.i2 = t.i2;
     s.d0 = t.d0;
+#if FL_STRIP_CLOCK  // tool builds: the issue clock rides in d0 of FFT tasks (unused there)
+    if (t.kind == TK_FFT) s.d0 = __longlong_as_double(clock64());
+#endif
     s.ndep = nd;
     for (int i = 0; i < nd; ++i) s.dep[i] = deps[i];
     Pend& p = S.pend[c][S.npend[c] % PEND_CAP];
@@ -1198,12 +1204,24 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
     const long long t1 = clock64();
     if (g.t == 0) prof_add(prof, PROF_IDLE_CYC, t1 - t0);
     if (t.kind == TK_EXIT) break;
+#if FL_STRIP_CLOCK  // tool builds: queue delay (issue -> claim) and service time per ring
+    const long long tq0 = t.kind == TK_FFT ? __double_as_longlong(t.d0) : t1;
+#endif
     // a stolen small-ring task runs with the medium group's block plan (same
     // arithmetic whichever group executes it)
     const bool stolen = (gi == 0 && tring == RING_SMALL);
     const double fl = pr.exec(S, t, buf, stolen ? SMALL_SLOTS : slots, stolen ? SMALL_LOGN : logN, tq, g);
     flops += fl > 0 ? fl : 0.0;
     gsync(g);
+#if FL_STRIP_CLOCK
+    if (g.t == 0 && prof && t.kind == TK_FFT) {
+      const int sl = 36 + 4 * tring;  // per ring: queue, service, count, stolen count
+      atomicAdd(prof + sl, (unsigned long long)(t1 - tq0));
+      atomicAdd(prof + sl + 1, (unsigned long long)(clock64() - t1));
+      atomicAdd(prof + sl + 2, 1ull);
+      if (gi == 0 && tring == RING_SMALL) atomicAdd(prof + sl + 3, 1ull);
+    }
+#endif
     if (g.t == 0) {
       publish_done(S, tring, idx);
       if (FL_PROFP(prof)) {
