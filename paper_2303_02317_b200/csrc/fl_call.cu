@@ -111,6 +111,8 @@ __device__ __forceinline__ int64_t call_leaf(CallChainCtx& X, const CallParams& 
   const int64_t jp = call_leaf_v4<CALL_LEAF / 32>(P, in_org, out_org, j - h + 1, i, j, h, &cells, X.scratch + CALL_E2,
                                                   X.scratch + CALL_BT);
   if (X.acct) X.flops += 5ull * (uint64_t)cells;
+  LCLK_ADD(X.prof, PROF_STRIP_CYC, clock64() - t1);
+  LCLK_ADD(X.prof, PROF_STRIP_N, h);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_STRIP_CYC, clock64() - t1);
     prof_add(FL_PROFP(X.prof), PROF_STRIP_N, h);
@@ -203,6 +205,10 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
     C.out = mid ? F.asmo : F.out;
     C.state = 0;
   }
+  LCLK_ADD(X.prof, PROF_WAIT_CYC, t1 - t0);
+  LCLK_ADD(X.prof, PROF_F_MID, twait);
+  LCLK_ADD(X.prof, PROF_FUSE_CYC, clock64() - t1);
+  LCLK_ADD(X.prof, PROF_FUSE_N, 1);
   if (FL_PROFP(X.prof) && lane_id() == 0) {
     prof_add(FL_PROFP(X.prof), PROF_WAIT_CYC, t1 - t0);
     prof_add(FL_PROFP(X.prof), PROF_F_MID, twait);
@@ -379,6 +385,7 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
     if (out.flops) atomicAdd(out.flops + 1, (unsigned long long)(X.ref_q / 4));
     prof_add(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   }
+  LCLK_ADD(out.prof, PROF_CHAIN_CYC, clock64() - t_opt);
   *chain_flops += (double)X.flops;
 }
 

@@ -98,6 +98,13 @@ __device__ int64_t call_leaf_v4(const CallParams& P, const double* __restrict__ 
     __syncwarp();
   }
   double bp = CPL <= 2 ? __shfl_sync(FULL, B0, 0) : bt[0];
+  // the exercise value of the right neighbour column at the previous row,
+  // bp e2[c+1] - K, IS that column's green value of the previous row: carried
+  // in registers (same operations, bit-identical) instead of recomputed, except
+  // for the lane's last column (its neighbour lives on the next lane)
+  double gp[CPL];
+#pragma unroll
+  for (int c = 1; c < CPL; ++c) gp[c] = __dsub_rn(__dmul_rn(bp, e2c[c]), P.K);
 #pragma unroll 2
   for (int s = 0; s < height; ++s) {
     const int t = s + 1;
@@ -109,15 +116,17 @@ __device__ int64_t call_leaf_v4(const CallParams& P, const double* __restrict__ 
       bc = bt[t];
     }
     const double right = __shfl_down_sync(FULL, v[0], 1);
+    const double ex_last = __dsub_rn(__dmul_rn(bp, e2c[CPL]), P.K);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-      const double ex_r = __dsub_rn(__dmul_rn(bp, e2c[c + 1]), P.K);
+      const double ex_r = (c + 1 < CPL) ? gp[c + 1] : ex_last;
       const double grn = __dsub_rn(__dmul_rn(bc, e2c[c]), P.K);
       const double a = __dmul_rn(P.wd, v[c]);
       const double vr = edge[c] ? ex_r : (c + 1 < CPL ? v[c + 1] : right);
       const double lin = __dadd_rn(a, __dmul_rn(P.wu, vr));
       green[c] = !(lin >= grn);
       v[c] = green[c] ? grn : lin;
+      if (c > 0) gp[c] = grn;
     }
     bp = bc;
   }

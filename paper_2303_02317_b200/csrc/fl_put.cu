@@ -163,12 +163,7 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
 #ifndef FL_FIXED_STRIP
 #define FL_FIXED_STRIP 1
 #endif
-#if FL_STRIP_CLOCK
-#define LCLK_ADD(p, slot, v) \
-  do { if ((p) && lane_id() == 0) atomicAdd((p) + (slot), (unsigned long long)(v)); } while (0)
-#else
-#define LCLK_ADD(p, slot, v) do { } while (0)
-#endif
+
 // Internal status (never reported): a fixed-frame leaf saw the exercise region
 // reach its left margin; the option is priced again on the full frame.
 constexpr int32_t FL_RETRY_FULL = 0x7f01;

@@ -47,6 +47,12 @@ namespace fl {
 #ifndef FL_STRIP_CLOCK  // tool builds: a few clock64 intervals only (tools/strip_clock.py)
 #define FL_STRIP_CLOCK 0
 #endif
+#if FL_STRIP_CLOCK
+#define LCLK_ADD(p, slot, v) \
+  do { if ((p) && (threadIdx.x & 31) == 0) atomicAdd((p) + (slot), (unsigned long long)(v)); } while (0)
+#else
+#define LCLK_ADD(p, slot, v) do { } while (0)
+#endif
 #ifndef FL_NHELP
 #define FL_NHELP 2
 #endif
