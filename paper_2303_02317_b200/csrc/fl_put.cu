@@ -361,7 +361,7 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
 
 __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                          int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_PROFP(X.prof));
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof));
 }
 
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
@@ -433,7 +433,8 @@ __device__ int64_t put_stage(PutChainCtx& X, const PutParams& P, int64_t f, int6
   const int h = (int)hh;
   if (red > 2 * hh) {  // far: cols f+h+1 .. f+red-h stay linear
     X.ref_flops += ref_jump_flops(red, 2 * hh + 1);
-    chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc, FL_PROFP(X.prof), true);
+    chain_conv(*X.S, X.c, X.st, cur_org + f + 1, red, nxt_org + f + h + 1, red - 2 * hh, h, X.kc,
+               FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof), true);
   }
   return put_solve_q<ACCT>(X, P, f, cur_org, nxt_org, h, err);
 }
@@ -487,6 +488,7 @@ __device__ int32_t put_chain_option(SchedShared& S, int c, const PutParams& P, i
   const PutLayout Lo = put_layout(n, ks);
   PutChainCtx X = put_chain_setup(S, c, P, Lo, n, arena, scratch, out.prof, nullptr, 0, 0, out.acct != 0);
   X.full = full;
+  LCLK_ADD(out.prof, PROF_DEPWAIT_CYC, clock64() - t_opt);  // option setup (kernel table, init task issue)
   double* cur_org = arena - Lo.colbase;
   double* nxt_org = arena + Lo.span - Lo.colbase;
   int32_t err = 0, cnt = 0;

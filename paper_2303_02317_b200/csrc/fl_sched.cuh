@@ -913,6 +913,7 @@ __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const doubl
     }
   }
   if (prof && lane_id() == 0) prof_add(prof, PROF_ISS_CYC, clock64() - t0);
+  LCLK_ADD(prof, PROF_ISS_CYC, clock64() - t0);
 }
 
 // Worker side: wait until slot `idx` of `ring` is published and its deps are done
