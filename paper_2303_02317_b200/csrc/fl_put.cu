@@ -573,8 +573,10 @@ template <bool ACCT>
 __device__ void put_chain_option_retry(SchedShared& S, int c, const PutParams& P, int o, double* arena,
                                        double* scratch, const BatchOut& out, double* chain_flops, double* ref_flops) {
   bool full = false;
-  while (put_chain_option<ACCT>(S, c, P, o, arena, scratch, out, chain_flops, ref_flops, full) == FL_RETRY_FULL)
+  while (put_chain_option<ACCT>(S, c, P, o, arena, scratch, out, chain_flops, ref_flops, full) == FL_RETRY_FULL) {
     full = true;
+    LCLK_ADD(out.prof, PROF_S_LEAF, 1);  // tool builds: options re-priced on the full frame
+  }
 }
 
 // Worker-side execution of the put-specific tasks.  slots: capacity of sbuf in
