@@ -31,3 +31,5 @@ two = [v for v in pairs.values() if len(v) == 2]
 print(f"SMs used {len(pairs)}: solo {len(solo)}, paired {len(two)}")
 if solo:
     print(f"solo durations mean {np.mean([dur[v[0]] for v in solo]):.3f}; paired mean {np.mean([dur[i] for v in two for i in v]):.3f}")
+if os.environ.get("TL_SAVE"):
+    np.savez(os.environ["TL_SAVE"], dur=dur, S=b.S, K=b.K, R=b.R, Y=b.Y, V=b.V, E=b.E, T=b.T, sm=sm, start=st, end=en)
