@@ -217,6 +217,10 @@ __device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __
   return kb;
 }
 
+#ifndef FL_FIXED_UNROLL
+#define FL_FIXED_UNROLL 2  // measured: 1 is -0.5..-2 % at the headline (two chains per SM) but +7 % at C4 (one per SM); 4 slower
+#endif
+constexpr int FIXED_UNROLL = FL_FIXED_UNROLL;
 constexpr int64_t FIXED_MISS = NONE_SEEN - 1;  // put_strip_fixed: left edge not exercise, nothing written
 
 // Fixed-column put strip with a ghost lane (production leaf).  Same contract as
@@ -271,7 +275,7 @@ __device__ int64_t put_strip_fixed(const double* __restrict__ in_org, double* __
   long long ta = 0;
   if (tm) { ta = clock64() + (long long)(v[0] + p[0] == 12345.678 ? 1 : 0); }
   bool cont0 = false;  // lane 1: column base turned continuation on some row
-#pragma unroll 2
+#pragma unroll FIXED_UNROLL
   for (int s = 0; s < h; ++s) {
     const double L = __shfl_up_sync(FULL, v[CPL - 1], 1);
     const double R = __shfl_down_sync(FULL, v[0], 1);
