@@ -217,6 +217,9 @@ __device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __
   return kb;
 }
 
+#ifndef FL_FIXED_MARGIN_CAP  // test builds only (tools/test_fixed_miss.sh): a tiny margin forces FIXED_MISS
+#define FL_FIXED_MARGIN_CAP 1000000
+#endif
 #ifndef FL_FIXED_UNROLL
 #define FL_FIXED_UNROLL 2  // measured: 1 is -0.5..-2 % at the headline (two chains per SM) but +7 % at C4 (one per SM); 4 slower
 #endif
@@ -255,7 +258,8 @@ __device__ int64_t put_strip_fixed(const double* __restrict__ in_org, double* __
   // margin: what the frame's 31 CPL cells leave, at most 2h (column base-1
   // stays inside the reference frame [f-2h-1, f+2h])
   const int Mx = 31 * CPL - 2 * h - 1;
-  const int M = Mx < 2 * h ? Mx : 2 * h;
+  int M = Mx < 2 * h ? Mx : 2 * h;
+  if (M > FL_FIXED_MARGIN_CAP) M = FL_FIXED_MARGIN_CAP;  // test builds: force the full-frame re-run path
   const int64_t base = f - M;
   const int W = M + 2 * h + 1;      // frame cells base .. f+2h
   const int j0 = (lane - 1) * CPL;  // lane 0: cells -CPL .. -1
