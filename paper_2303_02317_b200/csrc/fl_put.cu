@@ -160,9 +160,6 @@ __device__ __forceinline__ void ref_node_bottom(PutChainCtx& X, int h, int64_t A
   if (h > X.ref_cut) X.ref_flops += ref_jump_flops(A, 2 * (int64_t)(h - (h + 1) / 2) + 1);
 }
 
-#ifndef FL_FIXED_STRIP
-#define FL_FIXED_STRIP 1
-#endif
 
 // Internal status (never reported): a fixed-frame leaf saw the exercise region
 // reach its left margin; the option is priced again on the full frame.
@@ -180,11 +177,10 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
   const long long t1 = clock64();
   long long tm[2] = {0, 0};
   FL_TR(*X.S, X.c, EV_LEAF_B, height);
-  // sliding 2h+2 frame when the option's exercise margin allows it (host flag)
+  // the fixed frame when the option's exercise margin allows it (host flag PutParams::slide)
   const bool slide =
       SL == 1 || (SL < 0 && P.slide && !X.full && height <= PUT_SLIDE_H && hi == f + 2 * (int64_t)height);
   int64_t kb;
-#if FL_FIXED_STRIP
   if (slide) {
 #if FL_STRIP_CLOCK  // tool builds: the strip loop's cycles alone, nothing else profiled
     kb = put_strip_fixed<PUT_SLIDE_CPL>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu, X.prof ? tm : nullptr);
@@ -205,12 +201,6 @@ __device__ __forceinline__ int64_t put_leaf(PutChainCtx& X, const PutParams& P, 
     kb = put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
                                  FL_PROFP(X.prof) ? tm : nullptr);
   }
-#else
-  kb = slide ? put_strip_ghost<PUT_SLIDE_CPL, 0>(in_org, out_org, pay_org, f, height, P.cd, P.cm, P.cu,
-                                                 FL_PROFP(X.prof) ? tm : nullptr)
-             : put_strip_pipe<PUT_CPL>(in_org, out_org, pay_org, lo, hi, f, height, P.cd, P.cm, P.cu,
-                                       FL_PROFP(X.prof) ? tm : nullptr);
-#endif
   FL_TR(*X.S, X.c, EV_LEAF_E, height);
   LCLK_ADD(X.prof, PROF_STRIP_CYC, clock64() - t1);
   if (FL_PROFP(X.prof) && lane_id() == 0) {

@@ -7,6 +7,7 @@
 #include <vector>
 #include <cmath>
 #include "../paper_2303_02317_b200/csrc/fl_sched.cuh"
+#include "conv_variants.cuh"
 #include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
 using namespace fl;
 constexpr int NC = 1201, C0 = -600;

@@ -10,6 +10,7 @@
 #include <cmath>
 #include "../paper_2303_02317_b200/csrc/fl_common.cuh"
 #include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
+#include "strip_variants.cuh"
 using namespace fl;
 constexpr int NC = 1201, C0 = -600;
 constexpr double CD = 0.39790368627109396, CM = 0.199951171875, CU = 0.4020963137289061;

@@ -5,6 +5,7 @@
 //   put_strip_warp     the reference's full 4h+2 frame, one exchange per row
 //   put_strip_v2       3h+2 frame (columns that can still change)
 //   put_strip_slide    2h+2 sliding frame without the ghost lane
+//   put_strip_ghost    sliding 2h+2 frame with a ghost lane (production through round 2)
 //   put_strip_ghost2   ghost-lane frame, two rows per neighbour exchange
 //   put_strip_tiled    full frame, K rows per exchange (halo recompute)
 //   call_leaf_warp / call_leaf_v2 / call_leaf_tiled<K>   call strips
@@ -16,6 +17,113 @@
 #include "../paper_2303_02317_b200/csrc/fl_strip.cuh"
 
 namespace fl {
+
+// Sliding-frame put strip with a ghost lane (the production leaf through round 2; put_strip_fixed replaced it).  Same contract
+// as put_strip_pipe (lo = f-2h-1, hi = f+2h) but the frame follows the valid
+// cone: at row s it holds only the 2h+2 columns f-s-1 .. f+2h-s, cell j =
+// column f-s-1+j.  Two facts make that exact:
+//   * right side: the reference's valid range shrinks by one column per row
+//     (_accel.py:203-242: after s rows only [lo+s, hi-s] is valid), so
+//     columns right of f+2h-s never influence the final valid range;
+//   * left side: at row s every column < f-s is an exercise cell whose value
+//     is its payoff (the boundary drops by at most one column per row: a cell
+//     whose three parents are exercise cells gets lin = payoff - omega*dtau +
+//     O(dtau ds^2) < payoff; the host checks that margin per option,
+//     PutParams::slide, and options that fail it use put_strip_pipe).
+// In frame coordinates the stencil is left-shifted, new u[j] = F(u[j-2],
+// u[j-1], u[j]), so a lane needs two cells from its left neighbour and none
+// from its right: one shuffle direction.  Per-cell arithmetic:
+// fma(cd, left, fma(cu, right, cm * cur)), projected by max (equal to the
+// reference's lin > pay ? lin : pay), exercise iff the value equals the payoff.
+// Lane 0 holds the CPL exercise cells left of the frame (cols f-s-1-CPL ..
+// f-s-2 at row s) and lanes 1.. hold the frame, so no lane needs a select
+// after the shuffle.  Lane 0's values stay
+// exactly their payoffs: its own left inputs (shfl_up returns lane 0's own,
+// more-right cells, whose payoffs are smaller) only lower its lin, and an
+// exercise cell with a lower lin is still an exercise cell (cd, cm, cu >= 0).
+// Payoffs of the new row: PAYLDS = 0 shifts them one cell right in registers
+// and loads only the lane's first cell (one load per row); PAYLDS = 1 loads
+// every cell.  Requires 2h+2 <= 32*CPL - CPL; pay_org must cover cols
+// f-h-1-CPL .. f+2h.
+template <int CPL, int PAYLDS = 0>
+__device__ int64_t put_strip_ghost(const double* __restrict__ in_org, double* __restrict__ out_org,
+                                   const double* __restrict__ pay_org, int64_t f, int height, double cd, double cm,
+                                   double cu, long long* tm = nullptr) {
+  static_assert(CPL >= 2, "two left cells come from one neighbour");
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * height + 2;
+  const int j0 = (lane - 1) * CPL;  // lane 0: cells -CPL .. -1
+  // cells past the frame (idle lanes, the tail of the last lane) read the
+  // frame's last column; their values never reach a cell j < W
+  const double* pay0 = pay_org + (f - 1);
+  int jx[CPL];
+  double u[CPL], p[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    jx[c] = (j0 + c < W) ? j0 + c : W - 1;
+    p[c] = pay0[jx[c]];
+    u[c] = (jx[c] <= 1) ? p[c] : in_org[f - 1 + jx[c]];
+  }
+  long long ta = 0;
+  __syncwarp();
+  if (tm) { ta = clock64() + (long long)(u[0] == 12345.678 ? 1 : 0); }
+  // row s+1 payoff of cell j: col f-s-2+j = pay0[j - 1 - s]
+  const double* pq0 = pay0 - 1 + jx[0];
+  double np0 = pq0[0];
+  unsigned green = 0;
+  // unrolled by 2 only: in the kernel the strip shares the SM's instruction
+  // cache with every other role, and a longer body measured slower there
+  // (4 -> 14.2, 5 -> 14.8, 10 -> 15.8 ms; 2 -> 14.0 ms) although faster alone
+#pragma unroll 2
+  for (int s = 0; s < height; ++s) {
+    const double L2 = __shfl_up_sync(FULL, u[CPL - 2], 1);
+    const double L1 = __shfl_up_sync(FULL, u[CPL - 1], 1);
+    double np[CPL];
+    if (PAYLDS) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) np[c] = pay0[jx[c] - 1 - s];
+    } else {
+      np[0] = np0;
+#pragma unroll
+      for (int c = 1; c < CPL; ++c) np[c] = p[c - 1];
+      np0 = pq0[-(s + 1)];  // next row's first-cell payoff
+    }
+    double nu[CPL];
+#pragma unroll
+    for (int c = CPL - 1; c >= 2; --c) {
+      const double lin = fma(cd, u[c - 2], fma(cu, u[c], cm * u[c - 1]));
+      nu[c] = proj_max(lin, np[c]);
+    }
+    const double lin1 = fma(cd, L1, fma(cu, u[1], cm * u[0]));
+    const double lin0 = fma(cd, L2, fma(cu, u[0], cm * L1));
+    nu[1] = proj_max(lin1, np[1]);
+    nu[0] = proj_max(lin0, np[0]);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      u[c] = nu[c];
+      p[c] = np[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) green |= (u[c] == p[c] ? 1u : 0u) << c;
+  if (tm) { tm[0] += ta; tm[1] += clock64() + (long long)(u[0] == 12345.678 ? 1 : 0) - ta; }
+  int best = -1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+    if (((green >> c) & 1u) && j0 + c >= 0 && j0 + c < W) best = j0 + c;
+  best = warp_max_i32(best);
+  const int64_t base = f - height - 1;
+  const int64_t kb = (best < 0) ? NONE_SEEN : base + best;
+  const int jlo = (best < 0) ? W : best + 1;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const int j = j0 + c;
+    if (j >= jlo && j < W) out_org[base + j] = u[c];
+  }
+  __syncwarp();
+  return kb;
+}
+
 
 // Put strip over columns [lo, hi], `height` forward rows.  Cells <= f hold the
 // payoff, cells f+1..hi come from in_org[col].  Writes the continuation values
