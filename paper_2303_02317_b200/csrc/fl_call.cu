@@ -469,6 +469,7 @@ __device__ double call_exec_task(SchedShared& S, const Task& t, double2* sbuf, i
 }
 
 struct CallPricer {
+  static constexpr int kLayout = 6;  // one chain per SMSP (see warp_role)
   const CallParams* opts;
   const int32_t* order;
   BatchOut out;

@@ -67,6 +67,21 @@ constexpr int IDLE_WARPS = 2;
 constexpr int SCHED_WARPS = 2 * GROUP_WARPS + NCHAIN * (1 + NHELP) + IDLE_WARPS;
 constexpr int SCHED_THREADS = 32 * SCHED_WARPS;
 enum : int { ROLE_CHAIN = 0, ROLE_BIG = 1, ROLE_MED = 2, ROLE_HELPER = 3, ROLE_IDLE = 4 };
+// Pricers choose the warp placement (Pricer::kLayout, default 4): layout 4
+// puts both chains on SMSP 3 (the put's fixed strip runs best there, the FFT
+// groups spread over SMSPs 0-2); layout 6 gives each chain an SMSP of its own
+// with its helpers and one FFT group per remaining SMSP (the call's light
+// 2-tap strip: C2 3.02 -> 2.88 ms; puts 14 % slower, profiles/r02_experiments.md).
+template <class P>
+struct LayoutOf {
+  template <class Q>
+  static constexpr int pick(decltype(Q::kLayout)*) { return Q::kLayout; }
+  template <class Q>
+  static constexpr int pick(...) { return 4; }
+  static constexpr int value = pick<P>(nullptr);
+};
+
+template <int LAYOUT = 4>
 __device__ __forceinline__ int warp_role(int w, int* rank) {
   // The chains' leaf strips exchange neighbours by shuffle every row, and a
   // shuffle waits behind every shared-memory access queued on its SMSP's MIO
@@ -75,6 +90,15 @@ __device__ __forceinline__ int warp_role(int w, int* rank) {
   // SMSPs).  So both chains share SMSP 3 with nothing else (warps 3, 7; 11 and
   // 15 idle), and the FFT groups and the helpers (two per chain) fill SMSPs 0-2.
   static_assert(NCHAIN == 2 && NHELP == 2 && SCHED_WARPS == 16, "layout 4 shape");
+  if (LAYOUT == 6) {
+    // each chain on an SMSP of its own with its two helpers (chain 0: SMSP 3,
+    // chain 1: SMSP 2), the big group on SMSP 0, the medium group on SMSP 1
+    constexpr int kR[16] = {ROLE_BIG, ROLE_MED, ROLE_CHAIN, ROLE_CHAIN, ROLE_BIG, ROLE_MED, ROLE_HELPER, ROLE_HELPER,
+                            ROLE_BIG, ROLE_MED, ROLE_HELPER, ROLE_HELPER, ROLE_BIG, ROLE_MED, ROLE_IDLE, ROLE_IDLE};
+    constexpr int kK[16] = {0, 0, 1, 0, 1, 1, NHELP + 0, 0, 2, 2, NHELP + 1, 1, 3, 3, 0, 0};
+    *rank = kK[w];
+    return kR[w];
+  }
   if ((w & 3) == 3) {
     if (w < 8) { *rank = w >> 2; return ROLE_CHAIN; }
     *rank = 0;
@@ -898,7 +922,7 @@ __device__ __forceinline__ void sched_body(const Pricer& pr, int nwork, int32_t*
   if (threadIdx.x == 0) S.prof = prof;
   __syncthreads();
   int rank = 0;
-  const int role = warp_role(threadIdx.x >> 5, &rank);
+  const int role = warp_role<LayoutOf<Pricer>::value>(threadIdx.x >> 5, &rank);
   if (role == ROLE_IDLE) return;
   if (role == ROLE_HELPER) {
     // ---- helper warp of chain rank / NHELP: correlations from the chain's
