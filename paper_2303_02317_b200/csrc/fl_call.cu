@@ -220,7 +220,7 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
 
 __device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                           int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_PROFP(X.prof));
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof));
 }
 
 // _solve (american.py:201-257) with an explicit stack on the chain warp.
@@ -335,6 +335,7 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
   const long long t_opt = clock64();
   const int64_t n = P.n;
   CallChainCtx X = call_chain_setup(S, c, P, n, n, arena, scratch, out.prof, out.acct != 0);
+  LCLK_ADD(out.prof, PROF_DEPWAIT_CYC, clock64() - t_opt);  // option setup (kernel table, e2 table)
   double* cur_org = arena;
   double* nxt_org = arena + (n + 8);
   int32_t err = 0, cnt = 0;
@@ -369,7 +370,9 @@ __device__ void call_chain_option(SchedShared& S, int c, const CallParams& P, in
       t.i0 = i; t.i1 = j; t.i2 = __double_as_longlong(P.K);
       t.h = 0; t.span = 0;
       const int id = issue(S, c, RING_BIG, t, U(cur_org), U(cur_org + j + 1), 0, 0);
+      const long long tr = clock64();
       warp_wait_done(S, id);
+      LCLK_ADD(out.prof, PROF_LEAF_LOAD, clock64() - tr);  // residual sweep wait
       const int64_t j0 = S.iresult[c];
       price = (j0 >= 0) ? S.result[c] : P.S - P.K;
       X.flops += 5ull * (uint64_t)S.result2[c];

@@ -21,7 +21,8 @@ print(f"n={n}: chain {ch:.3g} cycles/option; per option: strip loop {p[LOOP]/n:.
       f"walk rest {(p[FUSE]-p[STAGE]-p[HWAIT]-p[HPOST]-p[STRIP_CYC])/n:.3g}, "
       f"above subtrees {(p[CHAIN]-p[FUSE]-p[WAIT])/n:.3g}  ({p[FUSE_N]/n:.0f} subtrees)")
 print(f"  options re-priced on the full frame: {int(p[51])} of {n}")
-print(f"  above subtrees: option setup {p[17] / n:.3g}, jump issue (chain_conv) {p[15] / n:.3g} cycles/option")
+print(f"  above subtrees: option setup {p[17] / n:.3g}, jump issue (chain_conv) {p[15] / n:.3g}, "
+      f"residual wait (calls) {p[25] / n:.3g} cycles/option")
 for r, nm in enumerate(["small", "big", "low"]):
     q, sv, cnt, st = p[36 + 4 * r: 40 + 4 * r]
     if cnt:
