@@ -469,6 +469,12 @@ __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t r
     if (nd <= NDEP) break;
     warp_wait_done(S, deps[0]);  // too many: retire the oldest conflict first
   }
+#if FL_STRIP_CLOCK  // tool builds: issued tasks per ring and those with no dependency at issue
+  if (S.prof && lane_id() == 0) {
+    atomicAdd(S.prof + 48 + ring, 1ull);
+    if (nd == 0) atomicAdd(S.prof + 52 + ring, 1ull);
+  }
+#endif
   // keep the pending list from overflowing: wait for the entry about to be overwritten
   {
     const int np = S.npend[c];

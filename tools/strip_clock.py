@@ -28,3 +28,5 @@ for r, nm in enumerate(["small", "big", "low"]):
     if cnt:
         print(f"  ring {nm}: {cnt / n:.0f} tasks/option, queue {q / cnt:.0f} cycles, service {sv / cnt:.0f} cycles"
               + (f", {100 * st / cnt:.0f} % run by the big group" if r == 0 else ""))
+print("  issued per option by ring (small, big, low):", [round(p[48 + r] / n) for r in range(3)],
+      " with no dependency at issue:", [round(p[52 + r] / n) for r in range(3)])
