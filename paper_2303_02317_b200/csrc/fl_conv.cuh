@@ -191,24 +191,58 @@ __device__ __forceinline__ void dit_stage(double2* buf, int logC, int logS, cons
 // 9.9k -> 13.2k cycles, profiles/r01_experiments.md.)
 struct FftPlan {
   int n16;   // radix-16 stages
+  int n8;    // radix-8 stages after them (small transforms only, else 0)
   int last;  // log2 radix of the remainder stage (0: none, else 1..3)
 };
-__device__ __forceinline__ FftPlan fft_plan(int logC, int /*gn*/) {
+#ifndef FL_FFT_R8  // 1: transforms with fewer radix-16 butterflies than group threads use radix-8 stages
+#define FL_FFT_R8 1
+#endif
+#ifndef FL_FFT_R8_K
+#define FL_FFT_R8_K 16
+#endif
+// A radix-16 stage of C points has C/16 butterflies: below 2048 points a
+// 128-thread group runs them on one or two warps, i.e. on one or two SMSPs'
+// FP64 pipes while the others idle (a radix-16 butterfly is ~300 FP64
+// instructions).  Such transforms (the small ring's h = 256 / 512 jumps: 512
+// and 1024 complex points) run radix-8 stages instead (C/8 butterflies of ~120
+// instructions), then a radix-2 / 4 remainder.
+__device__ __forceinline__ FftPlan fft_plan(int logC, int gn) {
   FftPlan p;
+#if FL_FFT_R8
+  if (logC >= 6 && (FL_FFT_R8_K << logC) < (gn << 8)) {  // C / 16 < gn (K = 32: gn / 2, measured slower)
+    p.n16 = 0;
+    p.n8 = logC / 3;
+    p.last = logC - 3 * p.n8;
+    return p;
+  }
+#endif
+  p.n8 = 0;
   p.last = logC & 3;
   p.n16 = logC >> 2;
   return p;
 }
 
-// remainder stage: radix 2, 4 or 8 (the radix-16 stage has one call site per
-// direction: the instruction footprint counts)
+// remainder stage: radix 2, 4 or 8 (each radix has one call site per
+// direction: the instruction footprint counts); the radix-8 case also runs the
+// n8 main stages of a small transform, `n` stages with spans stepping by 8
 template <bool DIF>
 __device__ __forceinline__ void fft_stage_rem(double2* buf, int lr, int logC, int logS, const double2* tq,
-                                              const Grp& g) {
+                                              const Grp& g, int n = 1) {
   switch (lr) {
     case 1: DIF ? dif_stage<2>(buf, logC, logS, tq, g) : dit_stage<2>(buf, logC, logS, tq, g); break;
     case 2: DIF ? dif_stage<4>(buf, logC, logS, tq, g) : dit_stage<4>(buf, logC, logS, tq, g); break;
-    default: DIF ? dif_stage<8>(buf, logC, logS, tq, g) : dit_stage<8>(buf, logC, logS, tq, g); break;
+    default:
+#pragma unroll 1
+      for (int s = 0; s < n; ++s) {
+        if (DIF) {
+          dif_stage<8>(buf, logC, logS, tq, g);
+          logS -= 3;
+        } else {
+          dit_stage<8>(buf, logC, logS, tq, g);
+          logS += 3;
+        }
+      }
+      break;
   }
 }
 
@@ -220,13 +254,39 @@ __device__ __forceinline__ void fft_dif(double2* buf, int logC, const double2* t
     dif_stage<16>(buf, logC, logS, tq, g);
     logS -= 4;
   }
+#if FL_FFT_R8
+  // the radix-8 stages of a small transform, then the remainder (one call site)
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int lr = pass == 0 ? (pl.n8 ? 3 : 0) : pl.last;
+    const int n = pass == 0 ? pl.n8 : 1;
+    if (lr) {
+      fft_stage_rem<true>(buf, lr, logC, logS, tq, g, n);
+      logS -= lr * n;
+    }
+  }
+#else
   if (pl.last) fft_stage_rem<true>(buf, pl.last, logC, logS, tq, g);
+#endif
 }
 
 // Inverse (unnormalised, x C): slot P(k) in, natural order out.
 __device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* tq, Grp g, const FftPlan& pl) {
+#if !FL_FFT_R8
   int logS = pl.last;
   if (pl.last) fft_stage_rem<false>(buf, pl.last, logC, logS, tq, g);
+#else
+  int logS = 0;
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {  // remainder first, then the radix-8 stages (one call site)
+    const int lr = pass == 0 ? pl.last : (pl.n8 ? 3 : 0);
+    const int n = pass == 0 ? 1 : pl.n8;
+    if (lr) {
+      fft_stage_rem<false>(buf, lr, logC, logS + lr, tq, g, n);
+      logS += lr * n;
+    }
+  }
+#endif
 #pragma unroll 1
   for (int s = 0; s < pl.n16; ++s) {
     logS += 4;
@@ -234,10 +294,17 @@ __device__ __forceinline__ void fft_dit(double2* buf, int logC, const double2* t
   }
 }
 
-// Slot holding frequency k after fft_dif: the base-16 digits of k (the first
-// stage's digit least significant) in reverse order, then the remainder
-// digit: slot = nibble_reverse(k mod 16^n16) << last | k >> 4 n16.
+// Slot holding frequency k after fft_dif: k's digits in stage order (the first
+// stage's digit is the least significant of k) written most significant first,
+// each digit's bits in place, then the remainder digit:
+// slot = digit_reverse(k mod R^n) << last | k >> n log2 R  (R = 16 or 8).
 __device__ __forceinline__ int slot_of(int k, int logC, const FftPlan& pl) {
+  if (FL_FFT_R8 && pl.n8) {
+    const int lo = 3 * pl.n8;
+    unsigned x = __brev((unsigned)k & ((1u << lo) - 1u)) >> (32 - lo);  // bit-reversed: digits reversed, each inside out
+    x = (x & 0x92492492u) | ((x & 0x49249249u) << 2) | ((x >> 2) & 0x49249249u);
+    return (int)((x << pl.last) | ((unsigned)k >> lo));
+  }
   const int lo = 4 * pl.n16;
   unsigned x = __brev((unsigned)k & ((1u << lo) - 1u));  // bit-reversed, nibbles internally reversed
   x = ((x & 0x33333333u) << 2) | ((x >> 2) & 0x33333333u);
@@ -405,8 +472,8 @@ __device__ double conv_fft(const double* __restrict__ x, int64_t L, double* __re
         Xc = make_double2(Zk.x - Zk.y, 0.0);
       }
       // spectrum at omega_k = conj(Wk), omega_{C-k} = -Wk; window phase W^{k rlo}
-      const double2 Hk = spectrum(st, cconj(Wk), ph, h, pl.tau, inv_c);
       const double2 ph_c = cscale(cconj(ph), rlo_sign);
+      const double2 Hk = spectrum(st, cconj(Wk), ph, h, pl.tau, inv_c);
       const double2 Hc = spectrum(st, make_double2(-Wk.x, -Wk.y), ph_c, h, pl.tau, inv_c);
       const double2 Yk = cmul(Xk, Hk);
       const double2 Yc = cmul(Xc, Hc);

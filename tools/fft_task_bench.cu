@@ -93,6 +93,18 @@ int main() {
       for (int i = 0; i < q.ngrp; ++i) mx = fmax(mx, (double)hc[2 * i]);
       printf("Lout %5lld h %5d logNmax %2d  %3d thr x %d grp: %8.0f cycles/task, %8.0f cycles per task per SM-set  %s\n",
              (long long)k.Lout, k.h, k.logN, q.gsz, q.ngrp, mx / 20.0, mx / 20.0 / q.ngrp, cudaGetErrorString(e));
+      if (q.gsz == 128 && q.ngrp == 1) {  // sanity: against a direct long-double correlation
+        std::vector<double> hy(k.Lout);
+        cudaMemcpy(hy.data(), y, 8 * k.Lout, cudaMemcpyDeviceToHost);
+        const std::vector<double> w = weights(k.h);
+        double dev = 0.0;
+        for (int64_t o = 0; o < k.Lout; o += 37) {
+          long double a = 0.0L;
+          for (size_t r = 0; r < w.size(); ++r) a += (long double)w[r] * hx[o + r];
+          dev = fmax(dev, fabs((double)a - hy[o]));
+        }
+        printf("      max |y - direct| = %.3g\n", dev);
+      }
       long long ta[4][8];
       cudaMemcpyFromSymbol(ta, fl_tacc, sizeof(ta));
       cudaMemset(c, 0, 8);
