@@ -28,6 +28,9 @@ namespace fl {
 constexpr int CALL_LEAF = FL_CALL_LEAF;  // leaf strip height (<= 64: call_leaf_v4<CALL_LEAF / 32>)
 static_assert(CALL_LEAF == 32 || CALL_LEAF == 64 || CALL_LEAF == 128 || CALL_LEAF == 256,
               "leaf strips hold 32 * 2^k <= 256 columns");
+#ifndef FL_CALL_LOW_H  // as FL_LOW_H (fl_put.cu) for the call's jumps; measured slower (C2 +2.7 %), off
+#define FL_CALL_LOW_H 0
+#endif
 #ifndef FL_CALL_HS
 #define FL_CALL_HS 256
 #endif
@@ -220,7 +223,8 @@ __device__ int64_t call_subtree(CallChainCtx& X, const CallParams& P, int64_t i0
 
 __device__ __forceinline__ void call_conv(CallChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                           int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof));
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof),
+             FL_CALL_LOW_H > 0 && h >= FL_CALL_LOW_H);
 }
 
 // _solve (american.py:201-257) with an explicit stack on the chain warp.

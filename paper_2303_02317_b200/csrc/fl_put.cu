@@ -46,6 +46,9 @@ constexpr int PUT_SLIDE_CPL = (2 * PUT_LEAF + 2 + 30) / 31;  // cells per lane (
 constexpr int PUT_SLIDE_H = (31 * PUT_SLIDE_CPL - 2) / 2;      // tallest strip the frame holds
 template <int SL>
 __host__ __device__ constexpr int put_leaf_h() { return SL == 1 ? PUT_LEAF : PUT_LEAF_FULL; }
+#ifndef FL_LOW_H  // mid / bottom jumps of kernel height >= FL_LOW_H go to the chunked low-priority ring (0: none)
+#define FL_LOW_H 4096
+#endif
 #ifndef FL_PUT_HS
 #define FL_PUT_HS 256
 #endif
@@ -351,7 +354,11 @@ __device__ int64_t put_subtree(PutChainCtx& X, const PutParams& P, int64_t f0, c
 
 __device__ __forceinline__ void put_conv(PutChainCtx& X, const double* x, int64_t L, double* y, int64_t Lout,
                                          int h) {
-  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof));
+  // the jumps of tall nodes have slack to spare (a sibling subtree of their own
+  // height): chunked on the low-priority ring, a latency-critical short jump
+  // never queues behind a whole one
+  chain_conv(*X.S, X.c, X.st, x, L, y, Lout, h, X.kc, FL_STRIP_CLOCK ? X.prof : FL_PROFP(X.prof),
+             FL_LOW_H > 0 && h >= FL_LOW_H);
 }
 
 // _solve_q (bsm.py:443-501) as an explicit-stack loop on the chain warp.
