@@ -298,7 +298,8 @@ __device__ CallChainCtx call_chain_setup(SchedShared& S, int c, const CallParams
   double* frames = arena + 2 * (row_len + 8);
   const int64_t fstride = 2 * h_max + 16 * CALL_MAX_DEPTH;
   double* kc = frames + 2 * fstride;
-  const Stencil st{P.wd, P.wu, 0.0, 1};
+  Stencil st{P.wd, P.wu, 0.0, 1};
+  st.hsmall = small_ring_hmax(st);
   build_kernel_table(kc, st, scratch);
   __syncwarp();
   for (int k = lane_id(); k < CALL_TAB; k += 32) scratch[CALL_E2 + k] = exp(2.0 * (double)k * P.lu);  // call_leaf_v4

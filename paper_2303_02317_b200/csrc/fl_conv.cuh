@@ -319,6 +319,7 @@ __device__ __forceinline__ int slot_of(int k, int logC, const FftPlan& pl) {
 struct Stencil {
   double c0, c1, c2;  // P(z) = c0 + c1 z + c2 z^2 (c2 = 0 for two taps)
   int span;           // taps - 1
+  int hsmall = 0;     // chains: tallest kernel whose window fits the small ring (0: not set, see fft_ring)
 };
 
 struct ConvPlan {

@@ -453,7 +453,8 @@ __device__ PutChainCtx put_chain_setup(SchedShared& S, int c, const PutParams& P
   double* frames = arena + 3 * Lo.span;
   const int64_t fstride = 2 * n_rows + 64 * PUT_MAX_DEPTH;
   double* kc = frames + 2 * fstride;
-  const Stencil st{P.cd, P.cm, P.cu, 2};
+  Stencil st{P.cd, P.cm, P.cu, 2};
+  st.hsmall = small_ring_hmax(st);
   build_kernel_table(kc, st, scratch);
   PutChainCtx X{&S,   c,       st,  kc, frames, fstride, 0u, pay - Lo.colbase, scratch, chain_wstash(scratch),
                 (int64_t)P.cutoff, acct, 0ull, 0ull, prof};

@@ -530,10 +530,28 @@ __device__ void wait_all_own(SchedShared& S, int c) {
   for (int i = first; i < np; ++i) warp_wait_done(S, S.pend[c][i % PEND_CAP].id);
 }
 
-// Which ring an FFT correlation goes to (uniform per task).
+// Which ring an FFT correlation goes to (uniform per task): the small ring when
+// the kernel's Hoeffding window is at most FL_SMALL_MW columns.  The window
+// grows with h, so a chain evaluates the rule once per option as a height
+// threshold (small_ring_hmax into Stencil::hsmall: the window formula is a
+// double sqrt plus conversions, ~400 cycles of the chain's serial time per
+// issued jump otherwise).
 __device__ __forceinline__ int fft_ring(const Stencil& st, int h) {
+  if (st.hsmall > 0) return h <= st.hsmall ? RING_SMALL : RING_BIG;
   const int64_t Mw = window_width(st, h, nullptr);
   return (Mw <= FL_SMALL_MW) ? RING_SMALL : RING_BIG;
+}
+// Tallest kernel height sent to the small ring: bisection on the window width,
+// then a walk to the exact edge (floor / ceil make the width jitter by a column).
+__device__ __forceinline__ int small_ring_hmax(const Stencil& st) {
+  int lo = 1, hi = 1 << 14;  // the width at 2^14 is > 1200 for any stencil
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (window_width(st, mid, nullptr) <= FL_SMALL_MW) lo = mid; else hi = mid - 1;
+  }
+  while (window_width(st, lo + 1, nullptr) <= FL_SMALL_MW) ++lo;
+  while (lo > 1 && window_width(st, lo, nullptr) > FL_SMALL_MW) --lo;
+  return lo;
 }
 
 // ---------------------------------------------------------------------------
