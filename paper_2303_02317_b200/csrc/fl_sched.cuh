@@ -462,6 +462,12 @@ __device__ void wait_conflicts(SchedShared& S, int c, uintptr_t r0, uintptr_t r1
 
 // Issue a task from chain warp `c` (all 32 lanes call).  Returns its id.
 // rlo/rhi: read range; wlo/whi: write range.
+#ifndef FL_ISSUE_CALL  // 1: issue() is a real call, 2: chain_conv() is (one copy of the code instead of 11)
+#define FL_ISSUE_CALL 1
+#endif
+#if FL_ISSUE_CALL == 1
+__noinline__
+#endif
 __device__ int issue(SchedShared& S, int c, int ring, const Task& t, uintptr_t rlo, uintptr_t rhi, uintptr_t wlo,
                      uintptr_t whi) {
   int* deps = S.cw_deps[c];
@@ -775,11 +781,19 @@ __device__ __forceinline__ void warp_stage(double* dst, const double* src, int n
   warp_stage_nb<8>(dst, src, n, n_total);
 }
 
+#ifndef FL_STAGE_UNROLL
+#define FL_STAGE_UNROLL 1
+#endif
+constexpr int kStageUnroll = FL_STAGE_UNROLL;
 // Asynchronous warp_stage: 8-byte cp.async copies global -> shared (zero-fill
 // from n to n_total), no register staging and every copy in flight at once.
 // The data may be read only after warp_stage_wait().
 __device__ __forceinline__ void warp_stage_async(double* dst, const double* src, int n, int n_total = -1) {
   if (n_total < n) n_total = n;
+  // not unrolled: the callers' lengths are compile-time constants, and a fully
+  // unrolled copy (33 iterations at a 256-row subtree) is ~40 KB of straight-line
+  // code in the persistent kernel (instruction-cache footprint)
+#pragma unroll kStageUnroll
   for (int i = lane_id(); i < n_total; i += 32) {
     const unsigned da = (unsigned)__cvta_generic_to_shared(dst + i);
     const int sz = (i < n) ? 8 : 0;
@@ -794,6 +808,9 @@ __device__ __forceinline__ void warp_stage_wait() {
 
 // A linear jump issued by chain c: a direct-dot-product task (h <= DIRECT_H)
 // or an FFT task, on the small or big ring.
+#if FL_ISSUE_CALL == 2
+__noinline__
+#endif
 __device__ void chain_conv(SchedShared& S, int c, const Stencil& st, const double* x, int64_t L, double* y,
                            int64_t Lout, int h, const double* kc, unsigned long long* prof, bool low = false) {
   if (Lout <= 0) return;
