@@ -18,6 +18,12 @@
 
 namespace {
 
+// mixed batches: chain slots of a B200 (148 SMs x 2 chains) and the fill ratio
+// (a kind's summed cost / (slots x its largest cost)) from which the two kinds run
+// as two kernels instead of one mixed kernel
+constexpr double kChainSlots = 2.0 * 148.0;
+constexpr double kSplitFill = 1.1;
+
 thread_local std::string g_last_error;
 
 int fail(const std::string& msg) {
@@ -274,7 +280,23 @@ int plan_host(fl_batch* b, int64_t n, const int8_t* kind, const double* S, const
   sort_by_cost(b->o_put_fast, b->cost);
   sort_by_cost(b->o_call_fast, b->cost);
   b->o_mixed.clear();
-  if (!b->o_put_fast.empty() && !b->o_call_fast.empty()) {  // one kernel, one cost-ordered queue
+  // Both kinds present: one kernel over one cost-ordered queue (the kinds share
+  // every SM) -- unless each kind alone keeps every chain slot of the GPU busy for
+  // longer than its longest option (cost model): then each kind runs on its own,
+  // smaller kernel (its own warp layout, register allocation and instruction
+  // footprint) back to back, the tail of the first being a few short options.
+  // Measured on C5 mixes: break-even at a fill ratio of 0.9 (3072 options), 12 %
+  // faster at 1.18 (4096), 8.6 % at 18.5 (65 536); far slower below 0.6
+  // (profiles/r02_experiments.md).  FL_SPLIT_KINDS=0 / 1 forces either dispatch.
+  auto fill = [&](const std::vector<int32_t>& ord) {
+    double sum = 0.0, mx = 0.0;
+    for (int32_t e : ord) { sum += b->cost[e]; mx = std::max(mx, b->cost[e]); }
+    return mx > 0.0 ? sum / (kChainSlots * mx) : 0.0;
+  };
+  const char* split_env = std::getenv("FL_SPLIT_KINDS");
+  const bool split = split_env ? split_env[0] == '1'
+                               : (fill(b->o_put_fast) >= kSplitFill && fill(b->o_call_fast) >= kSplitFill);
+  if (!b->o_put_fast.empty() && !b->o_call_fast.empty() && !split) {
     std::merge(b->o_put_fast.begin(), b->o_put_fast.end(), b->o_call_fast.begin(), b->o_call_fast.end(),
                std::back_inserter(b->o_mixed), [&](int32_t a, int32_t c) { return b->cost[a] > b->cost[c]; });
     for (int32_t& e : b->o_mixed)
