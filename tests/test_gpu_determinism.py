@@ -8,6 +8,7 @@ this is checked, not argued: the same options are priced
 * inside the 256-option headline batch,
 * inside a C5-style mix of all three kinds and every T,
 * inside each LPT shard of a 4-way split of that mix (shard.lpt_shards),
+* through both dispatches of a mixed batch (one mixed kernel / put then call kernel),
 * and through the multi-device entry on the one visible device,
 
 and every result must be identical to the bit."""
@@ -83,6 +84,31 @@ def test_mix_and_lpt_shards():
     res = _price(*both)
     for j in range(len(idx)):
         assert _same(whole, j, res, 64 + j), j
+
+
+def test_mixed_batch_dispatch_is_bit_identical(monkeypatch):
+    """A mixed put / call batch runs either in the one mixed kernel or as the put
+    kernel then the call kernel (fl_abi.cu picks by the per-kind fill ratio;
+    FL_SPLIT_KINDS forces either): both dispatches give the same bits, and both
+    match the golden prices."""
+    from conftest import price_close
+
+    g5 = golden("c5_fast")
+    rng = np.random.default_rng(55)
+    idx = rng.permutation(g5.n)[:400]
+    f = _fields(g5, idx)
+    assert (f[0] == 1).any() and (f[0] == 2).any()
+    monkeypatch.setenv("FL_SPLIT_KINDS", "0")
+    mixed = _price(*f)
+    monkeypatch.setenv("FL_SPLIT_KINDS", "1")
+    split = _price(*f)
+    monkeypatch.delenv("FL_SPLIT_KINDS")
+    auto = _price(*f)
+    for j, i in enumerate(idx):
+        assert _same(mixed, j, split, j), int(i)
+        assert _same(mixed, j, auto, j), int(i)
+        if np.isfinite(g5.price[i]):
+            assert price_close(split.price[j], g5.price[i], g5.K[i]), int(i)
 
 
 def test_multi_device_entry_matches_single():
